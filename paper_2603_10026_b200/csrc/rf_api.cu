@@ -1,0 +1,486 @@
+// librf_cuda C-ABI: plan layer (descriptor validation, kernel + tile choice,
+// workspace), stream-ordered dispatch, host-buffer end-to-end path.
+//
+// Reference interface replaced (see include/rf_cuda.h): run_incremental /
+// run_multisegment (proj/include/redfuse/simulator.hpp:76-82). Error mapping
+// mirrors the reference's exceptions: ShapeMismatch (check_shapes,
+// proj/src/simulator.cpp:235-245), IncompatibleSegmentation
+// (simulator.cpp:668-671), DomainError at finalize (simulator.cpp:611-621).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "rf_internal.h"
+
+namespace rf {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+}  // namespace rf
+
+using rf::set_error;
+
+struct rf_plan {
+  rf_desc d{};
+  rf::Kernel kernel = rf::Kernel::SoftmaxRows;
+  int64_t rows_total = 0;   // B*H*Sq (attention) / M (GEMM) / rows (softmax)
+  int64_t nsplit = 1;       // slices actually launched (>= segments for decode)
+  int64_t launches = 1;
+  // Segment partial workspace (attention, nsplit > 1).
+  float* ws_m = nullptr;
+  float* ws_l = nullptr;
+  float* ws_o = nullptr;
+  int* domain_flag = nullptr;
+  // Host-path staging (rf_run_host), allocated on first use.
+  bool staged = false;
+  void* dev_in[4] = {nullptr, nullptr, nullptr, nullptr};
+  void* dev_out[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t streams[2] = {nullptr, nullptr};
+  std::string describe;
+};
+
+namespace {
+
+size_t dtype_size(int dt) { return dt == RF_F32 ? 4 : dt == RF_BF16 ? 2 : 1; }
+
+rf_status fail(rf_status s, const std::string& msg) {
+  set_error(msg);
+  return s;
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Input/output byte sizes per pattern, for the host path and shape checks.
+void io_sizes(const rf_plan* p, size_t in[4], size_t out[3]) {
+  const rf_desc& d = p->d;
+  for (int i = 0; i < 4; ++i) in[i] = 0;
+  for (int i = 0; i < 3; ++i) out[i] = 0;
+  const size_t es = dtype_size(d.dtype);
+  switch (d.pattern) {
+    case RF_PATTERN_SAFE_SOFTMAX:
+      in[0] = sizeof(float) * d.rows * d.len;
+      out[0] = out[1] = sizeof(float) * d.rows;
+      break;
+    case RF_PATTERN_ATTENTION: {
+      const int64_t bh = d.batch * d.heads;
+      in[0] = es * bh * d.rows * d.free_len;
+      in[1] = in[2] = es * bh * d.len * d.free_len;
+      out[0] = out[1] = sizeof(float) * bh * d.rows;
+      out[2] = es * bh * d.rows * d.free_len;
+      break;
+    }
+    case RF_PATTERN_QUANT_GEMM_E4M3:
+      in[0] = 2 * d.rows * d.len;
+      out[0] = sizeof(float) * d.rows;
+      out[1] = sizeof(float) * d.rows * d.free_len;
+      break;
+    case RF_PATTERN_RMSNORM_GEMM:
+      in[0] = 2 * d.rows * d.len;
+      out[0] = sizeof(float) * d.rows;
+      out[1] = 2 * d.rows * d.free_len;
+      break;
+  }
+}
+
+const char* kernel_name(rf::Kernel k) {
+  switch (k) {
+    case rf::Kernel::SoftmaxRows: return "softmax_rows (SIMT, single pass)";
+    case rf::Kernel::AttentionF32: return "attention_f32 (SIMT, paper form)";
+    case rf::Kernel::AttentionSm100: return "attention_sm100 (bf16 tcgen05/TMEM/TMA)";
+    case rf::Kernel::AttentionDecode: return "attention_decode (bf16 split-KV, TMA bulk)";
+    case rf::Kernel::QuantGemmSm100: return "quant_gemm_sm100 (e4m3 tcgen05 kind::f8f6f4)";
+    case rf::Kernel::RmsGemmSm100: return "rmsnorm_gemm_sm100 (bf16 tcgen05 kind::f16)";
+  }
+  return "?";
+}
+
+// Decode split count: a multiple of `segments` dividing Skv with slices of at
+// least 512 keys, aiming at >= 4 CTAs per SM worth of (row, slice) units.
+int64_t pick_decode_splits(int64_t rows, int64_t skv, int64_t segments) {
+  int64_t best = segments;
+  for (int64_t s = segments; s <= skv; s += segments) {
+    if (skv % s) continue;
+    if (skv / s < 512 && s != segments) break;
+    best = s;
+    if (rows * s >= 148 * 4) break;
+  }
+  return best;
+}
+
+rf_status attention_run(const rf_plan* p, const rf_io* io, int64_t bh0, int64_t nbh,
+                        cudaStream_t st) {
+  const rf_desc& d = p->d;
+  const size_t es = dtype_size(d.dtype);
+  const int64_t q_off = bh0 * d.rows * d.free_len, kv_off = bh0 * d.len * d.free_len;
+  rf::AttnArgs a{};
+  a.q = static_cast<const char*>(io->in[0]) + q_off * es;
+  a.k = static_cast<const char*>(io->in[1]) + kv_off * es;
+  a.v = static_cast<const char*>(io->in[2]) + kv_off * es;
+  a.o = static_cast<char*>(io->d[2]) + q_off * es;
+  a.m = static_cast<float*>(io->d[0]) + bh0 * d.rows;
+  a.l = static_cast<float*>(io->d[1]) + bh0 * d.rows;
+  a.bh = nbh;
+  a.sq = d.rows;
+  a.skv = d.len;
+  a.d = d.free_len;
+  a.segments = p->nsplit;
+  a.slice_begin = 0;
+  a.nslices = p->nsplit;
+  a.part_base = 0;
+  a.rows_total = p->rows_total;
+  a.scale = static_cast<float>(d.softmax_scale);
+  a.dtype = d.dtype;
+  if (p->nsplit > 1) {
+    a.part_m = p->ws_m + bh0 * d.rows;
+    a.part_l = p->ws_l + bh0 * d.rows;
+    a.part_o = p->ws_o + bh0 * d.rows * d.free_len;
+  }
+  cudaError_t e;
+  switch (p->kernel) {
+    case rf::Kernel::AttentionSm100: e = rf::launch_attention_sm100(a, st); break;
+    case rf::Kernel::AttentionDecode: e = rf::launch_attention_decode(a, st); break;
+    default: e = rf::launch_attention_f32(a, st); break;
+  }
+  if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
+  if (p->nsplit > 1) {
+    e = rf::launch_attention_merge(a.part_m, a.part_l, a.part_o, p->nsplit, nbh * d.rows,
+                                   p->rows_total, d.free_len, a.m, a.l, a.o, d.dtype, st);
+    if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("merge launch: ") + cudaGetErrorString(e));
+  }
+  return RF_OK;
+}
+
+rf_status gemm_run(const rf_plan* p, const rf_io* io, int64_t m0, int64_t nm, cudaStream_t st) {
+  const rf_desc& d = p->d;
+  rf::GemmArgs g{};
+  g.a = static_cast<const char*>(io->in[0]) + 2 * m0 * d.len;
+  g.b = io->in[1];
+  g.d1 = static_cast<float*>(io->d[0]) + m0;
+  const size_t cs = d.pattern == RF_PATTERN_QUANT_GEMM_E4M3 ? 4 : 2;
+  g.c = static_cast<char*>(io->d[1]) + cs * m0 * d.free_len;
+  g.domain_flag = p->domain_flag;
+  g.m = nm;
+  g.n = d.free_len;
+  g.k = d.len;
+  g.fmax = static_cast<float>(d.fmax);
+  g.eps = static_cast<float>(d.eps);
+  cudaError_t e = d.pattern == RF_PATTERN_QUANT_GEMM_E4M3 ? rf::launch_quant_gemm_sm100(g, st)
+                                                          : rf::launch_rms_gemm_sm100(g, st);
+  if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
+  return RF_OK;
+}
+
+rf_status run_range(const rf_plan* p, const rf_io* io, int64_t u0, int64_t nu, cudaStream_t st) {
+  switch (p->d.pattern) {
+    case RF_PATTERN_SAFE_SOFTMAX: {
+      cudaError_t e = rf::launch_softmax_rows(
+          static_cast<const float*>(io->in[0]) + u0 * p->d.len, nu, p->d.len,
+          static_cast<float*>(io->d[0]) + u0, static_cast<float*>(io->d[1]) + u0, st);
+      if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("softmax launch: ") + cudaGetErrorString(e));
+      return RF_OK;
+    }
+    case RF_PATTERN_ATTENTION: return attention_run(p, io, u0, nu, st);
+    default: return gemm_run(p, io, u0, nu, st);
+  }
+}
+
+// Independent units for chunking: (b,h) pairs for attention, rows otherwise.
+int64_t units_of(const rf_plan* p) {
+  return p->d.pattern == RF_PATTERN_ATTENTION ? p->d.batch * p->d.heads : p->d.rows;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rf_abi_version(void) { return RF_CUDA_ABI_VERSION; }
+
+const char* rf_status_string(rf_status s) {
+  switch (s) {
+    case RF_OK: return "RF_OK";
+    case RF_ERR_SHAPE: return "RF_ERR_SHAPE (ShapeMismatch)";
+    case RF_ERR_SEGMENTATION: return "RF_ERR_SEGMENTATION (IncompatibleSegmentation)";
+    case RF_ERR_DOMAIN: return "RF_ERR_DOMAIN (DomainError)";
+    case RF_ERR_UNSUPPORTED: return "RF_ERR_UNSUPPORTED";
+    case RF_ERR_CUDA: return "RF_ERR_CUDA";
+    case RF_ERR_NCCL: return "RF_ERR_NCCL";
+    case RF_ERR_ARG: return "RF_ERR_ARG";
+  }
+  return "RF_ERR_UNKNOWN";
+}
+
+const char* rf_last_error(void) { return rf::g_last_error.c_str(); }
+
+rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
+  if (!desc || !out) return fail(RF_ERR_ARG, "null desc/out");
+  *out = nullptr;
+  const rf_desc& d = *desc;
+  // ---- shape validation (check_shapes, simulator.cpp:235-245) ----
+  if (d.rows < 0 || d.len < 1 || d.free_len < 0 || d.batch < 1 || d.heads < 1)
+    return fail(RF_ERR_SHAPE, "non-positive extent in descriptor");
+  if (d.segments < 1 || d.len % d.segments != 0)  // simulator.cpp:668-671
+    return fail(RF_ERR_SEGMENTATION, std::to_string(d.segments) +
+                                         " segments do not divide L0 = " + std::to_string(d.len));
+  rf_plan* p = new (std::nothrow) rf_plan();
+  if (!p) return fail(RF_ERR_CUDA, "out of host memory");
+  p->d = d;
+  if (p->d.softmax_scale == 0.0) p->d.softmax_scale = 1.0;
+  if (p->d.fmax == 0.0) p->d.fmax = 448.0;
+  auto bail = [&](rf_status s, const std::string& m) {
+    rf_plan_destroy(p);
+    return fail(s, m);
+  };
+
+  // ---- device: sm_100 only (no fallback) ----
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return bail(RF_ERR_CUDA, "no CUDA device (librf_cuda has no CPU fallback)");
+  if (d.device < 0 || d.device >= ndev) return bail(RF_ERR_ARG, "bad device ordinal");
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, d.device) != cudaSuccess)
+    return bail(RF_ERR_CUDA, "cudaGetDeviceProperties failed");
+  if (prop.major != 10 || prop.minor != 0)
+    return bail(RF_ERR_CUDA, "librf_cuda is built for sm_100a only; device is sm_" +
+                                 std::to_string(prop.major) + std::to_string(prop.minor));
+  int prev_dev = 0;
+  cudaGetDevice(&prev_dev);
+  cudaSetDevice(d.device);
+
+  // ---- kernel choice ----
+  switch (d.pattern) {
+    case RF_PATTERN_SAFE_SOFTMAX:
+      if (d.dtype != RF_F32) return bail(RF_ERR_UNSUPPORTED, "safe_softmax: f32 input only");
+      p->kernel = rf::Kernel::SoftmaxRows;
+      p->rows_total = d.rows;
+      if (d.segments != 1) p->nsplit = 1;  // single pass; segment merges are in-CTA
+      break;
+    case RF_PATTERN_ATTENTION:
+      if (d.dtype != RF_F32 && d.dtype != RF_BF16)
+        return bail(RF_ERR_UNSUPPORTED, "attention: f32 or bf16 inputs");
+      if (d.free_len != 16 && d.free_len != 32 && d.free_len != 64 && d.free_len != 128)
+        return bail(RF_ERR_UNSUPPORTED, "attention: head_dim must be 16/32/64/128");
+      p->rows_total = d.batch * d.heads * d.rows;
+      p->nsplit = d.segments;
+      if (d.dtype == RF_F32) {
+        p->kernel = rf::Kernel::AttentionF32;
+      } else if (d.rows == 1) {
+        p->kernel = rf::Kernel::AttentionDecode;
+        p->nsplit = pick_decode_splits(d.batch * d.heads, d.len, d.segments);
+      } else if (rf::attention_sm100_supports(d.rows, d.len, d.free_len, d.segments)) {
+        p->kernel = rf::Kernel::AttentionSm100;
+      } else {
+        p->kernel = rf::Kernel::AttentionF32;  // SIMT CUDA path for odd shapes
+      }
+      break;
+    case RF_PATTERN_QUANT_GEMM_E4M3:
+    case RF_PATTERN_RMSNORM_GEMM:
+      if (d.dtype != RF_BF16) return bail(RF_ERR_UNSUPPORTED, "GEMM patterns take bf16 activations");
+      if (d.segments != 1)
+        return bail(RF_ERR_UNSUPPORTED, "GEMM patterns: single-segment (run_incremental) only");
+      if (!rf::gemm_sm100_supports(d.pattern, d.rows, d.free_len, d.len))
+        return bail(RF_ERR_UNSUPPORTED, "GEMM shape has no tcgen05 tiling (need M%128, N%256, K%128)");
+      p->kernel = d.pattern == RF_PATTERN_QUANT_GEMM_E4M3 ? rf::Kernel::QuantGemmSm100
+                                                          : rf::Kernel::RmsGemmSm100;
+      p->rows_total = d.rows;
+      break;
+    default:
+      return bail(RF_ERR_UNSUPPORTED, "unknown pattern");
+  }
+  p->launches = (p->d.pattern == RF_PATTERN_ATTENTION && p->nsplit > 1) ? 2 : 1;
+
+  // ---- persistent workspace ----
+  if (cudaMalloc(&p->domain_flag, sizeof(int)) != cudaSuccess ||
+      cudaMemset(p->domain_flag, 0, sizeof(int)) != cudaSuccess)
+    return bail(RF_ERR_CUDA, "workspace allocation failed");
+  if (p->d.pattern == RF_PATTERN_ATTENTION && p->nsplit > 1) {
+    const size_t n = static_cast<size_t>(p->nsplit) * p->rows_total;
+    if (cudaMalloc(&p->ws_m, n * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&p->ws_l, n * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&p->ws_o, n * d.free_len * sizeof(float)) != cudaSuccess)
+      return bail(RF_ERR_CUDA, "segment workspace allocation failed");
+  }
+  char buf[512];
+  std::snprintf(buf, sizeof buf,
+                "{\"kernel\": \"%s\", \"pattern\": %d, \"dtype\": %d, \"rows_total\": %lld, "
+                "\"L0\": %lld, \"free\": %lld, \"segments\": %lld, \"slices_launched\": %lld, "
+                "\"launches_per_run\": %lld, \"device\": \"%s\"}",
+                kernel_name(p->kernel), d.pattern, d.dtype, (long long)p->rows_total,
+                (long long)d.len, (long long)d.free_len, (long long)d.segments,
+                (long long)p->nsplit, (long long)p->launches, prop.name);
+  p->describe = buf;
+  cudaSetDevice(prev_dev);
+  *out = p;
+  return RF_OK;
+}
+
+void rf_plan_destroy(rf_plan* p) {
+  if (!p) return;
+  cudaFree(p->ws_m);
+  cudaFree(p->ws_l);
+  cudaFree(p->ws_o);
+  cudaFree(p->domain_flag);
+  for (void* b : p->dev_in) cudaFree(b);
+  for (void* b : p->dev_out) cudaFree(b);
+  for (cudaStream_t s : p->streams)
+    if (s) cudaStreamDestroy(s);
+  delete p;
+}
+
+rf_status rf_plan_describe(const rf_plan* p, char* buf, size_t n) {
+  if (!p || !buf || n == 0) return fail(RF_ERR_ARG, "null plan/buffer");
+  std::snprintf(buf, n, "%s", p->describe.c_str());
+  return p->describe.size() < n ? RF_OK : fail(RF_ERR_ARG, "buffer too small");
+}
+
+int64_t rf_plan_launches_per_run(const rf_plan* p) { return p ? p->launches : 0; }
+
+rf_status rf_pack_weight(const rf_plan* p, const void* w, const void* g, void* packed,
+                         void* stream) {
+  if (!p || !w || !packed) return fail(RF_ERR_ARG, "null plan/w/packed");
+  cudaError_t e;
+  if (p->d.pattern == RF_PATTERN_QUANT_GEMM_E4M3) {
+    e = rf::launch_pack_e4m3(static_cast<const float*>(w), p->d.len, p->d.free_len,
+                             static_cast<uint8_t*>(packed), as_stream(stream));
+  } else if (p->d.pattern == RF_PATTERN_RMSNORM_GEMM) {
+    if (!g) return fail(RF_ERR_ARG, "rmsnorm pack needs g");
+    e = rf::launch_pack_rms(static_cast<const float*>(w), static_cast<const float*>(g), p->d.len,
+                            p->d.free_len, packed, as_stream(stream));
+  } else {
+    return fail(RF_ERR_UNSUPPORTED, "pattern has no packed weight");
+  }
+  if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("pack: ") + cudaGetErrorString(e));
+  return RF_OK;
+}
+
+rf_status rf_run(const rf_plan* p, const rf_io* io, void* stream) {
+  if (!p || !io) return fail(RF_ERR_ARG, "null plan/io");
+  size_t in[4], out[3];
+  io_sizes(p, in, out);
+  for (int i = 0; i < 4; ++i)
+    if (in[i] && !io->in[i]) return fail(RF_ERR_SHAPE, "missing input " + std::to_string(i));
+  for (int i = 0; i < 3; ++i)
+    if (out[i] && !io->d[i]) return fail(RF_ERR_SHAPE, "missing output d" + std::to_string(i + 1));
+  if ((p->d.pattern == RF_PATTERN_QUANT_GEMM_E4M3 || p->d.pattern == RF_PATTERN_RMSNORM_GEMM) &&
+      !io->in[1])
+    return fail(RF_ERR_SHAPE, "missing packed weight in[1]");
+  if (units_of(p) == 0 || p->d.rows == 0) return RF_OK;  // empty batch
+  return run_range(p, io, 0, units_of(p), as_stream(stream));
+}
+
+rf_status rf_run_host(rf_plan* p, const rf_host_io* io) {
+  if (!p || !io) return fail(RF_ERR_ARG, "null plan/io");
+  size_t in[4], out[3];
+  io_sizes(p, in, out);
+  const bool gemm =
+      p->d.pattern == RF_PATTERN_QUANT_GEMM_E4M3 || p->d.pattern == RF_PATTERN_RMSNORM_GEMM;
+  int prev_dev = 0;
+  cudaGetDevice(&prev_dev);
+  RF_CUDA_TRY(cudaSetDevice(p->d.device));
+  if (!p->staged) {
+    for (int i = 0; i < 4; ++i)
+      if (in[i]) RF_CUDA_TRY(cudaMalloc(&p->dev_in[i], in[i]));
+    for (int i = 0; i < 3; ++i)
+      if (out[i]) RF_CUDA_TRY(cudaMalloc(&p->dev_out[i], out[i]));
+    for (auto& s : p->streams) RF_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    p->staged = true;
+  }
+  rf_io dio{};
+  for (int i = 0; i < 4; ++i) dio.in[i] = p->dev_in[i];
+  for (int i = 0; i < 3; ++i) dio.d[i] = p->dev_out[i];
+  if (gemm) dio.in[1] = io->in[1];  // packed weight: plan-time resident device buffer
+  const int64_t units = units_of(p);
+  // Chunking: 8 chunks over independent units, alternating two streams, so
+  // the H2D of chunk c+1 and the D2H of chunk c-1 overlap chunk c's kernels.
+  const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(8, units));
+  const int64_t per = (units + nchunk - 1) / nchunk;
+  for (int64_t c = 0; c < nchunk; ++c) {
+    const int64_t u0 = c * per, nu = std::min(per, units - u0);
+    if (nu <= 0) break;
+    cudaStream_t st = p->streams[c & 1];
+    for (int i = 0; i < 4; ++i) {
+      if (!in[i] || (gemm && i == 1)) continue;
+      const size_t chunk = in[i] / units * nu, off = in[i] / units * u0;
+      RF_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(p->dev_in[i]) + off,
+                                  static_cast<const char*>(io->in[i]) + off, chunk,
+                                  cudaMemcpyHostToDevice, st));
+    }
+    rf_status s = run_range(p, &dio, u0, nu, st);
+    if (s != RF_OK) return s;
+    for (int i = 0; i < 3; ++i) {
+      if (!out[i] || !io->d[i]) continue;
+      const size_t chunk = out[i] / units * nu, off = out[i] / units * u0;
+      RF_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(io->d[i]) + off,
+                                  static_cast<char*>(p->dev_out[i]) + off, chunk,
+                                  cudaMemcpyDeviceToHost, st));
+    }
+  }
+  RF_CUDA_TRY(cudaStreamSynchronize(p->streams[0]));
+  RF_CUDA_TRY(cudaStreamSynchronize(p->streams[1]));
+  cudaSetDevice(prev_dev);
+  return RF_OK;
+}
+
+rf_status rf_run_partials(const rf_plan* p, const rf_io* io, int64_t slice_begin,
+                          rf_partials* outp, void* stream) {
+  if (!p || !io || !outp) return fail(RF_ERR_ARG, "null argument");
+  if (p->d.pattern != RF_PATTERN_ATTENTION) return fail(RF_ERR_UNSUPPORTED, "partials: attention only");
+  if (slice_begin < 0 || outp->nslices < 1 || slice_begin + outp->nslices > p->d.segments)
+    return fail(RF_ERR_SEGMENTATION, "slice range outside the plan's segments");
+  const rf_desc& d = p->d;
+  rf::AttnArgs a{};
+  a.q = io->in[0];
+  a.k = io->in[1];
+  a.v = io->in[2];
+  a.bh = d.batch * d.heads;
+  a.sq = d.rows;
+  a.skv = d.len;
+  a.d = d.free_len;
+  a.segments = d.segments;
+  a.slice_begin = slice_begin;
+  a.nslices = outp->nslices;
+  a.part_base = slice_begin;
+  a.rows_total = p->rows_total;
+  a.part_m = outp->m;
+  a.part_l = outp->l;
+  a.part_o = outp->o;
+  a.scale = static_cast<float>(d.softmax_scale);
+  a.dtype = d.dtype;
+  cudaError_t e;
+  switch (p->kernel) {
+    case rf::Kernel::AttentionSm100: e = rf::launch_attention_sm100(a, as_stream(stream)); break;
+    case rf::Kernel::AttentionDecode: e = rf::launch_attention_decode(a, as_stream(stream)); break;
+    default: e = rf::launch_attention_f32(a, as_stream(stream)); break;
+  }
+  if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("partials: ") + cudaGetErrorString(e));
+  return RF_OK;
+}
+
+rf_status rf_merge_partials(const rf_plan* p, const rf_partials* in, const rf_io* io,
+                            void* stream) {
+  if (!p || !in || !io) return fail(RF_ERR_ARG, "null argument");
+  if (p->d.pattern != RF_PATTERN_ATTENTION) return fail(RF_ERR_UNSUPPORTED, "merge: attention only");
+  cudaError_t e = rf::launch_attention_merge(in->m, in->l, in->o, in->nslices, p->rows_total,
+                                             p->rows_total, p->d.free_len,
+                                             static_cast<float*>(io->d[0]),
+                                             static_cast<float*>(io->d[1]), io->d[2], p->d.dtype,
+                                             as_stream(stream));
+  if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("merge: ") + cudaGetErrorString(e));
+  return RF_OK;
+}
+
+rf_status rf_check_domain(const rf_plan* p, void* stream) {
+  if (!p) return fail(RF_ERR_ARG, "null plan");
+  int flag = 0;
+  RF_CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
+  RF_CUDA_TRY(cudaMemcpy(&flag, p->domain_flag, sizeof(int), cudaMemcpyDeviceToHost));
+  RF_CUDA_TRY(cudaMemset(p->domain_flag, 0, sizeof(int)));
+  if (flag) return fail(RF_ERR_DOMAIN, "division by zero at finalize (a row's absmax is 0)");
+  return RF_OK;
+}
+
+}  // extern "C"

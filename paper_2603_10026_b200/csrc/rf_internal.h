@@ -1,0 +1,92 @@
+// Internal declarations shared by the librf_cuda translation units.
+// Not part of the ABI (see include/rf_cuda.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "rf_cuda.h"
+
+namespace rf {
+
+// Thread-local last-error text (rf_last_error).
+void set_error(const std::string& msg);
+
+#define RF_CUDA_TRY(expr)                                                   \
+  do {                                                                      \
+    cudaError_t err__ = (expr);                                             \
+    if (err__ != cudaSuccess) {                                             \
+      ::rf::set_error(std::string(#expr) + ": " + cudaGetErrorString(err__)); \
+      return RF_ERR_CUDA;                                                   \
+    }                                                                       \
+  } while (0)
+
+enum class Kernel {
+  SoftmaxRows,        // softmax.cu
+  AttentionF32,       // attn_f32.cu   (SIMT, paper form, cfg1)
+  AttentionSm100,     // attn_sm100.cu (bf16 tcgen05/TMEM/TMA prefill, cfg2)
+  AttentionDecode,    // attn_decode.cu (bf16 split-KV streaming, cfg3)
+  QuantGemmSm100,     // gemm_sm100.cu (e4m3 kind::f8f6f4, cfg4)
+  RmsGemmSm100,       // gemm_sm100.cu (bf16 kind::f16, cfg5)
+};
+
+// ---- kernel launchers (stream-ordered; return cudaGetLastError()) ----------
+
+// Safe softmax over rows (single pass, Eq.17 per element + Eq.16 merges).
+cudaError_t launch_softmax_rows(const float* x, int64_t rows, int64_t n, float* d1,
+                                float* d2, cudaStream_t st);
+
+// fp32 attention, paper form. Slices [slice_begin, slice_begin+nslices) of a
+// `segments`-way split of Skv. If part_* are null (segments == 1) the final
+// O/m/l are written, else partials at slice index (s - part_base).
+struct AttnArgs {
+  const void* q;
+  const void* k;
+  const void* v;
+  void* o;
+  float* m;
+  float* l;
+  float* part_m;
+  float* part_l;
+  float* part_o;
+  int64_t bh, sq, skv, d;
+  int64_t segments, slice_begin, nslices, part_base;
+  int64_t rows_total;  // bh * sq (stride of the partial buffers)
+  float scale;
+  int dtype;
+};
+cudaError_t launch_attention_f32(const AttnArgs& a, cudaStream_t st);
+cudaError_t launch_attention_decode(const AttnArgs& a, cudaStream_t st);
+// Returns cudaErrorNotSupported when the shape has no tcgen05 instantiation.
+cudaError_t launch_attention_sm100(const AttnArgs& a, cudaStream_t st);
+bool attention_sm100_supports(int64_t sq, int64_t skv, int64_t d, int64_t segments);
+
+// Slice-ordered fold of partial (m, l, O) states (incr_push_child).
+cudaError_t launch_attention_merge(const float* pm, const float* pl, const float* po,
+                                   int64_t nslices, int64_t rows, int64_t stride, int64_t d,
+                                   float* m, float* l, void* o, int out_dtype,
+                                   cudaStream_t st);
+
+// GEMM patterns.
+struct GemmArgs {
+  const void* a;       // [M,K] bf16
+  const void* b;       // packed [N,K] (e4m3 or bf16)
+  float* d1;           // [M]
+  void* c;             // [M,N] (f32 for quant, bf16 for rms)
+  int* domain_flag;    // device int, set to 1 on 0/0 at finalize
+  int64_t m, n, k;
+  float fmax, eps;
+};
+cudaError_t launch_quant_gemm_sm100(const GemmArgs& g, cudaStream_t st);
+cudaError_t launch_rms_gemm_sm100(const GemmArgs& g, cudaStream_t st);
+bool gemm_sm100_supports(int pattern, int64_t m, int64_t n, int64_t k);
+
+// Weight packing (plan time).
+cudaError_t launch_pack_e4m3(const float* w, int64_t k, int64_t n, uint8_t* packed,
+                             cudaStream_t st);
+cudaError_t launch_pack_rms(const float* w, const float* g, int64_t k, int64_t n,
+                            void* packed_bf16, cudaStream_t st);
+
+}  // namespace rf

@@ -1,0 +1,272 @@
+"""Batched fused-loop executors over librf_cuda (the C-ABI, include/rf_cuda.h).
+
+This is the Python mirror of the host plan layer: it builds rf_desc
+descriptors, owns rf_plan handles, and maps rf_status codes back onto the
+reference's exception types:
+
+  ShapeMismatch             proj/include/redfuse/simulator.hpp:17-19
+  IncompatibleSegmentation  proj/include/redfuse/simulator.hpp:21-23
+  DomainError               proj/include/redfuse/expr.hpp:29-31
+
+Tensors are torch tensors used purely as device memory (PyTorch is plumbing:
+allocation, streams, torch.distributed); every computation runs in a
+librf_cuda kernel. There is no CPU fallback — without the library or an
+sm_100 device the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+from . import _native as N
+
+
+class RedfuseError(RuntimeError):
+    pass
+
+
+class ShapeMismatch(RedfuseError):
+    """redfuse::ShapeMismatch (simulator.hpp:17-19)."""
+
+
+class IncompatibleSegmentation(RedfuseError):
+    """redfuse::IncompatibleSegmentation (simulator.hpp:21-23)."""
+
+
+class DomainError(RedfuseError):
+    """redfuse::DomainError (expr.hpp:29-31): a fault at finalize, e.g. 0/0."""
+
+
+class UnsupportedPattern(RedfuseError):
+    """No librf_cuda kernel implements this pattern / dtype / shape."""
+
+
+class CudaError(RedfuseError):
+    pass
+
+
+_EXC = {
+    N.RF_ERR_SHAPE: ShapeMismatch,
+    N.RF_ERR_SEGMENTATION: IncompatibleSegmentation,
+    N.RF_ERR_DOMAIN: DomainError,
+    N.RF_ERR_UNSUPPORTED: UnsupportedPattern,
+    N.RF_ERR_CUDA: CudaError,
+    N.RF_ERR_ARG: ValueError,
+}
+
+
+def check(status: int) -> None:
+    if status != N.RF_OK:
+        exc = _EXC.get(status, RedfuseError)
+        raise exc(f"{N.lib().rf_status_string(status).decode()}: {N.last_error()}")
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else int(t.data_ptr())
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+_DT = {"f32": N.RF_F32, "bf16": N.RF_BF16, "e4m3": N.RF_E4M3}
+
+
+@dataclass(frozen=True)
+class Desc:
+    pattern: int
+    dtype: str
+    rows: int
+    len: int
+    free_len: int = 0
+    batch: int = 1
+    heads: int = 1
+    segments: int = 1
+    fmax: float = 448.0
+    eps: float = 1e-6
+    softmax_scale: float = 1.0
+    device: int = 0
+
+    def to_c(self) -> N.rf_desc:
+        d = N.rf_desc()
+        d.pattern = self.pattern
+        d.dtype = _DT[self.dtype]
+        d.batch, d.heads, d.rows = self.batch, self.heads, self.rows
+        d.len, d.free_len, d.segments = self.len, self.free_len, self.segments
+        d.fmax, d.eps, d.softmax_scale = self.fmax, self.eps, self.softmax_scale
+        d.tile_rows = d.tile_stream = 0
+        d.device = self.device
+        return d
+
+
+class Plan:
+    """An immutable rf_plan (kernel + tiles + persistent workspace)."""
+
+    def __init__(self, desc: Desc):
+        self.desc = desc
+        self._h = ctypes.c_void_p()
+        c = desc.to_c()
+        check(N.lib().rf_plan_create(ctypes.byref(c), ctypes.byref(self._h)))
+        buf = ctypes.create_string_buffer(1024)
+        check(N.lib().rf_plan_describe(self._h, buf, 1024))
+        self.info = json.loads(buf.value.decode())
+        self.launches_per_run = int(N.lib().rf_plan_launches_per_run(self._h))
+
+    def close(self):
+        if self._h:
+            N.lib().rf_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _io(inputs: Sequence, outputs: Sequence) -> N.rf_io:
+        io = N.rf_io()
+        for i, t in enumerate(inputs):
+            io.in_[i] = t if isinstance(t, int) else _ptr(t)
+        for i, t in enumerate(outputs):
+            io.d[i] = _ptr(t)
+        return io
+
+    def run(self, inputs: Sequence, outputs: Sequence, stream=None) -> None:
+        io = self._io(inputs, outputs)
+        check(N.lib().rf_run(self._h, ctypes.byref(io), _stream_ptr(stream)))
+
+    def run_host(self, inputs: Sequence, outputs: Sequence) -> None:
+        """Host (pinned) buffers in and out; copies happen inside the call."""
+        io = self._io(inputs, outputs)
+        check(N.lib().rf_run_host(self._h, ctypes.byref(io)))
+
+    def run_partials(self, inputs: Sequence, slice_begin: int, m, l, o, stream=None) -> None:
+        io = self._io(inputs, [])
+        p = N.rf_partials(_ptr(m), _ptr(l), _ptr(o), int(m.shape[0]))
+        check(N.lib().rf_run_partials(self._h, ctypes.byref(io), slice_begin, ctypes.byref(p),
+                                      _stream_ptr(stream)))
+
+    def merge_partials(self, m, l, o, outputs: Sequence, stream=None) -> None:
+        io = self._io([], outputs)
+        p = N.rf_partials(_ptr(m), _ptr(l), _ptr(o), int(m.shape[0]))
+        check(N.lib().rf_merge_partials(self._h, ctypes.byref(p), ctypes.byref(io),
+                                        _stream_ptr(stream)))
+
+    def pack_weight(self, w, g=None, stream=None):
+        import torch
+
+        k, n = self.desc.len, self.desc.free_len
+        if tuple(w.shape) != (k, n) or w.dtype != torch.float32:
+            raise ShapeMismatch(f"w must be float32 [{k}, {n}] (reduce-axis major)")
+        if self.desc.pattern == N.RF_PATTERN_QUANT_GEMM_E4M3:
+            out = torch.empty((n, k), dtype=torch.uint8, device=w.device)
+        else:
+            out = torch.empty((n, k), dtype=torch.bfloat16, device=w.device)
+        check(N.lib().rf_pack_weight(self._h, _ptr(w.contiguous()), _ptr(g), _ptr(out),
+                                     _stream_ptr(stream)))
+        return out
+
+    def check_domain(self, stream=None) -> None:
+        check(N.lib().rf_check_domain(self._h, _stream_ptr(stream)))
+
+
+_plans: dict = {}
+
+
+def plan(desc: Desc) -> Plan:
+    p = _plans.get(desc)
+    if p is None:
+        p = _plans[desc] = Plan(desc)
+    return p
+
+
+# ----------------------------------------------------------- batched ops ---
+
+
+def _require(cond: bool, msg: str):
+    if not cond:
+        raise ShapeMismatch(msg)
+
+
+def attention(q, k, v, segments: int = 1, softmax_scale: float = 1.0, stream=None):
+    """Fused safe-softmax -> GEMM attention over every (b, h, query) row.
+
+    q: [B,H,Sq,D], k/v: [B,H,Skv,D] (float32 or bfloat16, contiguous, cuda).
+    Returns (d1 = m [B,H,Sq] f32, d2 = l [B,H,Sq] f32, d3 = O [B,H,Sq,D]).
+    """
+    import torch
+
+    _require(q.dim() == 4 and k.shape == v.shape and k.dim() == 4, "q/k/v must be 4-D")
+    B, H, Sq, D = q.shape
+    _require(k.shape[0] == B and k.shape[1] == H and k.shape[3] == D, "k/v shape mismatch")
+    _require(q.dtype == k.dtype == v.dtype, "q/k/v dtype mismatch")
+    dt = {torch.float32: "f32", torch.bfloat16: "bf16"}.get(q.dtype)
+    if dt is None:
+        raise UnsupportedPattern(f"attention: dtype {q.dtype}")
+    p = plan(Desc(N.RF_PATTERN_ATTENTION, dt, rows=Sq, len=k.shape[2], free_len=D, batch=B,
+                  heads=H, segments=segments, softmax_scale=softmax_scale,
+                  device=q.device.index or 0))
+    m = torch.empty((B, H, Sq), dtype=torch.float32, device=q.device)
+    l = torch.empty_like(m)
+    o = torch.empty_like(q)
+    p.run([q.contiguous(), k.contiguous(), v.contiguous()], [m, l, o], stream)
+    return m, l, o
+
+
+def safe_softmax(x, stream=None):
+    """d1 = max, d2 = sum exp(x - d1) per row of x [rows, n] (float32)."""
+    import torch
+
+    _require(x.dim() == 2 and x.dtype == torch.float32, "x must be float32 [rows, n]")
+    p = plan(Desc(N.RF_PATTERN_SAFE_SOFTMAX, "f32", rows=x.shape[0], len=x.shape[1],
+                  device=x.device.index or 0))
+    d1 = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
+    d2 = torch.empty_like(d1)
+    p.run([x.contiguous()], [d1, d2], stream)
+    return d1, d2
+
+
+def quant_gemm_plan(m: int, k: int, n: int, fmax: float = 448.0, device: int = 0) -> Plan:
+    return plan(Desc(N.RF_PATTERN_QUANT_GEMM_E4M3, "bf16", rows=m, len=k, free_len=n,
+                     fmax=fmax, device=device))
+
+
+def quant_gemm(a, w_packed, fmax: float = 448.0, stream=None):
+    """Per-token absmax -> e4m3 quantise -> GEMM. a: [M,K] bf16; w_packed from
+    Plan.pack_weight. Returns (d1 = amax [M] f32, d2 = C [M,N] f32)."""
+    import torch
+
+    M, K = a.shape
+    Nn = w_packed.shape[0]
+    p = quant_gemm_plan(M, K, Nn, fmax, a.device.index or 0)
+    amax = torch.empty(M, dtype=torch.float32, device=a.device)
+    c = torch.empty((M, Nn), dtype=torch.float32, device=a.device)
+    p.run([a.contiguous(), w_packed], [amax, c], stream)
+    return amax, c
+
+
+def rmsnorm_gemm_plan(t: int, k: int, n: int, eps: float = 1e-6, device: int = 0) -> Plan:
+    return plan(Desc(N.RF_PATTERN_RMSNORM_GEMM, "bf16", rows=t, len=k, free_len=n, eps=eps,
+                     device=device))
+
+
+def rmsnorm_gemm(x, w_packed, eps: float = 1e-6, stream=None):
+    """RMSNorm statistics fused with the following GEMM. x: [T,K] bf16;
+    w_packed from Plan.pack_weight (g folded). Returns (d1 = sum x^2 [T] f32,
+    d2 = Y [T,N] bf16)."""
+    import torch
+
+    T, K = x.shape
+    Nn = w_packed.shape[0]
+    p = rmsnorm_gemm_plan(T, K, Nn, eps, x.device.index or 0)
+    ss = torch.empty(T, dtype=torch.float32, device=x.device)
+    y = torch.empty((T, Nn), dtype=torch.bfloat16, device=x.device)
+    p.run([x.contiguous(), w_packed], [ss, y], stream)
+    return ss, y

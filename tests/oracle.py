@@ -1,0 +1,189 @@
+"""TEST INFRASTRUCTURE: numpy wrappers over the C oracle (oracle/rf_oracle.c,
+built into oracle/_ref/librf_oracle.so) and the golden-fixture reader.
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg use this."""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_SO = os.path.join(ROOT, "oracle", "_ref", "librf_oracle.so")
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(ORACLE_SO):
+            import subprocess
+
+            subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "oracle"], check=True,
+                           capture_output=True)
+        _lib = ctypes.CDLL(ORACLE_SO)
+        D = ctypes.POINTER(ctypes.c_double)
+        I = ctypes.c_int64
+        sig = {
+            "rfo_round_bf16": (ctypes.c_float, [ctypes.c_float]),
+            "rfo_round_e4m3": (ctypes.c_float, [ctypes.c_float]),
+            "rfo_round_bf16_array": (None, [D, D, I]),
+            "rfo_round_e4m3_array": (None, [D, D, I]),
+            "rfo_safe_softmax": (None, [D, I, I, D, D]),
+            "rfo_attention": (None, [D, D, D, I, I, I, I, ctypes.c_double, D, D, D, ctypes.c_int]),
+            "rfo_attention_incremental": (ctypes.c_int, [D, D, I, I, I, I, D, D, D]),
+            "rfo_attention_merge": (None, [D, D, D, I, I, I, D, D, D]),
+            "rfo_quant_gemm": (None, [D, D, I, I, I, ctypes.c_double, D, D, ctypes.c_int]),
+            "rfo_quant_gemm_e4m3": (None, [D, D, I, I, I, ctypes.c_double, I, D, D, ctypes.c_int]),
+            "rfo_rmsnorm_gemm": (None, [D, D, D, I, I, I, ctypes.c_double, D, D, ctypes.c_int]),
+            "rfo_rmsnorm_gemm_incremental": (None, [D, D, D, I, I, ctypes.c_double, D, D]),
+            "rfo_moe_routing": (None, [D, I, I, I, D, D, D, ctypes.POINTER(ctypes.c_int64)]),
+            "rfo_scaled_max_err": (ctypes.c_double, [D, D, I, ctypes.POINTER(ctypes.c_int64)]),
+        }
+        for n, (r, a) in sig.items():
+            f = getattr(_lib, n)
+            f.restype = r
+            f.argtypes = a
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+THREADS = max(1, min(32, os.cpu_count() or 1))
+
+
+def round_bf16(a):
+    a = _f64(a)
+    out = np.empty_like(a)
+    lib().rfo_round_bf16_array(_p(a), _p(out), a.size)
+    return out
+
+
+def round_e4m3(a):
+    a = _f64(a)
+    out = np.empty_like(a)
+    lib().rfo_round_e4m3_array(_p(a), _p(out), a.size)
+    return out
+
+
+def safe_softmax(x):
+    x = _f64(x)
+    rows, n = x.shape
+    d1, d2 = np.empty(rows), np.empty(rows)
+    lib().rfo_safe_softmax(_p(x), rows, n, _p(d1), _p(d2))
+    return d1, d2
+
+
+def attention(q, k, v, scale=1.0):
+    """q [BH,Sq,D], k/v [BH,Skv,D] -> m, l [BH,Sq], o [BH,Sq,D] (oracle form)."""
+    q, k, v = _f64(q), _f64(k), _f64(v)
+    bh, sq, d = q.shape
+    skv = k.shape[1]
+    m, l = np.empty((bh, sq)), np.empty((bh, sq))
+    o = np.empty((bh, sq, d))
+    lib().rfo_attention(_p(q), _p(k), _p(v), bh, sq, skv, d, scale, _p(m), _p(l), _p(o), THREADS)
+    return m, l, o
+
+
+def attention_incremental(p, v, segments=1):
+    """p [rows, kv], v [rows, kv, D] -> m, l, o (run_incremental/multisegment semantics)."""
+    p, v = _f64(p), _f64(v)
+    rows, kv = p.shape
+    d = v.shape[2]
+    m, l = np.empty(rows), np.empty(rows)
+    o = np.empty((rows, d))
+    rc = lib().rfo_attention_incremental(_p(p), _p(v), rows, kv, d, segments, _p(m), _p(l), _p(o))
+    if rc == -2:
+        raise ValueError("IncompatibleSegmentation")
+    return m, l, o
+
+
+def attention_merge(pm, pl, po):
+    pm, pl, po = _f64(pm), _f64(pl), _f64(po)
+    s, rows = pm.shape
+    d = po.shape[2]
+    m, l = np.empty(rows), np.empty(rows)
+    o = np.empty((rows, d))
+    lib().rfo_attention_merge(_p(pm), _p(pl), _p(po), s, rows, d, _p(m), _p(l), _p(o))
+    return m, l, o
+
+
+def quant_gemm(a, w, fmax=448.0):
+    a, w = _f64(a), _f64(w)
+    M, K = a.shape
+    Nn = w.shape[1]
+    d1, c = np.empty(M), np.empty((M, Nn))
+    lib().rfo_quant_gemm(_p(a), _p(w), M, K, Nn, fmax, _p(d1), _p(c), THREADS)
+    return d1, c
+
+
+def quant_gemm_e4m3(a, w, fmax=448.0, tile_k=128):
+    a, w = _f64(a), _f64(w)
+    M, K = a.shape
+    Nn = w.shape[1]
+    d1, c = np.empty(M), np.empty((M, Nn))
+    lib().rfo_quant_gemm_e4m3(_p(a), _p(w), M, K, Nn, fmax, tile_k, _p(d1), _p(c), THREADS)
+    return d1, c
+
+
+def rmsnorm_gemm(x, g, w, eps=1e-6):
+    x, g, w = _f64(x), _f64(g), _f64(w)
+    T, K = x.shape
+    Nn = w.shape[1]
+    d1, y = np.empty(T), np.empty((T, Nn))
+    lib().rfo_rmsnorm_gemm(_p(x), _p(g), _p(w), T, K, Nn, eps, _p(d1), _p(y), THREADS)
+    return d1, y
+
+
+def rmsnorm_gemm_incremental(x, g, w, eps=1e-6):
+    x, g, w = _f64(x), _f64(g), _f64(w)
+    K = x.shape[0]
+    Nn = w.shape[1]
+    d1 = np.empty(1)
+    y = np.empty(Nn)
+    lib().rfo_rmsnorm_gemm_incremental(_p(x), _p(g), _p(w), K, Nn, eps, _p(d1), _p(y))
+    return d1[0], y
+
+
+def moe_routing(s, k):
+    s = _f64(s)
+    rows, e = s.shape
+    d1, d2 = np.empty(rows), np.empty(rows)
+    tv = np.empty((rows, k))
+    ti = np.zeros((rows, k), dtype=np.int64)
+    lib().rfo_moe_routing(_p(s), rows, e, k, _p(d1), _p(d2), _p(tv),
+                          ti.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+    return d1, d2, tv, ti
+
+
+def scaled_max_err(x, y):
+    """compare_reports' metric (simulator.cpp:717-721): max |x-y|/(1+max(|x|,|y|))."""
+    x, y = _f64(x).ravel(), _f64(y).ravel()
+    assert x.shape == y.shape
+    w = ctypes.c_int64(-1)
+    e = lib().rfo_scaled_max_err(_p(x), _p(y), x.size, ctypes.byref(w))
+    return e, w.value
+
+
+def load_golden(name):
+    with open(os.path.join(GOLDEN, name + ".json")) as f:
+        man = json.load(f)
+    blob = np.fromfile(os.path.join(GOLDEN, name + ".f64"), dtype="<f8")
+    out = {}
+    for a in man["arrays"]:
+        out[a["name"]] = blob[a["offset"]:a["offset"] + a["count"]].reshape(a["shape"])
+    out["_meta"] = man["meta"]
+    return out
+
+
+def golden_names(prefix=""):
+    return sorted(f[:-5] for f in os.listdir(GOLDEN) if f.endswith(".json") and f.startswith(prefix))
