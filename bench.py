@@ -1,0 +1,372 @@
+"""Benchmark of the fused cascaded-reduction hot path (driver contract).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+A "step" is one pass of the fused loop (rf_run) over one batch of synthetic
+input of a BASELINE.json configuration. Default workload = configs[1]
+(bf16 MHA prefill B8 H32 S4096 D128, non-causal) — the config the metric is
+quoted on that fits one GPU. Multi-GPU (torchrun, NCCL): every rank runs the
+same per-GPU workload on its own (b,h) units (batch/head sharding needs no
+data-path collective) -> "scaling": "weak"; the timed region is bracketed by
+barriers, and the time is the max over ranks.
+
+`--impl reference` times the reference's own CPU fused loop
+(oracle/_ref/ref_driver, built from /root/reference/proj/src: run_incremental
+per row on all host threads) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused-op TFLOP/s & % roofline at 1/2/4/8 B200 vs CPU ref (cores stated)"
+REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+
+# BASELINE.json configs (index = position in BASELINE.json "configs").
+CONFIGS = {
+    0: dict(name="cfg1: single-head safe-softmax->GEMM attention fp32 S1024 D64 B1",
+            pattern="attention", B=1, H=1, Sq=1024, Skv=1024, D=64, dtype="f32", segments=8),
+    1: dict(name="cfg2: MHA prefill bf16 B8 H32 S4096 D128 (non-causal)",
+            pattern="attention", B=8, H=32, Sq=4096, Skv=4096, D=128, dtype="bf16", segments=1),
+    2: dict(name="cfg3: decode bf16 B64 H32 Sq1 Skv32768 D128 split-KV",
+            pattern="attention", B=64, H=32, Sq=1, Skv=32768, D=128, dtype="bf16", segments=8),
+    3: dict(name="cfg4: per-token absmax FP8 quant + GEMM M=K=N=8192",
+            pattern="quant", M=8192, K=8192, N=8192, dtype="bf16"),
+    4: dict(name="cfg5: RMSNorm stats + GEMM T16384 K4096 N11008",
+            pattern="rms", M=16384, K=4096, N=11008, dtype="bf16"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def work_of(cfg):
+    """Algorithmic FLOPs and bytes per step."""
+    if cfg["pattern"] == "attention":
+        B, H, Sq, Skv, D = cfg["B"], cfg["H"], cfg["Sq"], cfg["Skv"], cfg["D"]
+        es = 4 if cfg["dtype"] == "f32" else 2
+        flops = 4.0 * B * H * Sq * Skv * D
+        bytes_ = es * B * H * (2 * Sq * D + 2 * Skv * D) + 8 * B * H * Sq
+        return flops, bytes_
+    M, K, N = cfg["M"], cfg["K"], cfg["N"]
+    flops = 2.0 * M * N * K
+    if cfg["pattern"] == "quant":
+        bytes_ = 2 * M * K + N * K + 4 * M * N + 4 * M
+    else:
+        bytes_ = 2 * M * K + 2 * N * K + 2 * M * N + 4 * M
+    return flops, bytes_
+
+
+def bound_of(cfg):
+    if cfg["pattern"] == "attention" and cfg["Sq"] == 1:
+        return "hbm"
+    return "tensor"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        if not shutil.which("nvidia-smi"):
+            return
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        self.proc = subprocess.Popen(
+            ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+             "--format=csv,noheader,nounits", "-lms", "20"],
+            stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        time.sleep(0.3)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.1)
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
+        # "under load": samples at or above the median (idle gaps at start/end excluded)
+        med = statistics.median(sm) if sm else None
+        loaded = [x for x in sm if med is None or x >= 0.8 * med]
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_reference(cfg, budget_s=12.0, threads=None):
+    """The reference's CPU fused loop on the host cores (bounded sample)."""
+    if not os.path.exists(REF_DRIVER):
+        return None
+    threads = threads or os.cpu_count() or 1
+    if cfg["pattern"] == "attention":
+        segs = cfg.get("segments", 1) if cfg["Sq"] == 1 else 1
+        args = ["attention", str(cfg["Skv"]), str(cfg["D"]), "100000000", str(threads), str(segs)]
+        sample = f"rows = (b,h,query) cascades of kv={cfg['Skv']}, hd={cfg['D']}"
+    elif cfg["pattern"] == "quant":
+        args = ["quant", str(cfg["K"]), str(cfg["N"]), str(threads), str(threads), "1"]
+        sample = f"rows = tokens of K={cfg['K']}, N={cfg['N']}"
+    else:
+        args = ["rms", str(cfg["K"]), str(cfg["N"]), str(threads), str(threads), "1"]
+        sample = f"rows = tokens of K={cfg['K']}, N={cfg['N']}"
+    out = subprocess.run([REF_DRIVER, "bench"] + args + [f"{budget_s}"], capture_output=True,
+                         text=True, timeout=600)
+    if out.returncode != 0:
+        return None
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    return {
+        "value": r["flop_per_s"] / 1e12,
+        "unit": "TFLOP/s",
+        "cores": r["threads"],
+        "kind": "reference",
+        "sample": f"{r['rows']} {sample} through redfuse run_incremental"
+                  f"{' / run_multisegment' if r['segments'] > 1 else ''} "
+                  f"(oracle/_ref/ref_driver, {r['s_per_row_thread']:.3f} s/row/thread, "
+                  f"{r['wall_s']:.1f} s wall)",
+        "rows_per_s": r["rows_per_s"],
+    }
+
+
+def dist_setup(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def make_inputs(cfg, device):
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(1234)
+    if cfg["pattern"] == "attention":
+        dt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
+        B, H, Sq, Skv, D = cfg["B"], cfg["H"], cfg["Sq"], cfg["Skv"], cfg["D"]
+        q = ((torch.rand(B, H, Sq, D, device=device, generator=g) * 2 - 1) / D ** 0.5).to(dt)
+        k = (torch.rand(B, H, Skv, D, device=device, generator=g) * 2 - 1).to(dt)
+        v = (torch.rand(B, H, Skv, D, device=device, generator=g) * 2 - 1).to(dt)
+        return [q, k, v]
+    raise SystemExit(f"config {cfg['name']} not wired in bench yet")
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_10026_b200 import Desc, Plan
+    from paper_2603_10026_b200 import _native as N
+
+    world, rank, local = dist_setup(args)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    inputs = make_inputs(cfg, dev)
+    B, H, Sq, Skv, D = cfg["B"], cfg["H"], cfg["Sq"], cfg["Skv"], cfg["D"]
+    plan = Plan(Desc(N.RF_PATTERN_ATTENTION, cfg["dtype"], rows=Sq, len=Skv, free_len=D, batch=B,
+                     heads=H, segments=cfg.get("segments", 1), device=dev.index))
+    m = torch.empty(B, H, Sq, device=dev)
+    l = torch.empty_like(m)
+    o = torch.empty_like(inputs[0])
+    outs = [m, l, o]
+    stream = torch.cuda.Stream(device=dev)
+    flops, nbytes = work_of(cfg)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            plan.run(inputs, outs, stream)
+        stream.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        clocks = ClockSampler(dev.index)
+        clocks.start()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        ev[0].record(stream)
+        for i in range(args.steps):
+            plan.run(inputs, outs, stream)
+            ev[i + 1].record(stream)
+        stream.synchronize()
+        torch.cuda.synchronize()
+        barrier()
+        clk = clocks.stop()
+    per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = flops * world * args.steps / (total_ms * 1e-3) / 1e12
+
+    # ---- end-to-end through the C-ABI host path (pinned host buffers) ----
+    hin = [x.cpu().pin_memory() for x in inputs]
+    hout = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in outs]
+    for _ in range(2):
+        plan.run_host(hin, hout)
+    barrier()
+    e2e_steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        plan.run_host(hin, hout)
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_s = float(te.item())
+    h2d = sum(x.numel() * x.element_size() for x in hin)
+    d2h = sum(x.numel() * x.element_size() for x in hout)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    pk, pk_src = peaks()
+    bound = bound_of(cfg)
+    kern_ms = statistics.mean(per_step)
+    if bound == "hbm":
+        achieved = nbytes / (kern_ms * 1e-3) / 1e9
+        peak, unit = pk["hbm_gbs"], "GB/s"
+    else:
+        achieved = flops / (kern_ms * 1e-3) / 1e12
+        peak, unit = pk["bf16_tflops"], "TFLOP/s"
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        traffic = json.load(open(prof)).get(cfg["name"].split(":")[0])
+    line = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "TFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": cfg["dtype"],
+        "data": "synthetic (uniform, make_attention distributions; q pre-scaled by 1/sqrt(D))",
+        "config": {"workload": cfg["name"], "B": B, "H": H, "Sq": Sq, "Skv": Skv, "D": D,
+                   "segments": cfg.get("segments", 1), "kernel": plan.info["kernel"],
+                   "parallelism": f"batch/head shards x{world} (no collective)",
+                   "l2": f"inputs {sum(x.numel() * x.element_size() for x in inputs) / 1e6:.0f} MB "
+                         "> 126 MB L2, no flush"},
+        "roofline": {"bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "peak_source": f"{pk_src} (MEASURED_PEAKS.json burst)",
+                     "algorithmic": {"flops": flops, "bytes": nbytes}},
+        "e2e": {"value": round(flops * e2e_steps / e2e_s / 1e12, 3), "unit": "TFLOP/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": "rf_run_host (C-ABI, pinned host buffers, chunked H2D/compute/D2H)"},
+        "gpu_launches": args.steps * plan.launches_per_run,
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_reference(cfg)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    flops, _ = work_of(cfg)
+    t0 = time.perf_counter()
+    vals = []
+    cb = None
+    step_budget = min(5.0, max(0.5, 40.0 / args.steps))
+    for _ in range(args.warmup):
+        cpu_reference(cfg, budget_s=0.5)
+    for _ in range(args.steps):
+        cb = cpu_reference(cfg, budget_s=step_budget)
+        if cb is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_driver not built"}))
+            return
+        vals.append(cb["value"])
+    value = statistics.median(vals)
+    cb["value"] = value
+    print(json.dumps({
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": "TFLOP/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": flops / (value * 1e12) * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (the reference's own make_attention generator)",
+        "config": {"workload": cfg["name"]},
+        "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t0,
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", type=int, default=1, help="index into BASELINE.json configs")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -11,12 +11,13 @@
 //       The oracle restatement (oracle/rf_oracle.c) and the CUDA kernels are
 //       pinned against these.
 //
-//   ref_driver bench <pattern> <L0> <free> <rows> <threads> [segments]
+//   ref_driver bench <pattern> <L0> <free> <rows> <threads> [segments] [budget_s]
 //       Times the reference's CPU fused loop (run_incremental, or
 //       run_multisegment when segments > 1; proj/src/simulator.cpp:631-687) on
 //       a bounded sample of rows of a BASELINE.json configuration, one row per
-//       thread at a time (executors are pure; stores are per-row). Prints one
-//       JSON object.  This is the `cpu_baseline` / `--impl reference` arm.
+//       thread at a time (executors are pure; stores are per-row). With a
+//       budget, threads stop taking new rows once budget_s has elapsed (rows is
+//       then an upper bound). Prints one JSON object.  This is the `cpu_baseline` / `--impl reference` arm.
 //
 // Only reference *public API* is used (workloads.hpp, simulator.hpp, acrf.hpp).
 
@@ -334,6 +335,7 @@ int cmd_bench(int argc, char** argv) {
   long long rows = std::atoll(argv[5]);
   int threads = std::atoi(argv[6]);
   long long segs = argc > 7 ? std::atoll(argv[7]) : 1;
+  double budget = argc > 8 ? std::atof(argv[8]) : 0.0;
   std::unique_ptr<RowJob> job;
   if (pat == "attention") job = std::make_unique<AttentionJob>(l0, fr, segs);
   else if (pat == "quant") job = std::make_unique<QuantJob>(l0, fr);
@@ -343,24 +345,27 @@ int cmd_bench(int argc, char** argv) {
   if (threads < 1) threads = 1;
   if (rows < threads) rows = threads;
 
-  std::atomic<long long> next{0};
+  std::atomic<long long> next{0}, done{0};
   std::vector<double> busy(static_cast<std::size_t>(threads), 0.0);
   double t0 = now_s();
   std::vector<std::thread> pool;
   for (int t = 0; t < threads; ++t) {
     pool.emplace_back([&, t] {
       for (;;) {
+        if (budget > 0 && now_s() - t0 > budget) break;
         long long r = next.fetch_add(1);
         if (r >= rows) break;
         TensorStore st = job->make(1000003ull * static_cast<std::uint64_t>(r) + 42);
         double a = now_s();
         job->run(st);
         busy[static_cast<std::size_t>(t)] += now_s() - a;
+        done.fetch_add(1);
       }
     });
   }
   for (auto& th : pool) th.join();
   double wall = now_s() - t0;
+  rows = done.load();
   double busy_sum = 0;
   for (double b : busy) busy_sum += b;
   // Throughput of the timed bodies on `threads` threads: rows / (busy / threads).

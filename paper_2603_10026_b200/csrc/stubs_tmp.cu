@@ -1,8 +1,5 @@
 #include "rf_internal.h"
 namespace rf {
-cudaError_t launch_attention_decode(const AttnArgs& a, cudaStream_t st) { return launch_attention_f32(a, st); }
-cudaError_t launch_attention_sm100(const AttnArgs&, cudaStream_t) { return cudaErrorNotSupported; }
-bool attention_sm100_supports(int64_t, int64_t, int64_t, int64_t) { return false; }
 cudaError_t launch_quant_gemm_sm100(const GemmArgs&, cudaStream_t) { return cudaErrorNotSupported; }
 cudaError_t launch_rms_gemm_sm100(const GemmArgs&, cudaStream_t) { return cudaErrorNotSupported; }
 bool gemm_sm100_supports(int, int64_t, int64_t, int64_t) { return false; }

@@ -1,0 +1,81 @@
+"""GPU parity of the bf16 attention kernels — tcgen05 prefill (attn_sm100.cu)
+and split-KV decode (attn_decode.cu) — against the oracle evaluated on the
+same bf16-rounded inputs (tolerance 2e-2 scaled, north_star)."""
+import numpy as np
+import pytest
+
+from tests import oracle as O
+from tests.test_gpu_attention import _check, _inputs
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+def _run(B, H, Sq, Skv, D, segments=1, seed=0, expect=None):
+    import torch
+    from paper_2603_10026_b200 import Desc, Plan, _native as N
+
+    q, k, v = _inputs(B, H, Sq, Skv, D, seed, torch.bfloat16)
+    p = Plan(Desc(N.RF_PATTERN_ATTENTION, "bf16", rows=Sq, len=Skv, free_len=D, batch=B, heads=H,
+                  segments=segments))
+    if expect:
+        assert expect in p.info["kernel"], p.info
+    qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
+    m = torch.empty(B, H, Sq, device="cuda")
+    l = torch.empty_like(m)
+    o = torch.empty_like(qd)
+    p.run([qd, kd, vd], [m, l, o])
+    torch.cuda.synchronize()
+    return _check(q, k, v, m, l, o, TOL), (m, l, o)
+
+
+@pytest.mark.parametrize("D", [128, 64])
+@pytest.mark.parametrize("shape", [(1, 2, 256, 128), (1, 2, 512, 1024), (2, 1, 256, 4096)])
+def test_tcgen05_prefill_vs_oracle(D, shape):
+    B, H, Sq, Skv = shape
+    errs, _ = _run(B, H, Sq, Skv, D, expect="tcgen05")
+    assert max(errs) < TOL
+
+
+@pytest.mark.parametrize("segments", [2, 4])
+def test_tcgen05_prefill_multisegment(segments):
+    errs, _ = _run(1, 2, 256, 1024, 128, segments=segments, expect="tcgen05")
+    assert max(errs) < TOL
+
+
+def test_tcgen05_stats_are_tight():
+    """d1 is an exact max of fp32 logits; d2 accumulates fp32 exps: both far
+    tighter than the bf16 tolerance."""
+    (em, el, eo), _ = _run(1, 4, 256, 2048, 128, seed=5, expect="tcgen05")
+    assert em < 1e-5 and el < 1e-3 and eo < 1e-2
+
+
+def test_tcgen05_large_logits_rescale_path():
+    """Growing logits force exp(d1'-d1) != 1 on many tiles (correction warpgroup)."""
+    import torch
+    from paper_2603_10026_b200 import attention
+
+    B, H, Sq, Skv, D = 1, 2, 256, 2048, 128
+    q, k, v = _inputs(B, H, Sq, Skv, D, 9, torch.float64)
+    ramp = torch.linspace(0.0, 8.0, Skv, dtype=torch.float64).view(1, 1, Skv, 1)
+    k = k * (1 + ramp)  # later keys have larger logits -> max increases along the loop
+    q, k, v = (t.to(torch.bfloat16) for t in (q, k, v))
+    m, l, o = attention(q.cuda(), k.cuda(), v.cuda())
+    torch.cuda.synchronize()
+    _check(q, k, v, m, l, o, TOL)
+
+
+@pytest.mark.parametrize("segments", [1, 4, 8])
+def test_decode_split_kv(segments):
+    errs, _ = _run(2, 4, 1, 8192, 128, segments=segments, expect="decode")
+    assert max(errs) < TOL
+
+
+def test_decode_odd_slice_uses_generic_path():
+    errs, _ = _run(1, 2, 1, 96, 128, segments=1)
+    assert max(errs) < TOL
+
+
+def test_bf16_ragged_prefill_generic_path():
+    errs, _ = _run(1, 2, 100, 300, 64)
+    assert max(errs) < TOL
