@@ -10,20 +10,28 @@
 //     P (bf16) written back into TMEM over S and consumed as the A operand,
 //   * the cascaded statistics (running max d1, rescaled sum-exp d2) in
 //     registers, one thread per row,
-//   * the d3 correction exp(d1' - d1) applied tile by tile to the TMEM
-//     accumulator by a dedicated correction warpgroup; the d2'/d2 factor of
-//     the derived correction exp(d1'-d1)*d2'/d2 telescopes over the loop to
-//     1/d2(final) and is applied once at finalize (finalize_root,
-//     simulator.cpp:611-621, retargets the root's scaling the same way).
+//   * the d3 correction exp(d1' - d1) applied inside the loop to the TMEM
+//     accumulator (see below); the d2'/d2 factor of the derived correction
+//     exp(d1'-d1)*d2'/d2 telescopes over the loop to 1/d2(final) and is
+//     applied once at finalize (finalize_root, simulator.cpp:611-621,
+//     retargets the root's scaling the same way).
 //
 // CTA = 2 Q tiles x 128 rows (ping-pong), KV tiles of 128 keys.
-// Warp roles (512 threads):
-//   warps 0-3  softmax for Q tile 0 (thread = row)
-//   warps 4-7  softmax for Q tile 1
-//   warps 8-11 correction (O *= alpha in TMEM) + epilogue (O / l -> global)
-//   warp 12    TMA producer          warp 13  MMA issuer (one elected lane)
-//   warp 14    TMEM allocator        warp 15  idle
-// TMEM (512 cols): S0 [0,128)  S1 [128,256)  O0 [256,256+D)  O1 [384,384+D)
+// Warp roles (320 threads, ~200 registers per thread):
+//   warps 0-3  softmax + correction + epilogue for Q tile 0 (thread = row)
+//   warps 4-7  the same for Q tile 1
+//   warp 8     TMA producer          warp 9  MMA issuer (one elected lane) + TMEM owner
+// TMEM (512 cols): S0 [0,128)  S1 [128,256)  O0 [256,256+D)  O1 [384,384+D);
+// P_k (bf16 pairs) overwrites S_k cols [0,64) and is the A operand of P V.
+//
+// The correction O *= exp(d1' - d1) is applied by the softmax thread of the
+// row itself: tcgen05.mma executes in issue order, so when S_k,i is complete
+// PV_k,i-1 is too, and PV_k,i is only issued after the thread arrives on
+// p_full. Rescaling is lazy: the accumulator keeps a reference max m_ref and
+// is only re-based when the running max d1 exceeds it by more than 2^8 (the
+// exponentials stay <= 256, far from overflow); O and d2 always share the same
+// reference, so d3 = O / d2 is unchanged and d2 is re-based to the true d1 at
+// finalize. d1 itself is the exact running max.
 #include <cuda_bf16.h>
 
 #include "rf_internal.h"
@@ -37,7 +45,9 @@ using namespace sm100;
 constexpr int BM = 128;       // rows per Q tile
 constexpr int BN = 128;       // keys per KV tile
 constexpr int NSLOT = 4;      // K/V ring slots
-constexpr int NTHREADS = 512;
+constexpr int NTHREADS = 320;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 template <int D>
 struct Smem {
@@ -47,9 +57,7 @@ struct Smem {
   uint8_t kv[NSLOT][kTile];
   uint64_t bar_q;
   uint64_t kv_full[NSLOT], kv_empty[NSLOT];
-  uint64_t s_full[2], p_full[2], sc_full[2], o_ready[2], pv_done[2], l_ready[2];
-  float alpha[2][BM];
-  float lfin[2][BM];
+  uint64_t s_full[2], p_full[2], pv_done[2];
   uint32_t tmem_base;
 };
 
@@ -87,23 +95,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     for (int k = 0; k < 2; ++k) {
       mbar_init(&s.s_full[k], 1);
-      mbar_init(&s.p_full[k], BM);
-      mbar_init(&s.sc_full[k], BM);
-      mbar_init(&s.o_ready[k], BM);
+      mbar_init(&s.p_full[k], 4);  // one arrival per softmax warp
       mbar_init(&s.pv_done[k], 1);
-      mbar_init(&s.l_ready[k], BM);
     }
     fence_barrier_init();
   }
-  if (warp == 14) tmem_alloc<512>(&s.tmem_base);
+  if (warp == 9) tmem_alloc<512>(&s.tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s.tmem_base;
-  const uint32_t tS[2] = {tmem + 0, tmem + 128};
-  const uint32_t tO[2] = {tmem + 256, tmem + 384};
 
-  if (warp == 12) {
+  if (warp == 8) {
     // ------------------------------------------------------------ TMA ----
     if (elect_one()) {
       prefetch_tmap(&tq);
@@ -126,10 +129,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tma_load_2d(s.kv[slot] + c * BN * 128, m, &s.kv_full[slot], c * 64, y, kEvictLast);
       }
     }
-  } else if (warp == 13) {
+  } else if (warp == 9) {
     // ------------------------------------------------------------ MMA ----
     const uint32_t id_s = idesc_f16(BM, BN, kFmtBF16, false, false);
     const uint32_t id_o = idesc_f16(BM, D, kFmtBF16, false, true);
+    const uint32_t tS[2] = {tmem + 0, tmem + 128};
+    const uint32_t tO[2] = {tmem + 256, tmem + 384};
     const bool leader = elect_one();
     auto issue_s = [&](int k, int slot) {  // S_k = Q_k K^T
       if (leader) {
@@ -144,14 +149,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       __syncwarp();
     };
-    auto issue_pv = [&](int k, int slot, bool acc) {  // O_k += P_k V
+    auto issue_pv = [&](int k, int slot, bool acc, bool last) {  // O_k += P_k V
       if (leader) {
         const uint32_t vb = smem_u32(s.kv[slot]);
 #pragma unroll
         for (int ks = 0; ks < BN / 16; ++ks)
           mma_f16_ts(tO[k], tS[k] + ks * 8, sdesc_mnmajor_sw128(vb + ks * 2048, BN * 128), id_o,
                      acc || ks > 0);
-        mma_commit(&s.pv_done[k]);
+        if (last) mma_commit(&s.pv_done[k]);
       }
       __syncwarp();
     };
@@ -160,7 +165,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       __syncwarp();
     };
     mbar_wait(&s.bar_q, 0);
-    // prologue: S0_0, S1_0 on K_0 (ring index 0)
     mbar_wait(&s.kv_full[0], 0);
     tc_fence_after();
     issue_s(0, 0);
@@ -171,156 +175,137 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int sV = tV % NSLOT, sK = tK % NSLOT;
       const uint32_t phV = (tV / NSLOT) & 1, phK = (tK / NSLOT) & 1;
       const uint32_t ph = i & 1;
+      const bool last = i + 1 == n_tiles;
       mbar_wait(&s.kv_full[sV], phV);
       // tile 0: PV0_i then S0_{i+1}
       mbar_wait(&s.p_full[0], ph);
-      mbar_wait(&s.o_ready[0], ph);
       tc_fence_after();
-      issue_pv(0, sV, i > 0);
-      if (i + 1 < n_tiles) {
+      issue_pv(0, sV, i > 0, last);
+      if (!last) {
         mbar_wait(&s.kv_full[sK], phK);
         tc_fence_after();
         issue_s(0, sK);
       }
       // tile 1: PV1_i then S1_{i+1}
       mbar_wait(&s.p_full[1], ph);
-      mbar_wait(&s.o_ready[1], ph);
       tc_fence_after();
-      issue_pv(1, sV, i > 0);
+      issue_pv(1, sV, i > 0, last);
       release(sV);
-      if (i + 1 < n_tiles) {
+      if (!last) {
         issue_s(1, sK);
         release(sK);
       }
     }
-  } else if (warp < 8) {
-    // -------------------------------------------------------- softmax ----
-    const int k = warp >> 2;         // Q tile
+  } else {
+    // ----------------------------------- softmax / correction / epilogue --
+    const int k = warp >> 2;  // Q tile
     const int row = threadIdx.x & 127;
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const uint32_t tSk = tS[k] + lane_off;
+    const uint32_t tSk = tmem + k * 128 + lane_off;
+    const uint32_t tOk = tmem + 256 + k * 128 + lane_off;
     const float c1 = p.scale_log2;
-    float m = -INFINITY, l = 0.f;
+    float m_true = -INFINITY;  // d1: exact running max
+    float m_ref = -INFINITY;   // reference max of the accumulators
+    float l = 0.f;             // d2 relative to m_ref
     for (int i = 0; i < n_tiles; ++i) {
       mbar_wait(&s.s_full[k], i & 1);
       tc_fence_after();
-      // pass 1: reduction 1 (max) over the row of S
-      float tmax = -INFINITY;
+      uint32_t sr[4][32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tSk + c * 32, r);
-        tmem_ld_wait();
+      for (int c = 0; c < 4; ++c) tmem_ld32(tSk + c * 32, sr[c]);
+      tmem_ld_wait();
+#define SV(j) __uint_as_float(sr[(j) >> 5][(j) & 31])
+      // reduction 1: d1 = max(d1, max_tile)   (store-prev in m_ref / m_true)
+      float tmax = SV(0);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) tmax = fmaxf(tmax, __uint_as_float(r[j]));
+      for (int j = 1; j < BN; ++j) tmax = fmaxf(tmax, SV(j));
+      m_true = fmaxf(m_true, tmax * p.scale);
+      // correction exp(d1' - d1): lazily re-base the accumulators
+      const bool need = (m_true - m_ref) * kLog2e > kRescaleThreshold;
+      float alpha = 1.f;
+      if (need) {
+        alpha = ex2_mufu((m_ref - m_true) * kLog2e);  // 0 on the first tile
+        l *= alpha;
+        m_ref = m_true;
       }
-      const float m_new = fmaxf(m, tmax * p.scale);
-      const float alpha = (i == 0) ? 1.f : exp2f((m - m_new) * 1.4426950408889634f);
-      s.alpha[k][row] = alpha;
-      mbar_arrive(&s.sc_full[k]);
-      // pass 2: reduction 2 (sum exp, corrected by alpha) + P for reduction 3
-      const float mb = m_new * 1.4426950408889634f;
+      // reductions 2 and 3: P = exp(S - d1) in bf16 into TMEM, row sum in fp32
+      const float mb = m_ref * kLog2e;
       float rs = 0.f;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tSk + c * 32, r);
-        tmem_ld_wait();
-        uint32_t pk[16];
+      for (int h = 0; h < 2; ++h) {
+        uint32_t pk[32];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float p0 = exp2f(fmaf(__uint_as_float(r[2 * j]), c1, -mb));
-          const float p1 = exp2f(fmaf(__uint_as_float(r[2 * j + 1]), c1, -mb));
+        for (int j = 0; j < 32; ++j) {
+          const int c0 = 64 * h + 2 * j;
+          const float x0 = fmaf(SV(c0), c1, -mb), x1 = fmaf(SV(c0 + 1), c1, -mb);
+          // one of every four exponentials on the FMA pipe (MUFU offload)
+          const float p0 = ex2_mufu(x0);
+          const float p1 = (j & 1) ? ex2_poly(x1) : ex2_mufu(x1);
           rs += p0 + p1;
           pk[j] = pack_bf16x2(p0, p1);
         }
-        tmem_st16(tSk + c * 16, pk);
+        tmem_st32(tSk + 32 * h, pk);
       }
-      l = l * alpha + rs;
-      m = m_new;
+#undef SV
+      l += rs;
+      if (i > 0 && __any_sync(0xffffffffu, need)) {
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tOk + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * alpha);
+          tmem_st32(tOk + c * 32, r);
+        }
+      }
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&s.p_full[k]);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&s.p_full[k]);
     }
-    // finalize: publish l for the epilogue, write d1 / d2
-    s.lfin[k][row] = l;
-    mbar_arrive(&s.l_ready[k]);
+    // ---- finalize (finalize_root): d2 re-based to the true d1, d3 = O / d2 ----
+    const float l_true = l * ex2_mufu((m_ref - m_true) * kLog2e);
     const int64_t grow = static_cast<int64_t>(bh) * p.sq + q_row0 + k * BM + row;
+    const int64_t ps = slice - p.part_base;
     if (p.part_m == nullptr) {
-      p.m[grow] = m;
-      p.l[grow] = l;
+      p.m[grow] = m_true;
+      p.l[grow] = l_true;
     } else {
-      const int64_t ps = slice - p.part_base;
-      p.part_m[ps * p.rows_total + grow] = m;
-      p.part_l[ps * p.rows_total + grow] = l;
+      p.part_m[ps * p.rows_total + grow] = m_true;
+      p.part_l[ps * p.rows_total + grow] = l_true;
     }
-  } else if (warp < 12) {
-    // ----------------------------------------------------- correction ----
-    const int row = threadIdx.x & 127;
-    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    for (int i = 0; i < n_tiles; ++i) {
-      for (int k = 0; k < 2; ++k) {
-        mbar_wait(&s.sc_full[k], i & 1);
-        if (i > 0) {
-          const float a = s.alpha[k][row];
-          mbar_wait(&s.pv_done[k], (i - 1) & 1);
-          tc_fence_after();
-          // exp(d1' - d1) == 1 exactly for every row of this warp: skip (bit-identical)
-          if (__any_sync(0xffffffffu, a != 1.f)) {
+    mbar_wait(&s.pv_done[k], 0);
+    tc_fence_after();
+    const float inv_l = 1.f / l;
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
-              uint32_t r[32];
-              const uint32_t addr = tO[k] + lane_off + c * 32;
-              tmem_ld32(addr, r);
-              tmem_ld_wait();
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld32(tOk + c * 32, r);
+      tmem_ld_wait();
+      if (p.part_o == nullptr) {
+        uint4* dst = reinterpret_cast<uint4*>(p.o + grow * D + c * 32);
 #pragma unroll
-              for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * a);
-              tmem_st32(addr, r);
-            }
-            tmem_st_wait();
-          }
-          tc_fence_before();
+        for (int v = 0; v < 4; ++v) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(r[8 * v + 0]) * inv_l, __uint_as_float(r[8 * v + 1]) * inv_l);
+          w.y = pack_bf16x2(__uint_as_float(r[8 * v + 2]) * inv_l, __uint_as_float(r[8 * v + 3]) * inv_l);
+          w.z = pack_bf16x2(__uint_as_float(r[8 * v + 4]) * inv_l, __uint_as_float(r[8 * v + 5]) * inv_l);
+          w.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]) * inv_l, __uint_as_float(r[8 * v + 7]) * inv_l);
+          dst[v] = w;
         }
-        mbar_arrive(&s.o_ready[k]);
-      }
-    }
-    // epilogue: O / d2 -> global
-    for (int k = 0; k < 2; ++k) {
-      mbar_wait(&s.pv_done[k], (n_tiles - 1) & 1);
-      mbar_wait(&s.l_ready[k], 0);
-      tc_fence_after();
-      const float inv_l = 1.f / s.lfin[k][row];
-      const int64_t grow = static_cast<int64_t>(bh) * p.sq + q_row0 + k * BM + row;
+      } else {
+        float4* dst = reinterpret_cast<float4*>(p.part_o + (ps * p.rows_total + grow) * D + c * 32);
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tO[k] + lane_off + c * 32, r);
-        tmem_ld_wait();
-        if (p.part_o == nullptr) {
-          uint4* dst = reinterpret_cast<uint4*>(p.o + grow * D + c * 32);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            uint4 w;
-            w.x = pack_bf16x2(__uint_as_float(r[8 * v + 0]) * inv_l, __uint_as_float(r[8 * v + 1]) * inv_l);
-            w.y = pack_bf16x2(__uint_as_float(r[8 * v + 2]) * inv_l, __uint_as_float(r[8 * v + 3]) * inv_l);
-            w.z = pack_bf16x2(__uint_as_float(r[8 * v + 4]) * inv_l, __uint_as_float(r[8 * v + 5]) * inv_l);
-            w.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]) * inv_l, __uint_as_float(r[8 * v + 7]) * inv_l);
-            dst[v] = w;
-          }
-        } else {
-          const int64_t ps = slice - p.part_base;
-          float4* dst = reinterpret_cast<float4*>(p.part_o + (ps * p.rows_total + grow) * D + c * 32);
-#pragma unroll
-          for (int v = 0; v < 8; ++v)
-            dst[v] = make_float4(__uint_as_float(r[4 * v]) * inv_l, __uint_as_float(r[4 * v + 1]) * inv_l,
-                                 __uint_as_float(r[4 * v + 2]) * inv_l, __uint_as_float(r[4 * v + 3]) * inv_l);
-        }
+        for (int v = 0; v < 8; ++v)
+          dst[v] = make_float4(__uint_as_float(r[4 * v]) * inv_l, __uint_as_float(r[4 * v + 1]) * inv_l,
+                               __uint_as_float(r[4 * v + 2]) * inv_l, __uint_as_float(r[4 * v + 3]) * inv_l);
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 14) tmem_dealloc<512>(tmem);
+  if (warp == 9) tmem_dealloc<512>(tmem);
 }
 
 template <int D>

@@ -288,6 +288,28 @@ __host__ __device__ constexpr uint32_t idesc_f8(uint32_t m, uint32_t n) {
   return (1u << 4) | (kFmtE4M3 << 7) | (kFmtE4M3 << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
 
+// ------------------------------------------------------------- fast math --
+
+// MUFU 2^x (ex2.approx.ftz): the XU pipe.
+__device__ __forceinline__ float ex2_mufu(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 2^x on the FMA/ALU pipes: 2^floor(x) * p(frac), p = degree-3 minimax of 2^f
+// on [0,1) (max rel err 8.8e-5, below bf16's 3.9e-3). Used to offload part
+// of the softmax exponentials from the MUFU pipe. Valid for x <= 127.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float xi = floorf(x);
+  const float f = x - xi;
+  float p = fmaf(f, 0.077119089663028717041015625f, 0.227564394474029541015625f);
+  p = fmaf(p, f, 0.695146143436431884765625f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (static_cast<int>(xi) << 23));
+}
+
 // ---------------------------------------------------------- packing utils --
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
