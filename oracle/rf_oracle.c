@@ -260,29 +260,43 @@ void rfo_quant_gemm(const double* a, const double* w, int64_t M, int64_t K, int6
   for_rows(quant_row, &q, M, threads);
 }
 
+/* Smallest power of two >= x (x > 0); 0 for x == 0. */
+static float pow2_ceil(float x) {
+  if (!(x > 0.0f)) return 0.0f;
+  int e;
+  float f = frexpf(x, &e); /* x = f 2^e, f in [0.5, 1) */
+  return f == 0.5f ? ldexpf(1.0f, e - 1) : ldexpf(1.0f, e);
+}
+
 static void quant_e4m3_row(void* vctx, int64_t row) {
   quant_ctx* q = (quant_ctx*)vctx;
   const double* ar = q->a + row * q->K;
   double* cr = q->c + row * q->N;
   for (int64_t f = 0; f < q->N; ++f) cr[f] = 0.0;
   float amax = 0.0f; /* running d1 (float32, as the kernel keeps it) */
+  float ref = 0.0f;  /* H' reference: power of two >= running d1 */
   int64_t tk = q->tile_k > 0 ? q->tile_k : q->K;
   for (int64_t l0 = 0; l0 < q->K; l0 += tk) {
     int64_t l1 = l0 + tk < q->K ? l0 + tk : q->K;
-    float prev = amax;
     for (int64_t l = l0; l < l1; ++l) amax = fmaxf(amax, fabsf((float)ar[l]));
-    /* Eq.17 correction, corr = d1'/d1 (quant_gemm d2), on touched lanes */
-    if (l0 > 0 && prev != amax) {
-      double corr = (double)prev / (double)amax;
+    float nref = pow2_ceil(amax);
+    /* Eq.17 correction of the accumulator, corr = H'(d1')/H'(d1) = ref'/ref
+     * (quant_gemm d2: d1'/d1 with d1 replaced by its power-of-two H' proxy) */
+    if (l0 > 0 && nref != ref && ref > 0.0f) {
+      double corr = (double)ref / (double)nref;
       for (int64_t f = 0; f < q->N; ++f) cr[f] *= corr;
     }
-    float scale = (float)q->fmax / amax; /* kernel: one reciprocal per tile */
+    ref = nref;
+    float scale = (float)q->fmax / ref; /* exact: fmax * 2^-e */
     for (int64_t l = l0; l < l1; ++l) {
       double qv = (double)rfo_round_e4m3((float)ar[l] * scale);
       const double* wr = q->w + l * q->N;
       for (int64_t f = 0; f < q->N; ++f) cr[f] += qv * wr[f];
     }
   }
+  /* finalize_root: retarget H'(ref) -> H(d1): c *= ref / d1 (0/0 -> NaN) */
+  double fin = (double)ref / (double)amax;
+  for (int64_t f = 0; f < q->N; ++f) cr[f] *= fin;
   q->d1[row] = amax;
 }
 

@@ -75,13 +75,16 @@ void rfo_attention_merge(const double* part_m, const double* part_l,
 void rfo_quant_gemm(const double* a, const double* w, int64_t M, int64_t K, int64_t N,
                     double fmax, double* d1, double* c, int threads);
 
-/* The FP8 kernel's arithmetic restated: running absmax per K tile of width
- * tile_k (amax_t = max(amax_{t-1}, max_{l in t}|a_l|)), q_l =
- * e4m3(fp32(fmax * a_l / amax_t)), acc = acc * amax_{t-1}/amax_t + sum q_l w[l,f]
- * (incremental form with corr = d1'/d1, tests/golden corrections.txt).
+/* The FP8 kernel's arithmetic restated (quant_gemm_sm100 in
+ * paper_2603_10026_b200/csrc/gemm_sm100.cu). Per row, per K tile of width
+ * tile_k: running absmax d1 (float32); H' reference ref = smallest power of
+ * two >= d1; q_l = e4m3(fp32(a_l * fmax/ref)) (exact power-of-two scaling,
+ * one RNE/satfinite rounding); acc = acc * ref'/ref + sum q_l w[l,f] (the
+ * incremental form with corr = d1'/d1 evaluated on the H' proxy); finalize
+ * c = acc * ref / d1 (finalize_root retarget, simulator.cpp:611-621).
  * w must already be e4m3-representable (static pre-rounded weight).
  * Rows whose absmax is 0 produce NaN (0/0), matching the reference's
- * DomainError at finalize_root (simulator.cpp:611-621).                     */
+ * DomainError at finalize_root.                                              */
 void rfo_quant_gemm_e4m3(const double* a, const double* w, int64_t M, int64_t K,
                          int64_t N, double fmax, int64_t tile_k, double* d1, double* c,
                          int threads);

@@ -187,6 +187,238 @@ __global__ void __launch_bounds__(NT, 1)
 
 }  // namespace rms
 
+
+// ========================================================= QUANT_GEMM_E4M3 ==
+
+namespace qnt {
+
+constexpr int BK = 128;   // e4m3: one 128 B swizzle row; the bf16 A tile is 2 chunks
+constexpr int BNQ = 512;  // two N=256 MMAs per K step (amortises the in-loop quantiser)
+constexpr int SA = 2, SW = 2, S8 = 2;
+constexpr int NT = 192;   // warps 0-3 quantiser + epilogue, 4 TMA, 5 MMA
+constexpr int ABF_BYTES = BM * BK * 2;  // 32 KB
+constexpr int W_BYTES = BNQ * BK;       // 64 KB
+constexpr int A8_BYTES = BM * BK;       // 16 KB
+
+struct Smem {
+  uint8_t abf[SA][ABF_BYTES];
+  uint8_t w[SW][W_BYTES];
+  uint8_t a8[S8][A8_BYTES];
+  uint64_t abf_full[SA], abf_empty[SA], w_full[SW], w_empty[SW], a8_full[S8], a8_empty[S8];
+  uint64_t acc_full;
+  uint32_t tmem_base;
+};
+
+struct Params {
+  float* d1;
+  int* domain_flag;
+  int64_t k;
+  float fmax;
+};
+
+__device__ __forceinline__ float pow2_ceil(float x) {
+  if (!(x > 0.f)) return 0.f;
+  const uint32_t b = __float_as_uint(x);
+  return (b & 0x007fffffu) ? __uint_as_float((b & 0x7f800000u) + 0x00800000u) : x;
+}
+
+__device__ __forceinline__ uint32_t absmax_bf16x2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("max.xorsign.abs.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+// 2 bf16 (packed) * scale -> 2 e4m3 (RNE, satfinite) in the low 16 bits.
+__device__ __forceinline__ uint32_t quant_pair(uint32_t u, uint64_t scale2) {
+  uint64_t x, y;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "r"(u << 16), "r"(u & 0xffff0000u));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(y) : "l"(x), "l"(scale2));
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(y));
+  return pack_e4m3x2(lo, hi);
+}
+
+__global__ void __launch_bounds__(NT, 1)
+    quant_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tw,
+                      const __grid_constant__ CUtensorMap tc, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = warp_id();
+  const int n0 = blockIdx.x * BNQ;
+  const int m0 = blockIdx.y * BM;
+  const int kt = static_cast<int>(p.k / BK);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < SA; ++i) {
+      mbar_init(&s.abf_full[i], 1);
+      mbar_init(&s.abf_empty[i], 4);
+    }
+    for (int i = 0; i < SW; ++i) {
+      mbar_init(&s.w_full[i], 1);
+      mbar_init(&s.w_empty[i], 1);
+    }
+    for (int i = 0; i < S8; ++i) {
+      mbar_init(&s.a8_full[i], 4);
+      mbar_init(&s.a8_empty[i], 1);
+    }
+    mbar_init(&s.acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<512>(&s.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+
+  if (warp == 4) {
+    if (elect_one()) {
+      prefetch_tmap(&ta);
+      prefetch_tmap(&tw);
+      prefetch_tmap(&tc);
+      for (int t = 0; t < kt; ++t) {
+        const int sa = t % SA, sw = t % SW;
+        mbar_wait(&s.abf_empty[sa], ((t / SA) & 1) ^ 1);
+        mbar_arrive_expect_tx(&s.abf_full[sa], ABF_BYTES);
+        tma_load_2d(s.abf[sa], &ta, &s.abf_full[sa], t * BK, m0, kEvictFirst);
+        tma_load_2d(s.abf[sa] + BM * 128, &ta, &s.abf_full[sa], t * BK + 64, m0, kEvictFirst);
+        mbar_wait(&s.w_empty[sw], ((t / SW) & 1) ^ 1);
+        mbar_arrive_expect_tx(&s.w_full[sw], W_BYTES);
+        tma_load_2d(s.w[sw], &tw, &s.w_full[sw], t * BK, n0, kEvictLast);
+        tma_load_2d(s.w[sw] + 256 * 128, &tw, &s.w_full[sw], t * BK, n0 + 256, kEvictLast);
+      }
+    }
+  } else if (warp == 5) {
+    const uint32_t idesc = idesc_f8(BM, 256);
+    const bool leader = elect_one();
+    for (int t = 0; t < kt; ++t) {
+      const int sw = t % SW, s8 = t % S8;
+      mbar_wait(&s.w_full[sw], (t / SW) & 1);
+      mbar_wait(&s.a8_full[s8], (t / S8) & 1);
+      tc_fence_after();
+      if (leader) {
+        const uint32_t a = smem_u32(s.a8[s8]), b = smem_u32(s.w[sw]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int ks = 0; ks < BK / 32; ++ks)
+            mma_f8_ss(tmem + h * 256, sdesc_kmajor_sw128(a + ks * 32),
+                      sdesc_kmajor_sw128(b + h * 256 * 128 + ks * 32), idesc, (t | ks) != 0);
+        mma_commit(&s.w_empty[sw]);
+        mma_commit(&s.a8_empty[s8]);
+        if (t + 1 == kt) mma_commit(&s.acc_full);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---- reduction 1 (running absmax) + e4m3 quantisation of A, thread = row ----
+    const int r = threadIdx.x;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    float amax = 0.f, ref = 0.f;
+    for (int t = 0; t < kt; ++t) {
+      const int sa = t % SA, s8 = t % S8;
+      mbar_wait(&s.abf_full[sa], (t / SA) & 1);
+      uint32_t x[64];  // logical K order: x[8c + 4*vv + i] covers K = 64c + 8vv + 2i .. +1
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const uint4 q = *reinterpret_cast<const uint4*>(s.abf[sa] + c * (BM * 128) + sw128(r, v));
+          x[32 * c + 4 * v + 0] = q.x;
+          x[32 * c + 4 * v + 1] = q.y;
+          x[32 * c + 4 * v + 2] = q.z;
+          x[32 * c + 4 * v + 3] = q.w;
+        }
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&s.abf_empty[sa]);
+      uint32_t mx = absmax_bf16x2(x[0], x[1]);
+#pragma unroll
+      for (int i = 2; i < 64; ++i) mx = absmax_bf16x2(mx, x[i]);
+      const float tile_max = fmaxf(__uint_as_float((mx << 16) & 0x7fffffffu),
+                                   __uint_as_float(mx & 0x7fff0000u));
+      amax = fmaxf(amax, tile_max);  // d1: store-prev (ref) / reduce
+      const float nref = pow2_ceil(amax);
+      // Eq.17 correction of the accumulator rows: corr = ref'/ref (powers of two)
+      const bool changed = t > 0 && nref != ref;
+      if (__any_sync(0xffffffffu, changed)) {
+        const int sp = (t - 1) % S8;
+        mbar_wait(&s.a8_empty[sp], ((t - 1) / S8) & 1);  // MMA of tile t-1 complete
+        tc_fence_after();
+        const float f = changed ? ref / nref : 1.f;
+#pragma unroll 1
+        for (int c = 0; c < 2 * 256 / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tmem + lane_off + c * 32, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * f);
+          tmem_st32(tmem + lane_off + c * 32, v);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+      }
+      ref = nref;
+      const float sc = p.fmax / ref;  // exact: fmax * 2^-e
+      uint64_t sc2;
+      asm("mov.b64 %0, {%1, %1};" : "=l"(sc2) : "f"(sc));
+      mbar_wait(&s.a8_empty[s8], ((t / S8) & 1) ^ 1);
+      uint8_t* dst = s.a8[s8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {  // logical 16-element unit u = K [16u, 16u+16)
+        uint32_t w[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const uint32_t lo = quant_pair(x[8 * u + 2 * h], sc2);
+          const uint32_t hi = quant_pair(x[8 * u + 2 * h + 1], sc2);
+          w[h] = (lo & 0xffffu) | (hi << 16);
+        }
+        *reinterpret_cast<uint4*>(dst + sw128(r, u)) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&s.a8_full[s8]);
+    }
+    // ---- finalize_root: retarget H'(ref) -> H(d1): c = acc * ref / d1 ----
+    const float fin = ref / amax;  // 0/0 -> NaN for an all-zero row (DomainError)
+    if (!(amax > 0.f)) atomicExch(p.domain_flag, 1);
+    if (blockIdx.x == 0) p.d1[m0 + r] = amax;
+    named_bar_sync(1, 128);
+    mbar_wait(&s.acc_full, 0);
+    tc_fence_after();
+    uint8_t* stage = s.abf[0];  // 192 KB of drained stages: C half-tile staging (128 KB)
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_off + h * 256 + c * 32, v);
+        tmem_ld_wait();
+        uint8_t* chunk = stage + c * (BM * 128);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          *reinterpret_cast<float4*>(chunk + sw128(r, u)) =
+              make_float4(__uint_as_float(v[4 * u]) * fin, __uint_as_float(v[4 * u + 1]) * fin,
+                          __uint_as_float(v[4 * u + 2]) * fin, __uint_as_float(v[4 * u + 3]) * fin);
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          tma_store_2d(&tc, stage + c * (BM * 128), n0 + h * 256 + 32 * c, m0);
+        bulk_commit();
+        bulk_wait_read0();
+      }
+      named_bar_sync(1, 128);
+    }
+    if (threadIdx.x == 0) bulk_wait0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace qnt
+
 // ============================================================== packing ====
 
 // w [K,N] f32 (reduce-axis major) -> out [N,K]: transposed, g folded (rms) or
@@ -223,6 +455,7 @@ __global__ void pack_kernel(const float* __restrict__ w, const float* __restrict
 bool gemm_sm100_supports(int pattern, int64_t m, int64_t n, int64_t k) {
   if (m % BM || n % BN) return false;
   if (pattern == RF_PATTERN_RMSNORM_GEMM) return k % rms::BK == 0;
+  if (pattern == RF_PATTERN_QUANT_GEMM_E4M3) return n % qnt::BNQ == 0 && k % qnt::BK == 0;
   return false;
 }
 
@@ -257,7 +490,37 @@ cudaError_t launch_rms_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_quant_gemm_sm100(const GemmArgs&, cudaStream_t) { return cudaErrorNotSupported; }
+cudaError_t launch_quant_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
+  if (!gemm_sm100_supports(RF_PATTERN_QUANT_GEMM_E4M3, g.m, g.n, g.k)) return cudaErrorNotSupported;
+  CUtensorMap ta, tw, tc;
+  {
+    const uint64_t dims[2] = {static_cast<uint64_t>(g.k), static_cast<uint64_t>(g.m)};
+    const uint64_t str[1] = {static_cast<uint64_t>(g.k) * 2};
+    const uint32_t box[2] = {64, BM};
+    if (!make_tmap(&ta, g.a, 2, dims, str, box, 2)) return cudaErrorInvalidValue;
+  }
+  {
+    const uint64_t dims[2] = {static_cast<uint64_t>(g.k), static_cast<uint64_t>(g.n)};
+    const uint64_t str[1] = {static_cast<uint64_t>(g.k)};
+    const uint32_t box[2] = {qnt::BK, 256};
+    if (!make_tmap(&tw, g.b, 2, dims, str, box, 1)) return cudaErrorInvalidValue;
+  }
+  {
+    const uint64_t dims[2] = {static_cast<uint64_t>(g.n), static_cast<uint64_t>(g.m)};
+    const uint64_t str[1] = {static_cast<uint64_t>(g.n) * 4};
+    const uint32_t box[2] = {32, BM};
+    if (!make_tmap(&tc, g.c, 2, dims, str, box, 4)) return cudaErrorInvalidValue;
+  }
+  qnt::Params p{g.d1, g.domain_flag, g.k, g.fmax};
+  const size_t smem = sizeof(qnt::Smem) + 1024;
+  cudaError_t e = cudaFuncSetAttribute(qnt::quant_gemm_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  dim3 grid(static_cast<unsigned>(g.n / qnt::BNQ), static_cast<unsigned>(g.m / BM));
+  qnt::quant_gemm_kernel<<<grid, qnt::NT, smem, st>>>(ta, tw, tc, p);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_pack_e4m3(const float* w, int64_t k, int64_t n, uint8_t* packed, cudaStream_t st) {
   dim3 grid(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((k + 31) / 32));

@@ -78,3 +78,92 @@ def test_rmsnorm_gemm_unsupported_shape_raises():
 
     with pytest.raises(UnsupportedPattern):
         rmsnorm_gemm_plan(100, 64, 256)
+
+
+# ------------------------------------------------------------------- quant --
+
+def _quant_run(a, w, fmax=448.0):
+    import torch
+    from paper_2603_10026_b200 import quant_gemm, quant_gemm_plan
+
+    M, K = a.shape
+    N = w.shape[1]
+    p = quant_gemm_plan(M, K, N, fmax)
+    assert "tcgen05" in p.info["kernel"]
+    wp = p.pack_weight(torch.tensor(w, dtype=torch.float32).cuda())
+    ad = torch.tensor(a).to(torch.bfloat16).cuda()
+    amax, c = quant_gemm(ad, wp, fmax)
+    torch.cuda.synchronize()
+    w8 = wp.view(torch.float8_e4m3fn).double().cpu().numpy().T  # [K, N] static e4m3 weight
+    return amax.double().cpu().numpy(), c.double().cpu().numpy(), w8, p
+
+
+@pytest.mark.parametrize("shape", [(128, 128, 512), (256, 1024, 1024), (128, 2048, 512)])
+def test_quant_gemm_vs_oracle(shape):
+    M, K, N = shape
+    rng = np.random.default_rng(M + K + N)
+    a = O.round_bf16(rng.uniform(-2, 2, (M, K)))
+    w = rng.uniform(-1, 1, (K, N))
+    amax, c, w8, _ = _quant_run(a, w)
+    assert np.array_equal(w8, O.round_e4m3(w))  # packing = RNE satfinite e4m3
+    d1, cr = O.quant_gemm_e4m3(a, w8, tile_k=128)  # same rounded inputs, kernel's scheme
+    assert _err(amax, d1) == 0.0  # absmax is exact
+    assert _err(c, cr) < TOL
+    assert _err(c, cr) < 1e-3  # same quantisation decisions: only fp32 accumulation differs
+    # deviation from the unrounded real-arithmetic reference (reported, not the gate)
+    _, creal = O.quant_gemm(a, w)
+    rel = np.sqrt(np.mean((c - creal) ** 2)) / np.sqrt(np.mean(creal ** 2))
+    assert rel < 0.06
+
+
+def test_quant_gemm_rescale_path():
+    """Magnitudes growing along K force ref (power of two >= running absmax) to
+    change on many tiles: the in-loop accumulator correction ref'/ref runs."""
+    M, K, N = 128, 1024, 512
+    rng = np.random.default_rng(3)
+    grow = 2.0 ** (np.arange(K) // 128)  # x2 per tile
+    a = O.round_bf16(rng.uniform(-1, 1, (M, K)) * grow)
+    w = rng.uniform(-1, 1, (K, N))
+    amax, c, w8, _ = _quant_run(a, w)
+    d1, cr = O.quant_gemm_e4m3(a, w8, tile_k=128)
+    assert _err(amax, d1) == 0.0
+    assert _err(c, cr) < 1e-3
+
+
+def test_quant_gemm_known_answer_and_domain_error():
+    """test_simulator.cpp:53-68: a=[1], w=[[2]] -> d1 = 1, d2 = 896 (padded to a
+    tile); an all-zero row is the reference's DomainError (0/0) at finalize."""
+    import torch
+    from paper_2603_10026_b200 import DomainError
+
+    a = np.zeros((128, 128))
+    a[0, 0] = 1.0
+    a[1, :] = 0.0  # all-zero row
+    a[2:, :] = 0.5
+    w = np.zeros((128, 512))
+    w[0, 0] = 2.0
+    amax, c, _, p = _quant_run(a, w)
+    assert amax[0] == 1.0 and c[0, 0] == 896.0
+    assert amax[1] == 0.0 and np.isnan(c[1]).all()
+    with pytest.raises(DomainError):
+        p.check_domain(torch.cuda.current_stream())
+    p.check_domain(torch.cuda.current_stream())  # flag cleared
+
+
+@pytest.mark.parametrize("name", O.golden_names("quant_gemm_"))
+def test_quant_gemm_against_reference_goldens(name):
+    gd = O.load_golden(name)
+    K, N = gd["in.w"].shape
+    Kp = -(-K // 128) * 128
+    a = np.zeros((128, Kp))
+    a[0, :K] = gd["in.a"]
+    w = np.zeros((Kp, 512))
+    w[:K, :N] = gd["in.w"]
+    amax, c, w8, _ = _quant_run(O.round_bf16(a), w)
+    d1, cr = O.quant_gemm_e4m3(O.round_bf16(a[:1]), w8, tile_k=128)
+    assert _err(amax[:1], d1) == 0.0
+    assert _err(c[0], cr[0]) < 1e-3
+    # the reference's unrounded result: within FP8 input-rounding error
+    rel = np.sqrt(np.mean((c[0, :N] - gd["oracle.d2"]) ** 2)) / np.sqrt(np.mean(gd["oracle.d2"] ** 2))
+    assert rel < 0.06
+    assert abs(amax[0] - gd["oracle.d1"][0]) <= 2e-2 * gd["oracle.d1"][0]
