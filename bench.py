@@ -176,38 +176,81 @@ def dist_setup(args):
     return world, rank, local
 
 
-def make_inputs(cfg, device):
-    import torch
+class Workload:
+    """Plan + device/host buffers for one BASELINE config (plan-time work, e.g.
+    weight packing, happens here — outside every timed region)."""
 
-    g = torch.Generator(device=device)
-    g.manual_seed(1234)
-    if cfg["pattern"] == "attention":
-        dt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
-        B, H, Sq, Skv, D = cfg["B"], cfg["H"], cfg["Sq"], cfg["Skv"], cfg["D"]
-        q = ((torch.rand(B, H, Sq, D, device=device, generator=g) * 2 - 1) / D ** 0.5).to(dt)
-        k = (torch.rand(B, H, Skv, D, device=device, generator=g) * 2 - 1).to(dt)
-        v = (torch.rand(B, H, Skv, D, device=device, generator=g) * 2 - 1).to(dt)
-        return [q, k, v]
-    raise SystemExit(f"config {cfg['name']} not wired in bench yet")
+    def __init__(self, cfg, dev):
+        import torch
+
+        from paper_2603_10026_b200 import Desc, Plan
+        from paper_2603_10026_b200 import _native as N
+
+        g = torch.Generator(device=dev)
+        g.manual_seed(1234)
+        rnd = lambda *shape: torch.rand(*shape, device=dev, generator=g)  # noqa: E731
+        self.cfg = cfg
+        pat = cfg["pattern"]
+        if pat == "attention":
+            dt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
+            B, H, Sq, Skv, D = cfg["B"], cfg["H"], cfg["Sq"], cfg["Skv"], cfg["D"]
+            q = ((rnd(B, H, Sq, D) * 2 - 1) / D ** 0.5).to(dt)
+            k = (rnd(B, H, Skv, D) * 2 - 1).to(dt)
+            v = (rnd(B, H, Skv, D) * 2 - 1).to(dt)
+            self.plan = Plan(Desc(N.RF_PATTERN_ATTENTION, cfg["dtype"], rows=Sq, len=Skv,
+                                  free_len=D, batch=B, heads=H, segments=cfg.get("segments", 1),
+                                  device=dev.index))
+            self.inputs = [q, k, v]
+            m = torch.empty(B, H, Sq, device=dev)
+            self.outputs = [m, torch.empty_like(m), torch.empty_like(q)]
+            self.step_inputs = [0, 1, 2]  # all inputs are per-step data
+            self.data = "synthetic (uniform, make_attention distributions; q pre-scaled by 1/sqrt(D))"
+        else:
+            M, K, Nn = cfg["M"], cfg["K"], cfg["N"]
+            if pat == "quant":
+                a = (rnd(M, K) * 4 - 2).bfloat16()  # make_quant_gemm: a ~ U(-2, 2)
+                self.plan = Plan(Desc(N.RF_PATTERN_QUANT_GEMM_E4M3, "bf16", rows=M, len=K,
+                                      free_len=Nn, device=dev.index))
+                w = rnd(K, Nn) * 2 - 1  # w ~ U(-1, 1)
+                wp = self.plan.pack_weight(w)
+                del w
+                self.outputs = [torch.empty(M, device=dev), torch.empty(M, Nn, device=dev)]
+                self.data = "synthetic (make_quant_gemm distributions: a~U(-2,2), w~U(-1,1) packed e4m3)"
+            else:
+                a = (rnd(M, K) * 2 - 1).bfloat16()
+                self.plan = Plan(Desc(N.RF_PATTERN_RMSNORM_GEMM, "bf16", rows=M, len=K,
+                                      free_len=Nn, eps=1e-6, device=dev.index))
+                w = rnd(K, Nn) * 2 - 1
+                gam = rnd(K) * 2 - 1
+                wp = self.plan.pack_weight(w, gam)
+                del w
+                self.outputs = [torch.empty(M, device=dev),
+                                torch.empty(M, Nn, dtype=torch.bfloat16, device=dev)]
+                self.data = "synthetic (DSL wrap_spec convention: x, g, w ~ U(-1,1); g folded into bf16 W)"
+            self.inputs = [a, wp]
+            self.step_inputs = [0]  # the packed weight is plan-time resident
+        torch.cuda.synchronize()
+
+    def run(self, stream):
+        self.plan.run(self.inputs, self.outputs, stream)
+
+    def host_buffers(self):
+        import torch
+
+        hin = [x.cpu().pin_memory() if i in self.step_inputs else x
+               for i, x in enumerate(self.inputs)]
+        hout = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in self.outputs]
+        return hin, hout
 
 
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
 
-    from paper_2603_10026_b200 import Desc, Plan
-    from paper_2603_10026_b200 import _native as N
-
     world, rank, local = dist_setup(args)
     dev = torch.device("cuda", torch.cuda.current_device())
-    inputs = make_inputs(cfg, dev)
-    B, H, Sq, Skv, D = cfg["B"], cfg["H"], cfg["Sq"], cfg["Skv"], cfg["D"]
-    plan = Plan(Desc(N.RF_PATTERN_ATTENTION, cfg["dtype"], rows=Sq, len=Skv, free_len=D, batch=B,
-                     heads=H, segments=cfg.get("segments", 1), device=dev.index))
-    m = torch.empty(B, H, Sq, device=dev)
-    l = torch.empty_like(m)
-    o = torch.empty_like(inputs[0])
-    outs = [m, l, o]
+    wl = Workload(cfg, dev)
+    plan = wl.plan
     stream = torch.cuda.Stream(device=dev)
     flops, nbytes = work_of(cfg)
 
@@ -217,7 +260,7 @@ def run_ours(args, cfg):
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
-            plan.run(inputs, outs, stream)
+            wl.run(stream)
         stream.synchronize()
         barrier()
         torch.cuda.synchronize()
@@ -226,7 +269,7 @@ def run_ours(args, cfg):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         ev[0].record(stream)
         for i in range(args.steps):
-            plan.run(inputs, outs, stream)
+            wl.run(stream)
             ev[i + 1].record(stream)
         stream.synchronize()
         torch.cuda.synchronize()
@@ -242,8 +285,7 @@ def run_ours(args, cfg):
     value = flops * world * args.steps / (total_ms * 1e-3) / 1e12
 
     # ---- end-to-end through the C-ABI host path (pinned host buffers) ----
-    hin = [x.cpu().pin_memory() for x in inputs]
-    hout = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in outs]
+    hin, hout = wl.host_buffers()
     for _ in range(2):
         plan.run_host(hin, hout)
     barrier()
@@ -256,7 +298,7 @@ def run_ours(args, cfg):
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_s = float(te.item())
-    h2d = sum(x.numel() * x.element_size() for x in hin)
+    h2d = sum(hin[i].numel() * hin[i].element_size() for i in wl.step_inputs)
     d2h = sum(x.numel() * x.element_size() for x in hout)
 
     if rank != 0:
@@ -268,14 +310,30 @@ def run_ours(args, cfg):
     kern_ms = statistics.mean(per_step)
     if bound == "hbm":
         achieved = nbytes / (kern_ms * 1e-3) / 1e9
-        peak, unit = pk["hbm_gbs"], "GB/s"
+        peak, unit, psrc = pk["hbm_gbs"], "GB/s", f"{pk_src} hbm_gbs (MEASURED_PEAKS.json)"
+    elif cfg["dtype"] == "f32":
+        # fp32 SIMT FMA peak: 148 SMs x 128 lanes x 2 FLOP x max SM clock
+        peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        achieved = flops / (kern_ms * 1e-3) / 1e12
+        unit, psrc, bound = "TFLOP/s", "fp32 SIMT FMA peak at max SM clock (no tensor cores on this path)", "compute"
     else:
         achieved = flops / (kern_ms * 1e-3) / 1e12
-        peak, unit = pk["bf16_tflops"], "TFLOP/s"
+        unit = "TFLOP/s"
+        if cfg["pattern"] == "quant":
+            peak = 2 * pk["bf16_tflops"]
+            psrc = f"2 x {pk_src} bf16 burst (dense FP8 = 2x BF16 tensor rate on sm_100)"
+        else:
+            peak = pk["bf16_tflops"]
+            psrc = f"{pk_src} bf16 burst (MEASURED_PEAKS.json)"
     traffic = None
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
         traffic = json.load(open(prof)).get(cfg["name"].split(":")[0])
+    conf = {"workload": cfg["name"], "kernel": plan.info["kernel"],
+            "parallelism": f"batch/head (or token) shards x{world}, no data-path collective",
+            "l2": f"step inputs {sum(wl.inputs[i].numel() * wl.inputs[i].element_size() for i in wl.step_inputs) / 1e6:.0f} MB"
+                  " vs 126 MB L2, no flush"}
+    conf.update({k: v for k, v in cfg.items() if k not in ("name", "pattern", "dtype")})
     line = {
         "metric": METRIC,
         "value": round(value, 3),
@@ -287,16 +345,12 @@ def run_ours(args, cfg):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": cfg["dtype"],
-        "data": "synthetic (uniform, make_attention distributions; q pre-scaled by 1/sqrt(D))",
-        "config": {"workload": cfg["name"], "B": B, "H": H, "Sq": Sq, "Skv": Skv, "D": D,
-                   "segments": cfg.get("segments", 1), "kernel": plan.info["kernel"],
-                   "parallelism": f"batch/head shards x{world} (no collective)",
-                   "l2": f"inputs {sum(x.numel() * x.element_size() for x in inputs) / 1e6:.0f} MB "
-                         "> 126 MB L2, no flush"},
-        "roofline": {"bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "peak_source": f"{pk_src} (MEASURED_PEAKS.json burst)",
+        "dtype": {"quant": "e4m3 (bf16 in)", "rms": "bf16"}.get(cfg["pattern"], cfg["dtype"]),
+        "data": wl.data,
+        "config": conf,
+        "roofline": {"bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 1),
+                     "unit": unit, "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "peak_source": psrc,
                      "algorithmic": {"flops": flops, "bytes": nbytes}},
         "e2e": {"value": round(flops * e2e_steps / e2e_s / 1e12, 3), "unit": "TFLOP/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
