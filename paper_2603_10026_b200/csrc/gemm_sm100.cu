@@ -40,6 +40,21 @@ constexpr int BN = 256;
 __device__ __forceinline__ float bf_lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
 
+// Grouped rasterisation: CTAs walk column panels of `gn` N-tiles over all
+// M-tiles, so a panel of the static weight (gn x BN x K) stays L2-resident
+// while the activations stream, instead of re-reading the whole weight from
+// HBM once per M-tile (the output stream would evict it).
+__device__ __forceinline__ void tile_of(int b, int mt_count, int nt_count, int gn, int& mt,
+                                        int& nt) {
+  const int per_group = gn * mt_count;
+  const int g = b / per_group;
+  const int first_n = g * gn;
+  const int width = min(gn, nt_count - first_n);
+  const int w = b - g * per_group;
+  mt = w / width;
+  nt = first_n + w % width;
+}
+
 // Offset of logical 16-byte unit u of row r inside a [rows x 128 B] SWIZZLE_128B tile.
 __device__ __forceinline__ uint32_t sw128(uint32_t r, uint32_t u) {
   return (r >> 3) * 1024 + (r & 7) * 128 + ((u ^ (r & 7)) << 4);
@@ -67,7 +82,7 @@ struct Params {
   float* d1;
   int64_t k;
   float inv_k, eps;
-  int write_d1_tile;  // blockIdx.x that writes d1
+  int mt_count, nt_count, group_n;
 };
 
 __global__ void __launch_bounds__(NT, 1)
@@ -76,8 +91,10 @@ __global__ void __launch_bounds__(NT, 1)
   extern __shared__ uint8_t smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = warp_id();
-  const int n0 = blockIdx.x * BN;
-  const int m0 = blockIdx.y * BM;
+  int mt, nt;
+  tile_of(blockIdx.x, p.mt_count, p.nt_count, p.group_n, mt, nt);
+  const int n0 = nt * BN;
+  const int m0 = mt * BM;
   const int kt = static_cast<int>(p.k / BK);
 
   if (threadIdx.x == 0) {
@@ -132,10 +149,12 @@ __global__ void __launch_bounds__(NT, 1)
     for (int t = 0; t < kt; ++t) {
       const int st = t % STAGES;
       mbar_wait(&s.full[st], (t / STAGES) & 1);
-      const uint8_t* row = s.a[st] + (r >> 3) * 1024 + (r & 7) * 128;
+      const uint32_t row = smem_u32(s.a[st]) + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const uint4 v = *reinterpret_cast<const uint4*>(row + 16 * u);
+        // physical unit u ^ (r & 7): conflict-free across the 8 rows of a phase
+        // (the sum of squares does not depend on the order within the row)
+        const uint4 v = lds128(row + ((u ^ (r & 7)) << 4));
         const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -149,18 +168,18 @@ __global__ void __launch_bounds__(NT, 1)
     }
     // ---- finalize: d2 = acc * 1/sqrt(d1/K + eps) -> bf16 -> smem -> TMA store ----
     const float inv = rsqrtf(fmaf(ss, p.inv_k, p.eps));
-    if (blockIdx.x == p.write_d1_tile) p.d1[m0 + r] = ss;
+    if (nt == 0) p.d1[m0 + r] = ss;
     named_bar_sync(1, 128);  // every stats warp is done reading the stages
     mbar_wait(&s.acc_full, 0);
     tc_fence_after();
-    uint8_t* stage = s.a[0];  // all stages are drained: reuse 64 KB as the Y tile
+    const uint32_t stage = smem_u32(s.a[0]);  // all stages are drained: reuse 64 KB as the Y tile
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
 #pragma unroll
     for (int c = 0; c < BN / 32; ++c) {
       uint32_t v[32];
       tmem_ld32(tmem + lane_off + c * 32, v);
       tmem_ld_wait();
-      uint8_t* chunk = stage + (c >> 1) * (BM * 128);
+      const uint32_t chunk = stage + (c >> 1) * (BM * 128);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         uint4 w;
@@ -168,14 +187,14 @@ __global__ void __launch_bounds__(NT, 1)
         w.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
         w.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
         w.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
-        *reinterpret_cast<uint4*>(chunk + sw128(r, (c & 1) * 4 + q)) = w;
+        sts128(chunk + sw128(r, (c & 1) * 4 + q), w);
       }
     }
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
     if (threadIdx.x == 0) {
 #pragma unroll
-      for (int c = 0; c < BN / 64; ++c) tma_store_2d(&ty, stage + c * (BM * 128), n0 + 64 * c, m0);
+      for (int c = 0; c < BN / 64; ++c) tma_store_2d(&ty, s.a[0] + c * (BM * 128), n0 + 64 * c, m0);
       bulk_commit();
       bulk_wait0();
     }
@@ -214,6 +233,7 @@ struct Params {
   int* domain_flag;
   int64_t k;
   float fmax;
+  int mt_count, nt_count, group_n;
 };
 
 __device__ __forceinline__ float pow2_ceil(float x) {
@@ -244,8 +264,10 @@ __global__ void __launch_bounds__(NT, 1)
   extern __shared__ uint8_t smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = warp_id();
-  const int n0 = blockIdx.x * BNQ;
-  const int m0 = blockIdx.y * BM;
+  int mt, nt;
+  tile_of(blockIdx.x, p.mt_count, p.nt_count, p.group_n, mt, nt);
+  const int n0 = nt * BNQ;
+  const int m0 = mt * BM;
   const int kt = static_cast<int>(p.k / BK);
 
   if (threadIdx.x == 0) {
@@ -322,7 +344,7 @@ __global__ void __launch_bounds__(NT, 1)
       for (int c = 0; c < 2; ++c)
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
-          const uint4 q = *reinterpret_cast<const uint4*>(s.abf[sa] + c * (BM * 128) + sw128(r, v));
+          const uint4 q = lds128(smem_u32(s.abf[sa]) + c * (BM * 128) + sw128(r, v));
           x[32 * c + 4 * v + 0] = q.x;
           x[32 * c + 4 * v + 1] = q.y;
           x[32 * c + 4 * v + 2] = q.z;
@@ -361,7 +383,7 @@ __global__ void __launch_bounds__(NT, 1)
       uint64_t sc2;
       asm("mov.b64 %0, {%1, %1};" : "=l"(sc2) : "f"(sc));
       mbar_wait(&s.a8_empty[s8], ((t / S8) & 1) ^ 1);
-      uint8_t* dst = s.a8[s8];
+      const uint32_t dst = smem_u32(s.a8[s8]);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {  // logical 16-element unit u = K [16u, 16u+16)
         uint32_t w[4];
@@ -371,7 +393,7 @@ __global__ void __launch_bounds__(NT, 1)
           const uint32_t hi = quant_pair(x[8 * u + 2 * h + 1], sc2);
           w[h] = (lo & 0xffffu) | (hi << 16);
         }
-        *reinterpret_cast<uint4*>(dst + sw128(r, u)) = make_uint4(w[0], w[1], w[2], w[3]);
+        sts128(dst + sw128(r, u), make_uint4(w[0], w[1], w[2], w[3]));
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -380,11 +402,11 @@ __global__ void __launch_bounds__(NT, 1)
     // ---- finalize_root: retarget H'(ref) -> H(d1): c = acc * ref / d1 ----
     const float fin = ref / amax;  // 0/0 -> NaN for an all-zero row (DomainError)
     if (!(amax > 0.f)) atomicExch(p.domain_flag, 1);
-    if (blockIdx.x == 0) p.d1[m0 + r] = amax;
+    if (nt == 0) p.d1[m0 + r] = amax;
     named_bar_sync(1, 128);
     mbar_wait(&s.acc_full, 0);
     tc_fence_after();
-    uint8_t* stage = s.abf[0];  // 192 KB of drained stages: C half-tile staging (128 KB)
+    const uint32_t stage = smem_u32(s.abf[0]);  // 192 KB of drained stages: C half-tile staging
 #pragma unroll 1
     for (int h = 0; h < 2; ++h) {
 #pragma unroll 1
@@ -392,19 +414,21 @@ __global__ void __launch_bounds__(NT, 1)
         uint32_t v[32];
         tmem_ld32(tmem + lane_off + h * 256 + c * 32, v);
         tmem_ld_wait();
-        uint8_t* chunk = stage + c * (BM * 128);
+        const uint32_t chunk = stage + c * (BM * 128);
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          *reinterpret_cast<float4*>(chunk + sw128(r, u)) =
-              make_float4(__uint_as_float(v[4 * u]) * fin, __uint_as_float(v[4 * u + 1]) * fin,
-                          __uint_as_float(v[4 * u + 2]) * fin, __uint_as_float(v[4 * u + 3]) * fin);
+          sts128(chunk + sw128(r, u),
+                 make_uint4(__float_as_uint(__uint_as_float(v[4 * u]) * fin),
+                            __float_as_uint(__uint_as_float(v[4 * u + 1]) * fin),
+                            __float_as_uint(__uint_as_float(v[4 * u + 2]) * fin),
+                            __float_as_uint(__uint_as_float(v[4 * u + 3]) * fin)));
       }
       fence_proxy_async_smem();
       named_bar_sync(1, 128);
       if (threadIdx.x == 0) {
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-          tma_store_2d(&tc, stage + c * (BM * 128), n0 + h * 256 + 32 * c, m0);
+          tma_store_2d(&tc, s.abf[0] + c * (BM * 128), n0 + h * 256 + 32 * c, m0);
         bulk_commit();
         bulk_wait_read0();
       }
@@ -480,12 +504,13 @@ cudaError_t launch_rms_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
     const uint32_t box[2] = {64, BM};
     if (!make_tmap(&ty, g.c, 2, dims, str, box, 2)) return cudaErrorInvalidValue;
   }
-  rms::Params p{g.d1, g.k, 1.f / static_cast<float>(g.k), g.eps, 0};
+  rms::Params p{g.d1, g.k, 1.f / static_cast<float>(g.k), g.eps, static_cast<int>(g.m / BM),
+                static_cast<int>(g.n / BN), 8};
   const size_t smem = sizeof(rms::Smem) + 1024;
   cudaError_t e = cudaFuncSetAttribute(rms::rms_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  dim3 grid(static_cast<unsigned>(g.n / BN), static_cast<unsigned>(g.m / BM));
+  dim3 grid(static_cast<unsigned>((g.n / BN) * (g.m / BM)));
   rms::rms_gemm_kernel<<<grid, rms::NT, smem, st>>>(ta, tb, ty, p);
   return cudaGetLastError();
 }
@@ -511,13 +536,14 @@ cudaError_t launch_quant_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
     const uint32_t box[2] = {32, BM};
     if (!make_tmap(&tc, g.c, 2, dims, str, box, 4)) return cudaErrorInvalidValue;
   }
-  qnt::Params p{g.d1, g.domain_flag, g.k, g.fmax};
+  qnt::Params p{g.d1, g.domain_flag, g.k, g.fmax, static_cast<int>(g.m / BM),
+                static_cast<int>(g.n / qnt::BNQ), 4};
   const size_t smem = sizeof(qnt::Smem) + 1024;
   cudaError_t e = cudaFuncSetAttribute(qnt::quant_gemm_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  dim3 grid(static_cast<unsigned>(g.n / qnt::BNQ), static_cast<unsigned>(g.m / BM));
+  dim3 grid(static_cast<unsigned>((g.n / qnt::BNQ) * (g.m / BM)));
   qnt::quant_gemm_kernel<<<grid, qnt::NT, smem, st>>>(ta, tw, tc, p);
   return cudaGetLastError();
 }
