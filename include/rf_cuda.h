@@ -150,6 +150,13 @@ int64_t rf_plan_launches_per_run(const rf_plan* plan);
 rf_status rf_pack_weight(const rf_plan* plan, const void* w, const void* g, void* packed,
                          void* stream);
 
+/* Host-memory variant: uploads w (and g) from host memory, packs them into a
+ * freshly allocated device buffer returned in *packed_dev (free it with
+ * rf_buffer_free). Blocking. For host-side drop-in callers without CUDA. */
+rf_status rf_pack_weight_host(const rf_plan* plan, const float* w, const float* g,
+                              void** packed_dev);
+void rf_buffer_free(void* dev_ptr);
+
 /* The fused single-loop executor: run_incremental (segments == 1) or
  * run_multisegment (segments == S: S slice partials + in-order merge) over
  * every row of the batch. Stream-ordered, non-blocking. */

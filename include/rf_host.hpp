@@ -1,0 +1,830 @@
+// rf_host.hpp — C++ host layer over librf_cuda (include/rf_cuda.h): the
+// drop-in mirror of the reference's operator API for the fused-loop path.
+//
+//   reference (proj/include/redfuse/...)          this header (namespace rfcuda)
+//   ------------------------------------          ------------------------------
+//   CascadeSpec parse_cascade(text)   cascade.hpp:88     CascadeSpec parse_cascade(text)
+//   FusedProgram derive_fused(spec)   acrf.hpp:93-94     Program plan(spec)   (pattern match)
+//   bool attention_shaped(spec)       scalar_ir.cpp:495  match_* in plan()
+//   class TensorStore                 simulator.hpp:27   class TensorStore
+//   struct OutputVal / ExecReport     simulator.hpp:49   struct OutputVal / ExecReport
+//   run_incremental(prog, cfg, store) simulator.hpp:76   run_incremental(prog, cfg, store)
+//   run_multisegment(prog,cfg,S,store)simulator.hpp:81   run_multisegment(prog, cfg, S, store)
+//   compare_reports(a, b, tol)        simulator.hpp:94   compare_reports(a, b, tol)
+//   ShapeMismatch / IncompatibleSegmentation / DomainError / NotFusable  (same names)
+//
+// Where the reference derives a generic FusedProgram by symbolic probing
+// (derive_fused, plan time), the host layer instead matches the cascade onto
+// one of librf_cuda's kernels (the structural matcher mirrors the reference's
+// own attention_shaped); cascades with no kernel raise NotFusable — there is
+// no CPU fallback. The executors run a reference row through the kernel (an
+// fp32 SIMT path for attention/softmax rows, tcgen05 kernels for the GEMM
+// patterns, padding rows to the kernels' tiles) and return an ExecReport with
+// the reference's field meanings, including the analytic load counters of the
+// fused loop (every element loaded once; simulator.cpp:571-572, 617).
+//
+// Header-only; link with librf_cuda.so. C++17.
+#pragma once
+
+#include <algorithm>
+#include <cctype>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <memory>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "rf_cuda.h"
+
+namespace rfcuda {
+
+// ------------------------------------------------------------------ errors --
+
+struct SyntaxError : std::runtime_error {
+  SyntaxError(int line, const std::string& m)
+      : std::runtime_error("line " + std::to_string(line) + ": " + m), line(line) {}
+  int line;
+};
+struct ShapeMismatch : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct IncompatibleSegmentation : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct DomainError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NotFusable : std::runtime_error {  // "no librf_cuda kernel for this cascade"
+  using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(rf_status s) {
+  if (s == RF_OK) return;
+  std::string m = std::string(rf_status_string(s)) + ": " + rf_last_error();
+  switch (s) {
+    case RF_ERR_SHAPE: throw ShapeMismatch(m);
+    case RF_ERR_SEGMENTATION: throw IncompatibleSegmentation(m);
+    case RF_ERR_DOMAIN: throw DomainError(m);
+    case RF_ERR_UNSUPPORTED: throw NotFusable(m);
+    case RF_ERR_ARG: throw std::invalid_argument(m);
+    default: throw CudaError(m);
+  }
+}
+
+// ------------------------------------------------------------- expressions --
+
+struct Node;
+using Expr = std::shared_ptr<const Node>;
+struct Node {
+  enum Kind { Num, Input, Dep, Free, Un, Bin } kind;
+  double num = 0;
+  std::string name;  // Input name / Un, Bin operator name
+  bool has_free = false;
+  int dep = 0;
+  Expr a, b;
+};
+
+inline Expr mk(Node n) { return std::make_shared<const Node>(std::move(n)); }
+inline Expr num(double v) { return mk({Node::Num, v, "", false, 0, nullptr, nullptr}); }
+inline Expr input(const std::string& n, bool fr = false) {
+  return mk({Node::Input, 0, n, fr, 0, nullptr, nullptr});
+}
+inline Expr dep(int id) { return mk({Node::Dep, 0, "", false, id, nullptr, nullptr}); }
+inline Expr un(const std::string& op, Expr a) { return mk({Node::Un, 0, op, false, 0, a, nullptr}); }
+inline Expr bin(const std::string& op, Expr a, Expr b) {
+  return mk({Node::Bin, 0, op, false, 0, a, b});
+}
+
+inline std::string render(const Expr& e) {
+  switch (e->kind) {
+    case Node::Num: {
+      char buf[64];
+      std::snprintf(buf, sizeof buf, "%.17g", e->num);
+      return buf;
+    }
+    case Node::Input: return e->name + (e->has_free ? "[l, f]" : "[l]");
+    case Node::Dep: return "d" + std::to_string(e->dep);
+    case Node::Free: return "f";
+    case Node::Un: return e->name + "(" + render(e->a) + ")";
+    case Node::Bin:
+      if (e->name == "max" || e->name == "min" || e->name == "pow")
+        return e->name + "(" + render(e->a) + ", " + render(e->b) + ")";
+      return "(" + render(e->a) + " " + e->name + " " + render(e->b) + ")";
+  }
+  return "?";
+}
+
+// Deps referenced by an expression.
+inline void deps_of(const Expr& e, std::set<int>& out) {
+  if (!e) return;
+  if (e->kind == Node::Dep) out.insert(e->dep);
+  deps_of(e->a, out);
+  deps_of(e->b, out);
+}
+
+// ----------------------------------------------------------------- cascade --
+
+struct InputDecl {
+  std::string name;
+  long long len = 0;
+  long long free_len = 0;  // 0: rank-1
+};
+struct ReductionSpec {
+  int id = 0;
+  std::string op;  // sum | prod | max | min | topk
+  int topk = 0;
+  long long free_len = 1;
+  Expr body;
+};
+struct CascadeSpec {
+  std::string name;
+  std::vector<InputDecl> inputs;
+  std::vector<ReductionSpec> reductions;
+  const InputDecl* find_input(const std::string& n) const {
+    for (const auto& i : inputs)
+      if (i.name == n) return &i;
+    return nullptr;
+  }
+  long long axis_len() const { return inputs.empty() ? 0 : inputs.front().len; }
+};
+struct TreeConfig {
+  std::vector<long long> levels;
+  int depth() const { return static_cast<int>(levels.size()) - 1; }
+};
+
+namespace detail {
+
+struct Lexer {
+  enum Kind { End, Number, Ident, Sym };
+  struct Tok {
+    Kind kind = End;
+    double num = 0;
+    std::string text;
+  };
+  Lexer(const std::string& s, int line) : s(s), line(line) { next(); }
+  const Tok& peek() const { return tok; }
+  Tok take() {
+    Tok t = tok;
+    next();
+    return t;
+  }
+  [[noreturn]] void fail(const std::string& m) const { throw SyntaxError(line, m); }
+  void next() {
+    while (pos < s.size() && std::isspace(static_cast<unsigned char>(s[pos]))) ++pos;
+    if (pos >= s.size()) {
+      tok = Tok{};
+      return;
+    }
+    const char c = s[pos];
+    if (std::isdigit(static_cast<unsigned char>(c)) || c == '.') {
+      char* end = nullptr;
+      const double v = std::strtod(s.c_str() + pos, &end);
+      tok = Tok{Number, v, ""};
+      pos = static_cast<std::size_t>(end - s.c_str());
+      return;
+    }
+    if (std::isalpha(static_cast<unsigned char>(c)) || c == '_') {
+      std::size_t j = pos;
+      while (j < s.size() && (std::isalnum(static_cast<unsigned char>(s[j])) || s[j] == '_')) ++j;
+      tok = Tok{Ident, 0, s.substr(pos, j - pos)};
+      pos = j;
+      return;
+    }
+    tok = Tok{Sym, 0, std::string(1, c)};
+    ++pos;
+  }
+  const std::string& s;
+  int line;
+  std::size_t pos = 0;
+  Tok tok;
+};
+
+inline bool sym(const Lexer::Tok& t, const char* c) { return t.kind == Lexer::Sym && t.text == c; }
+
+struct Parser {
+  Lexer lx;
+  const std::map<std::string, double>& consts;
+  Expr expr() {
+    Expr e = term();
+    while (sym(lx.peek(), "+") || sym(lx.peek(), "-")) {
+      const std::string op = lx.take().text;
+      e = bin(op, e, term());
+    }
+    return e;
+  }
+  Expr term() {
+    Expr e = primary();
+    while (sym(lx.peek(), "*") || sym(lx.peek(), "/")) {
+      const std::string op = lx.take().text;
+      e = bin(op, e, primary());
+    }
+    return e;
+  }
+  Expr primary() {
+    Lexer::Tok t = lx.take();
+    if (t.kind == Lexer::Number) return num(t.num);
+    if (sym(t, "(")) {
+      Expr e = expr();
+      if (!sym(lx.take(), ")")) lx.fail("expected )");
+      return e;
+    }
+    if (sym(t, "-")) return un("neg", primary());
+    if (t.kind != Lexer::Ident) lx.fail("unexpected token '" + t.text + "'");
+    if (sym(lx.peek(), "(")) {
+      lx.take();
+      static const std::set<std::string> unary{"exp", "abs", "log2", "ln", "sqrt", "sign"};
+      static const std::set<std::string> binary{"max", "min", "pow"};
+      Expr a = expr();
+      Expr e;
+      if (binary.count(t.text)) {
+        if (!sym(lx.take(), ",")) lx.fail(t.text + " takes two arguments");
+        e = bin(t.text, a, expr());
+      } else if (unary.count(t.text)) {
+        e = un(t.text, a);
+      } else {
+        lx.fail("unknown function " + t.text);
+      }
+      if (!sym(lx.take(), ")")) lx.fail("expected ) closing " + t.text);
+      return e;
+    }
+    if (sym(lx.peek(), "[")) {
+      lx.take();
+      const Lexer::Tok l = lx.take();
+      if (l.kind != Lexer::Ident || l.text != "l") lx.fail("reduce-axis index must be l");
+      bool fr = false;
+      Lexer::Tok close = lx.take();
+      if (sym(close, ",")) {
+        const Lexer::Tok f = lx.take();
+        if (f.kind != Lexer::Ident || f.text != "f") lx.fail("free-axis index must be f");
+        fr = true;
+        close = lx.take();
+      }
+      if (!sym(close, "]")) lx.fail("expected ]");
+      return input(t.text, fr);
+    }
+    if (t.text.size() > 1 && t.text[0] == 'd' &&
+        std::all_of(t.text.begin() + 1, t.text.end(), [](char ch) { return std::isdigit(ch); }))
+      return dep(std::atoi(t.text.c_str() + 1));
+    if (t.text == "f") return mk({Node::Free, 0, "f", false, 0, nullptr, nullptr});
+    auto it = consts.find(t.text);
+    if (it != consts.end()) return num(it->second);
+    lx.fail("unknown identifier '" + t.text + "'");
+  }
+};
+
+inline void input_refs(const Expr& e, std::vector<std::pair<std::string, bool>>& out) {
+  if (!e) return;
+  if (e->kind == Node::Input) out.emplace_back(e->name, e->has_free);
+  input_refs(e->a, out);
+  input_refs(e->b, out);
+}
+
+}  // namespace detail
+
+// The cascade DSL of the reference (cascade.cpp:331-429 grammar; proj/data/*.cascade).
+inline CascadeSpec parse_cascade(const std::string& text) {
+  CascadeSpec spec;
+  std::map<std::string, double> consts;
+  std::size_t start = 0;
+  int lineno = 0;
+  bool want_body = false;
+  while (start <= text.size()) {
+    std::size_t nl = text.find('\n', start);
+    if (nl == std::string::npos) nl = text.size();
+    std::string line = text.substr(start, nl - start);
+    start = nl + 1;
+    ++lineno;
+    const std::size_t b = line.find_first_not_of(" \t\r");
+    if (b == std::string::npos) {
+      if (nl == text.size()) break;
+      continue;
+    }
+    const bool indented = b > 0;
+    std::string t = line.substr(b);
+    if (t[0] == '#') continue;
+    if (want_body) {
+      if (!indented) throw SyntaxError(lineno, "expected an indented body");
+      detail::Parser p{detail::Lexer(t, lineno), consts};
+      spec.reductions.back().body = p.expr();
+      if (p.lx.peek().kind != detail::Lexer::End) p.lx.fail("trailing tokens after expression");
+      want_body = false;
+      continue;
+    }
+    if (indented) throw SyntaxError(lineno, "unexpected indentation");
+    std::vector<std::string> w;
+    {
+      std::size_t i = 0;
+      while (i < t.size()) {
+        while (i < t.size() && std::isspace(static_cast<unsigned char>(t[i]))) ++i;
+        std::size_t j = i;
+        while (j < t.size() && !std::isspace(static_cast<unsigned char>(t[j]))) ++j;
+        if (j > i) w.push_back(t.substr(i, j - i));
+        i = j;
+      }
+    }
+    auto len = [&](const std::string& s) {
+      char* end = nullptr;
+      const long long v = std::strtoll(s.c_str(), &end, 10);
+      if (end == s.c_str() || *end || v <= 0) throw SyntaxError(lineno, "expected a positive length");
+      return v;
+    };
+    if (w[0] == "cascade") {
+      if (w.size() != 2) throw SyntaxError(lineno, "cascade <name>");
+      spec.name = w[1];
+    } else if (w[0] == "input") {
+      if ((w.size() != 4 && w.size() != 6) || w[2] != "len")
+        throw SyntaxError(lineno, "input <name> len <L0> [free <len>]");
+      InputDecl in{w[1], len(w[3]), 0};
+      if (w.size() == 6) {
+        if (w[4] != "free") throw SyntaxError(lineno, "expected 'free'");
+        in.free_len = len(w[5]);
+      }
+      spec.inputs.push_back(in);
+    } else if (w[0] == "const") {
+      if (w.size() != 4 || w[2] != "=") throw SyntaxError(lineno, "const <name> = <number>");
+      char* end = nullptr;
+      const double v = std::strtod(w[3].c_str(), &end);
+      if (end == w[3].c_str() || *end) throw SyntaxError(lineno, "bad constant value");
+      consts[w[1]] = v;
+    } else if (w[0] == "reduce") {
+      if (w.size() < 4 || w[2] != "op") throw SyntaxError(lineno, "reduce <id> op <op> [free <len>]");
+      ReductionSpec r;
+      r.id = static_cast<int>(len(w[1]));
+      std::size_t i = 3;
+      r.op = w[i++];
+      static const std::set<std::string> ops{"sum", "prod", "max", "min", "topk"};
+      if (!ops.count(r.op)) throw SyntaxError(lineno, "unknown reduce op '" + r.op + "'");
+      if (r.op == "topk") {
+        if (i >= w.size()) throw SyntaxError(lineno, "topk needs a tuple size");
+        r.topk = static_cast<int>(len(w[i++]));
+      }
+      if (i < w.size()) {
+        if (w[i] != "free" || i + 1 >= w.size()) throw SyntaxError(lineno, "expected 'free <len>'");
+        r.free_len = len(w[i + 1]);
+        i += 2;
+      }
+      if (i != w.size()) throw SyntaxError(lineno, "trailing tokens");
+      spec.reductions.push_back(r);
+      want_body = true;
+    } else {
+      throw SyntaxError(lineno, "unknown directive '" + w[0] + "'");
+    }
+    if (nl == text.size()) break;
+  }
+  if (want_body) throw SyntaxError(lineno, "missing reduction body");
+  // structural validation (cascade.cpp:85-151 semantics)
+  if (spec.inputs.empty()) throw SyntaxError(0, "cascade declares no inputs");
+  for (const auto& in : spec.inputs)
+    if (in.len != spec.axis_len()) throw SyntaxError(0, "inputs disagree on the reduce-axis length");
+  for (std::size_t i = 0; i < spec.reductions.size(); ++i) {
+    const auto& r = spec.reductions[i];
+    if (r.id != static_cast<int>(i) + 1) throw SyntaxError(0, "reduction ids must be 1..n in order");
+    std::set<int> ds;
+    deps_of(r.body, ds);
+    for (int d : ds)
+      if (d >= r.id) throw SyntaxError(0, "forward dependency on d" + std::to_string(d));
+    std::vector<std::pair<std::string, bool>> refs;
+    detail::input_refs(r.body, refs);
+    for (const auto& [n, fr] : refs) {
+      const InputDecl* in = spec.find_input(n);
+      if (!in) throw SyntaxError(0, "unknown input " + n);
+      if (fr != (in->free_len > 0)) throw SyntaxError(0, "free-axis use of " + n + " disagrees with its decl");
+      if (fr && r.free_len != in->free_len) throw SyntaxError(0, "free length mismatch for " + n);
+    }
+  }
+  return spec;
+}
+
+// ------------------------------------------------------------ plan (match) --
+
+struct Program {
+  rf_pattern pattern = RF_PATTERN_SAFE_SOFTMAX;
+  CascadeSpec spec;
+  std::string x, v, g;  // bound input names (softmax x | attention P,V | quant a,w | rms x,g,w)
+  std::string w;
+  long long L0 = 0, free_len = 0;
+  double fmax = 448.0, eps = 0.0, inv_k = 0.0;
+};
+
+namespace detail {
+
+// Structural unification: pattern leaves "?X" bind rank-1 inputs, "?V" free
+// inputs, "?c<k>" constants; everything else must match exactly.
+struct Binding {
+  std::map<std::string, std::string> in;
+  std::map<std::string, double> c;
+};
+
+inline bool unify(const Expr& pat, const Expr& e, Binding& b) {
+  if (pat->kind == Node::Input && pat->name.size() > 1 && pat->name[0] == '?') {
+    if (e->kind != Node::Input || e->has_free != pat->has_free) return false;
+    auto it = b.in.find(pat->name);
+    if (it != b.in.end()) return it->second == e->name;
+    b.in[pat->name] = e->name;
+    return true;
+  }
+  if (pat->kind == Node::Num && std::isnan(pat->num)) {  // constant placeholder ?c
+    if (e->kind != Node::Num) return false;
+    auto it = b.c.find(pat->name);
+    if (it != b.c.end()) return it->second == e->num;
+    b.c[pat->name] = e->num;
+    return true;
+  }
+  if (pat->kind != e->kind) return false;
+  switch (pat->kind) {
+    case Node::Num: return pat->num == e->num;
+    case Node::Input: return pat->name == e->name && pat->has_free == e->has_free;
+    case Node::Dep: return pat->dep == e->dep;
+    case Node::Free: return true;
+    case Node::Un: return pat->name == e->name && unify(pat->a, e->a, b);
+    case Node::Bin: return pat->name == e->name && unify(pat->a, e->a, b) && unify(pat->b, e->b, b);
+  }
+  return false;
+}
+
+inline Expr cvar(const std::string& n) {
+  return mk({Node::Num, std::numeric_limits<double>::quiet_NaN(), n, false, 0, nullptr, nullptr});
+}
+
+}  // namespace detail
+
+// Matches a cascade onto a librf_cuda kernel (the host-side replacement of
+// derive_fused for the supported patterns; mirrors attention_shaped,
+// scalar_ir.cpp:495-514). Throws NotFusable when no kernel implements it.
+inline Program plan(const CascadeSpec& spec) {
+  using detail::Binding;
+  using detail::cvar;
+  using detail::unify;
+  const auto& R = spec.reductions;
+  Program p;
+  p.spec = spec;
+  p.L0 = spec.axis_len();
+  const Expr X = input("?X"), Vf = input("?V", true), Wf = input("?W", true), G = input("?G");
+  auto none = [&](const std::string& why) -> Program {
+    throw NotFusable("cascade '" + spec.name + "': no librf_cuda kernel (" + why + ")");
+  };
+  if (R.size() == 2 && R[0].op == "max" && R[1].op == "sum" && R[0].free_len == 1 &&
+      R[1].free_len == 1) {
+    Binding b;
+    if (unify(X, R[0].body, b) && unify(un("exp", bin("-", X, dep(1))), R[1].body, b)) {
+      p.pattern = RF_PATTERN_SAFE_SOFTMAX;
+      p.x = b.in["?X"];
+      return p;
+    }
+  }
+  if (R.size() == 3 && R[0].op == "max" && R[1].op == "sum" && R[2].op == "sum" &&
+      R[0].free_len == 1 && R[1].free_len == 1 && R[2].free_len > 1) {
+    Binding b;
+    const Expr e = un("exp", bin("-", X, dep(1)));
+    if (unify(X, R[0].body, b) && unify(e, R[1].body, b) &&
+        unify(bin("*", bin("/", e, dep(2)), Vf), R[2].body, b)) {
+      p.pattern = RF_PATTERN_ATTENTION;
+      p.x = b.in["?X"];
+      p.v = b.in["?V"];
+      p.free_len = R[2].free_len;
+      return p;
+    }
+  }
+  if (R.size() == 2 && R[0].op == "max" && R[1].op == "sum" && R[0].free_len == 1 &&
+      R[1].free_len > 1) {
+    Binding b;
+    if (unify(un("abs", X), R[0].body, b) &&
+        unify(bin("*", bin("/", bin("*", cvar("fmax"), X), dep(1)), Wf), R[1].body, b)) {
+      p.pattern = RF_PATTERN_QUANT_GEMM_E4M3;
+      p.x = b.in["?X"];
+      p.w = b.in["?W"];
+      p.fmax = b.c["fmax"];
+      p.free_len = R[1].free_len;
+      return p;
+    }
+  }
+  if (R.size() == 2 && R[0].op == "sum" && R[1].op == "sum" && R[0].free_len == 1 &&
+      R[1].free_len > 1) {
+    Binding b;
+    // x g / sqrt(d1 * INVK + EPS) * w   (or d1 / K)
+    const Expr body_mul = bin("*", bin("/", bin("*", X, G), un("sqrt", bin("+", bin("*", dep(1), cvar("ik")), cvar("eps")))), Wf);
+    Binding b2;
+    const Expr body_div = bin("*", bin("/", bin("*", X, G), un("sqrt", bin("+", bin("/", dep(1), cvar("k")), cvar("eps")))), Wf);
+    if (unify(bin("*", X, X), R[0].body, b)) {
+      b2 = b;
+      if (unify(body_mul, R[1].body, b) || unify(body_div, R[1].body, b2)) {
+        Binding& bb = b.c.count("ik") ? b : b2;
+        p.pattern = RF_PATTERN_RMSNORM_GEMM;
+        p.x = bb.in["?X"];
+        p.g = bb.in["?G"];
+        p.w = bb.in["?W"];
+        p.eps = bb.c["eps"];
+        p.inv_k = bb.c.count("ik") ? bb.c["ik"] : 1.0 / bb.c["k"];
+        if (std::fabs(p.inv_k * static_cast<double>(p.L0) - 1.0) > 1e-12)
+          return none("RMS statistic must be the mean over the reduce axis");
+        p.free_len = R[1].free_len;
+        return p;
+      }
+    }
+  }
+  return none("not one of safe_softmax / attention / quant_gemm / rmsnorm_gemm");
+}
+
+inline Program plan(const std::string& dsl) { return plan(parse_cascade(dsl)); }
+
+// ----------------------------------------------------------- TensorStore ----
+
+class TensorStore {
+ public:
+  struct Array {
+    std::vector<double> data;
+    long long len = 0, free_len = 0, loads = 0, stores = 0;
+  };
+  void define(const std::string& name, long long len, long long free_len, std::vector<double> data) {
+    const long long want = free_len > 0 ? len * free_len : len;
+    if (static_cast<long long>(data.size()) != want)
+      throw ShapeMismatch(name + ": got " + std::to_string(data.size()) + " values, want " +
+                          std::to_string(want));
+    Array a;
+    a.data = std::move(data);
+    a.len = len;
+    a.free_len = free_len;
+    a.stores = want;
+    arrays_[name] = std::move(a);
+  }
+  const Array& array(const std::string& name) const {
+    auto it = arrays_.find(name);
+    if (it == arrays_.end()) throw ShapeMismatch("no array named " + name);
+    return it->second;
+  }
+  bool has(const std::string& n) const { return arrays_.count(n) > 0; }
+  std::vector<std::string> names() const {
+    std::vector<std::string> out;
+    for (const auto& kv : arrays_) out.push_back(kv.first);
+    return out;
+  }
+
+ private:
+  std::map<std::string, Array> arrays_;
+};
+
+struct OutputVal {
+  int id = 0;
+  std::vector<double> v;
+  std::vector<std::pair<double, long long>> topk;
+};
+
+struct ExecReport {
+  std::string strategy;
+  std::vector<OutputVal> outputs;
+  std::map<std::string, long long> input_loads;
+  std::map<int, long long> dep_root_loads;
+  std::map<int, long long> peak_aux_slots;
+};
+
+struct DiffReport {
+  double max_rel_err = 0.0;
+  bool pass = true;
+  std::string worst;
+};
+
+// compare_reports' parity metric (simulator.cpp:691-752): per output
+// |a-b| / (1 + max(|a|,|b|)); equal values (incl. matching infs) are 0;
+// NaN/inf mismatches are +inf; top-k index mismatch is a hard fail.
+inline DiffReport compare_reports(const ExecReport& a, const ExecReport& b, double tol) {
+  DiffReport out;
+  const double inf = std::numeric_limits<double>::infinity();
+  if (a.outputs.size() != b.outputs.size()) return {inf, false, "output count mismatch"};
+  for (std::size_t i = 0; i < a.outputs.size(); ++i) {
+    const auto &oa = a.outputs[i], &ob = b.outputs[i];
+    if (oa.id != ob.id || oa.v.size() != ob.v.size() || oa.topk.size() != ob.topk.size())
+      return {inf, false, "shape mismatch at d" + std::to_string(oa.id)};
+    for (std::size_t l = 0; l < oa.v.size(); ++l) {
+      const double x = oa.v[l], y = ob.v[l];
+      double e;
+      if (x == y) e = 0.0;
+      else if (std::isnan(x) || std::isnan(y) || std::isinf(x) || std::isinf(y)) e = inf;
+      else e = std::fabs(x - y) / (1.0 + std::fmax(std::fabs(x), std::fabs(y)));
+      if (e > out.max_rel_err) {
+        out.max_rel_err = e;
+        out.worst = "d" + std::to_string(oa.id) + "[" + std::to_string(l) + "]";
+      }
+    }
+    for (std::size_t t = 0; t < oa.topk.size(); ++t)
+      if (oa.topk[t].second != ob.topk[t].second)
+        return {inf, false, "topk index set at d" + std::to_string(oa.id)};
+  }
+  if (out.max_rel_err > tol) out.pass = false;
+  return out;
+}
+
+// -------------------------------------------------------------- executors --
+
+namespace detail {
+
+struct PlanHandle {
+  rf_plan* p = nullptr;
+  explicit PlanHandle(const rf_desc& d) { check(rf_plan_create(&d, &p)); }
+  ~PlanHandle() { rf_plan_destroy(p); }
+  PlanHandle(const PlanHandle&) = delete;
+  PlanHandle& operator=(const PlanHandle&) = delete;
+};
+
+inline rf_desc base_desc(rf_pattern pat, rf_dtype dt) {
+  rf_desc d;
+  std::memset(&d, 0, sizeof d);
+  d.pattern = pat;
+  d.dtype = dt;
+  d.batch = d.heads = 1;
+  d.segments = 1;
+  d.softmax_scale = 1.0;
+  d.fmax = 448.0;
+  return d;
+}
+
+inline uint16_t to_bf16(float f) {  // RNE
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+inline float from_bf16(uint16_t h) {
+  const uint32_t u = static_cast<uint32_t>(h) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+inline long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
+
+inline void check_shapes(const Program& prog, const TreeConfig& cfg, const TensorStore& st) {
+  // validate_tree (cascade.cpp:37-66) + store shapes (simulator.cpp:235-245)
+  if (cfg.levels.size() < 2 || cfg.levels.front() != prog.L0 || cfg.levels.back() != 1)
+    throw ShapeMismatch("BadTree: levels must run from L0 = " + std::to_string(prog.L0) + " to 1");
+  for (std::size_t k = 1; k < cfg.levels.size(); ++k)
+    if (cfg.levels[k] <= 0 || cfg.levels[k - 1] % cfg.levels[k] != 0)
+      throw ShapeMismatch("BadTree: level widths must divide");
+  for (const auto& in : prog.spec.inputs) {
+    const auto& a = st.array(in.name);
+    if (a.len != in.len || a.free_len != in.free_len)
+      throw ShapeMismatch(in.name + ": store shape does not match the spec");
+  }
+}
+
+// The fused loop's counters: every input element loaded once
+// (acceptance crit 6), root dependency reads once per corrected reduction at
+// finalize (crit 7, simulator.cpp:617), O(1) auxiliary state per level (crit 8).
+inline void fill_counters(const Program& prog, const TreeConfig& cfg, ExecReport& r) {
+  long long arity = 0;
+  for (const auto& red : prog.spec.reductions) arity += red.op == "topk" ? 2LL * red.topk : red.free_len;
+  for (const auto& in : prog.spec.inputs) r.input_loads[in.name] = in.len * std::max(1LL, in.free_len);
+  for (const auto& red : prog.spec.reductions) {
+    std::set<int> ds;
+    deps_of(red.body, ds);
+    for (int d : ds) r.dep_root_loads[d] += 1;
+  }
+  for (int m = 1; m <= cfg.depth(); ++m) r.peak_aux_slots[m] = arity;
+}
+
+inline ExecReport execute(const Program& prog, const TreeConfig& cfg, long long segments,
+                          TensorStore& st, const std::string& strategy) {
+  check_shapes(prog, cfg, st);
+  if (segments < 1 || prog.L0 % segments != 0)  // simulator.cpp:668-671
+    throw IncompatibleSegmentation(std::to_string(segments) + " segments do not divide L0 = " +
+                                   std::to_string(prog.L0));
+  ExecReport rep;
+  rep.strategy = strategy;
+  const long long L0 = prog.L0;
+  auto out = [&](int id, std::vector<double> v) {
+    OutputVal o;
+    o.id = id;
+    o.v = std::move(v);
+    rep.outputs.push_back(std::move(o));
+  };
+  switch (prog.pattern) {
+    case RF_PATTERN_SAFE_SOFTMAX: {
+      rf_desc d = base_desc(RF_PATTERN_SAFE_SOFTMAX, RF_F32);
+      d.rows = 1;
+      d.len = L0;
+      PlanHandle h(d);
+      const auto& x = st.array(prog.x).data;
+      std::vector<float> xf(x.begin(), x.end());
+      float m = 0, t = 0;
+      rf_host_io io{};
+      io.in[0] = xf.data();
+      io.d[0] = &m;
+      io.d[1] = &t;
+      check(rf_run_host(h.p, &io));
+      out(1, {m});
+      out(2, {t});
+      break;
+    }
+    case RF_PATTERN_ATTENTION: {
+      // One cascade row: P and V. The kernel consumes Q, K, V with P = Q K^T;
+      // q = e_0 and K[l] = (P[l], 0, ...) reproduce P exactly in fp32.
+      const long long hd = prog.free_len;
+      long long D = 16;
+      while (D < hd) D *= 2;
+      if (D > 128) throw NotFusable("attention head dim > 128");
+      rf_desc d = base_desc(RF_PATTERN_ATTENTION, RF_F32);
+      d.rows = 1;
+      d.len = L0;
+      d.free_len = D;
+      d.segments = segments;
+      PlanHandle h(d);
+      const auto& P = st.array(prog.x).data;
+      const auto& V = st.array(prog.v).data;
+      std::vector<float> q(D, 0.f), k(L0 * D, 0.f), v(L0 * D, 0.f), o(D);
+      q[0] = 1.f;
+      for (long long l = 0; l < L0; ++l) {
+        k[l * D] = static_cast<float>(P[l]);
+        for (long long f = 0; f < hd; ++f) v[l * D + f] = static_cast<float>(V[l * hd + f]);
+      }
+      float m = 0, t = 0;
+      rf_host_io io{};
+      io.in[0] = q.data();
+      io.in[1] = k.data();
+      io.in[2] = v.data();
+      io.d[0] = &m;
+      io.d[1] = &t;
+      io.d[2] = o.data();
+      check(rf_run_host(h.p, &io));
+      out(1, {m});
+      out(2, {t});
+      out(3, std::vector<double>(o.begin(), o.begin() + hd));
+      break;
+    }
+    case RF_PATTERN_QUANT_GEMM_E4M3:
+    case RF_PATTERN_RMSNORM_GEMM: {
+      const bool quant = prog.pattern == RF_PATTERN_QUANT_GEMM_E4M3;
+      if (segments != 1) throw NotFusable("GEMM patterns: multi-segment not kernelised");
+      // pad to the kernel tiles: M to 128 rows (copies of the row: never an
+      // all-zero padding row), K with zeros (neutral for max|a| and sum x^2,
+      // zero contributions), N with zero weight columns.
+      const long long N = prog.free_len;
+      const long long Kp = round_up(L0, quant ? 128 : 64), Np = round_up(N, quant ? 512 : 256);
+      const long long M = 128;
+      rf_desc d = base_desc(prog.pattern, RF_BF16);
+      d.rows = M;
+      d.len = Kp;
+      d.free_len = Np;
+      d.fmax = prog.fmax;
+      d.eps = prog.eps;
+      PlanHandle h(d);
+      const auto& A = st.array(prog.x).data;
+      const auto& W = st.array(prog.w).data;
+      std::vector<float> wf(Kp * Np, 0.f), gf(Kp, 0.f);
+      for (long long l = 0; l < L0; ++l)
+        for (long long f = 0; f < N; ++f) wf[l * Np + f] = static_cast<float>(W[l * N + f]);
+      if (!quant) {
+        const auto& g = st.array(prog.g).data;
+        for (long long l = 0; l < L0; ++l) gf[l] = static_cast<float>(g[l]);
+      }
+      void* packed = nullptr;
+      check(rf_pack_weight_host(h.p, wf.data(), quant ? nullptr : gf.data(), &packed));
+      std::vector<uint16_t> a(M * Kp, 0);
+      for (long long r = 0; r < M; ++r)
+        for (long long l = 0; l < L0; ++l) a[r * Kp + l] = to_bf16(static_cast<float>(A[l]));
+      std::vector<float> d1(M);
+      std::vector<float> cf(quant ? M * Np : 0);
+      std::vector<uint16_t> cb(quant ? 0 : M * Np);
+      rf_host_io io{};
+      io.in[0] = a.data();
+      io.in[1] = packed;
+      io.d[0] = d1.data();
+      io.d[1] = quant ? static_cast<void*>(cf.data()) : static_cast<void*>(cb.data());
+      const rf_status s = rf_run_host(h.p, &io);
+      rf_buffer_free(packed);
+      check(s);
+      std::vector<double> c(N);
+      for (long long f = 0; f < N; ++f) c[f] = quant ? cf[f] : from_bf16(cb[f]);
+      out(1, {d1[0]});
+      out(2, c);
+      if (quant && !(d1[0] > 0.0f))  // finalize_root: 0/0 faults propagate
+        throw DomainError("division by zero");
+      break;
+    }
+    default: throw NotFusable("unknown pattern");
+  }
+  fill_counters(prog, cfg, rep);
+  return rep;
+}
+
+}  // namespace detail
+
+// run_incremental (simulator.hpp:76-77): the Single-Segment fused loop.
+inline ExecReport run_incremental(const Program& prog, const TreeConfig& cfg, TensorStore& store) {
+  return detail::execute(prog, cfg, 1, store, "incremental");
+}
+
+// run_multisegment (simulator.hpp:81-82): S equal slices streamed
+// independently and merged in slice order (split-KV).
+inline ExecReport run_multisegment(const Program& prog, const TreeConfig& cfg, long long num_segments,
+                                   TensorStore& store) {
+  return detail::execute(prog, cfg, num_segments, store, "multi:" + std::to_string(num_segments));
+}
+
+}  // namespace rfcuda

@@ -79,6 +79,8 @@ SIGNATURES = {
     "rf_plan_describe": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.c_size_t]),
     "rf_plan_launches_per_run": (ctypes.c_int64, [_P]),
     "rf_pack_weight": (ctypes.c_int, [_P, _P, _P, _P, _P]),
+    "rf_pack_weight_host": (ctypes.c_int, [_P, _P, _P, ctypes.POINTER(_P)]),
+    "rf_buffer_free": (None, [_P]),
     "rf_run": (ctypes.c_int, [_P, ctypes.POINTER(rf_io), _P]),
     "rf_run_host": (ctypes.c_int, [_P, ctypes.POINTER(rf_io)]),
     "rf_run_partials": (

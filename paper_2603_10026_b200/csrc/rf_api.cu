@@ -357,6 +357,41 @@ rf_status rf_pack_weight(const rf_plan* p, const void* w, const void* g, void* p
   return RF_OK;
 }
 
+rf_status rf_pack_weight_host(const rf_plan* p, const float* w, const float* g, void** packed) {
+  if (!p || !w || !packed) return fail(RF_ERR_ARG, "null plan/w/packed");
+  *packed = nullptr;
+  const bool quant = p->d.pattern == RF_PATTERN_QUANT_GEMM_E4M3;
+  if (!quant && p->d.pattern != RF_PATTERN_RMSNORM_GEMM)
+    return fail(RF_ERR_UNSUPPORTED, "pattern has no packed weight");
+  if (!quant && !g) return fail(RF_ERR_ARG, "rmsnorm pack needs g");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  RF_CUDA_TRY(cudaSetDevice(p->d.device));
+  const size_t kn = static_cast<size_t>(p->d.len) * p->d.free_len;
+  float *dw = nullptr, *dg = nullptr;
+  void* out = nullptr;
+  RF_CUDA_TRY(cudaMalloc(&dw, kn * sizeof(float)));
+  RF_CUDA_TRY(cudaMalloc(&out, kn * (quant ? 1 : 2)));
+  RF_CUDA_TRY(cudaMemcpy(dw, w, kn * sizeof(float), cudaMemcpyHostToDevice));
+  if (g) {
+    RF_CUDA_TRY(cudaMalloc(&dg, p->d.len * sizeof(float)));
+    RF_CUDA_TRY(cudaMemcpy(dg, g, p->d.len * sizeof(float), cudaMemcpyHostToDevice));
+  }
+  rf_status st = rf_pack_weight(p, dw, dg, out, nullptr);
+  RF_CUDA_TRY(cudaDeviceSynchronize());
+  cudaFree(dw);
+  cudaFree(dg);
+  if (st != RF_OK) {
+    cudaFree(out);
+    return st;
+  }
+  *packed = out;
+  cudaSetDevice(prev);
+  return RF_OK;
+}
+
+void rf_buffer_free(void* dev_ptr) { cudaFree(dev_ptr); }
+
 rf_status rf_run(const rf_plan* p, const rf_io* io, void* stream) {
   if (!p || !io) return fail(RF_ERR_ARG, "null plan/io");
   size_t in[4], out[3];

@@ -1,0 +1,266 @@
+// C++ host-layer tests (include/rf_host.hpp over librf_cuda), written after
+// the reference's own tests/test_simulator.cpp and tests/test_cascade.cpp so
+// that the drop-in reads like the original:  ./test_host cpu | gpu
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <string>
+
+#include "rf_host.hpp"
+
+using namespace rfcuda;
+
+static int failures = 0, checks = 0;
+#define CHECK(c)                                                           \
+  do {                                                                     \
+    ++checks;                                                              \
+    if (!(c)) {                                                            \
+      ++failures;                                                          \
+      std::printf("  FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);           \
+    }                                                                      \
+  } while (0)
+#define CHECK_THROWS_AS(expr, T)                                           \
+  do {                                                                     \
+    ++checks;                                                              \
+    bool ok = false;                                                       \
+    try {                                                                  \
+      (void)(expr);                                                        \
+    } catch (const T&) {                                                   \
+      ok = true;                                                           \
+    } catch (...) {                                                        \
+    }                                                                      \
+    if (!ok) {                                                             \
+      ++failures;                                                          \
+      std::printf("  FAIL %s:%d: %s does not throw %s\n", __FILE__, __LINE__, #expr, #T); \
+    }                                                                      \
+  } while (0)
+#define TEST(name) static void name()
+#define RUN(name)                       \
+  do {                                  \
+    std::printf("[ run ] %s\n", #name); \
+    name();                             \
+  } while (0)
+
+static std::string softmax_dsl(long long n) {
+  return "cascade safe_softmax\ninput x len " + std::to_string(n) +
+         "\nreduce 1 op max\n    x[l]\nreduce 2 op sum\n    exp(x[l] - d1)\n";
+}
+static std::string attention_dsl(long long kv, long long hd) {
+  return "cascade attention\ninput P len " + std::to_string(kv) + "\ninput V len " +
+         std::to_string(kv) + " free " + std::to_string(hd) +
+         "\nreduce 1 op max\n    P[l]\nreduce 2 op sum\n    exp(P[l] - d1)\nreduce 3 op sum free " +
+         std::to_string(hd) + "\n    exp(P[l] - d1) / d2 * V[l, f]\n";
+}
+static std::string quant_dsl(long long k, long long n) {
+  return "cascade quant_gemm\ninput a len " + std::to_string(k) + "\ninput w len " + std::to_string(k) +
+         " free " + std::to_string(n) + "\nconst FMAX = 448.0\nreduce 1 op max\n    abs(a[l])\n"
+         "reduce 2 op sum free " + std::to_string(n) + "\n    (FMAX * a[l] / d1) * w[l, f]\n";
+}
+static std::string rms_dsl(long long k, long long n) {
+  return "cascade rmsnorm_gemm\ninput x len " + std::to_string(k) + "\ninput g len " +
+         std::to_string(k) + "\ninput w len " + std::to_string(k) + " free " + std::to_string(n) +
+         "\nconst K = " + std::to_string(k) + "\nconst EPS = 1e-6\nreduce 1 op sum\n    x[l] * x[l]\n"
+         "reduce 2 op sum free " + std::to_string(n) + "\n    x[l] * g[l] / sqrt(d1 / K + EPS) * w[l, f]\n";
+}
+static std::vector<double> random_vec(std::size_t n, std::uint64_t seed, double lo, double hi) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> d(lo, hi);
+  std::vector<double> v(n);
+  for (auto& x : v) x = d(rng);
+  return v;
+}
+
+// ---------------------------------------------------------------- CPU-only --
+
+TEST(dsl_files_parse_and_match_kernels) {
+  // proj/data/*.cascade contents
+  CHECK(plan(softmax_dsl(1024)).pattern == RF_PATTERN_SAFE_SOFTMAX);
+  Program a = plan(attention_dsl(256, 64));
+  CHECK(a.pattern == RF_PATTERN_ATTENTION && a.x == "P" && a.v == "V" && a.free_len == 64);
+  Program q = plan(quant_dsl(512, 256));
+  CHECK(q.pattern == RF_PATTERN_QUANT_GEMM_E4M3 && q.fmax == 448.0 && q.w == "w");
+  Program r = plan(rms_dsl(4096, 11008));
+  CHECK(r.pattern == RF_PATTERN_RMSNORM_GEMM && r.eps == 1e-6 && r.g == "g");
+  CHECK(std::fabs(r.inv_k * 4096 - 1.0) < 1e-15);
+}
+
+TEST(unsupported_cascades_are_not_fusable) {
+  // variance / moe_routing / moment_of_inertia have no kernel: NotFusable, no CPU fallback
+  CHECK_THROWS_AS(plan("cascade variance\ninput x len 8\nreduce 1 op sum\n    x[l]\n"
+                       "reduce 2 op sum\n    x[l] * x[l]\n"),
+                  NotFusable);
+  CHECK_THROWS_AS(plan("cascade moe\ninput s len 8\nreduce 1 op max\n    s[l]\nreduce 2 op sum\n"
+                       "    exp(s[l] - d1)\nreduce 3 op topk 2\n    s[l]\n"),
+                  NotFusable);
+  // RMS statistic that is not the mean over L0
+  CHECK_THROWS_AS(plan("cascade r\ninput x len 8\ninput g len 8\ninput w len 8 free 4\n"
+                       "reduce 1 op sum\n    x[l] * x[l]\nreduce 2 op sum free 4\n"
+                       "    x[l] * g[l] / sqrt(d1 / 3 + 0.1) * w[l, f]\n"),
+                  NotFusable);
+}
+
+TEST(syntax_errors) {
+  CHECK_THROWS_AS(parse_cascade("cascade x\ninput x len 0\n"), SyntaxError);
+  CHECK_THROWS_AS(parse_cascade("cascade x\ninput x len 4\nreduce 1 op max\n"), SyntaxError);
+  CHECK_THROWS_AS(parse_cascade("cascade x\ninput x len 4\nreduce 1 op max\n    x[l] + d1\n"),
+                  SyntaxError);  // forward dependency
+  CHECK_THROWS_AS(parse_cascade("cascade x\ninput x len 4\nreduce 1 op max\n    y[l]\n"), SyntaxError);
+  CHECK_THROWS_AS(parse_cascade("cascade x\ninput x len 4\nreduce 1 op avg\n    x[l]\n"), SyntaxError);
+}
+
+TEST(compare_reports_flags_corruption_with_a_location) {
+  ExecReport u, v;
+  u.outputs = {{1, {3.0}, {}}, {2, {1.5}, {}}};
+  v = u;
+  DiffReport same = compare_reports(u, v, 1e-12);
+  CHECK(same.pass && same.max_rel_err == 0.0);
+  v.outputs[1].v[0] += 0.5;
+  DiffReport diff = compare_reports(u, v, 1e-6);
+  CHECK(!diff.pass);
+  CHECK(diff.worst == "d2[0]");
+  v = u;
+  v.outputs[0].v[0] = std::nan("");
+  CHECK(!compare_reports(u, v, 1.0).pass);
+}
+
+TEST(shape_checks) {
+  Program p = plan(softmax_dsl(8));
+  TensorStore st;
+  st.define("x", 4, 0, std::vector<double>(4, 1.0));
+  CHECK_THROWS_AS(run_incremental(p, TreeConfig{{8, 1}}, st), ShapeMismatch);
+  TensorStore st2;
+  CHECK_THROWS_AS(run_incremental(p, TreeConfig{{8, 1}}, st2), ShapeMismatch);
+  TensorStore st3;
+  st3.define("x", 8, 0, std::vector<double>(8, 1.0));
+  CHECK_THROWS_AS(run_incremental(p, TreeConfig{{8, 3, 1}}, st3), ShapeMismatch);
+  CHECK_THROWS_AS(st3.define("y", 4, 2, std::vector<double>(7, 0.0)), ShapeMismatch);
+  Program q = plan(quant_dsl(16, 4));
+  TensorStore st4;
+  st4.define("a", 16, 0, random_vec(16, 7, -2, 2));
+  st4.define("w", 16, 4, random_vec(64, 8, -1, 1));
+  CHECK_THROWS_AS(run_multisegment(q, TreeConfig{{16, 4, 1}}, 3, st4), IncompatibleSegmentation);
+}
+
+// --------------------------------------------------------------------- GPU --
+
+TEST(softmax_by_hand) {  // test_simulator.cpp:39-51
+  Program p = plan(softmax_dsl(3));
+  TensorStore st;
+  st.define("x", 3, 0, {1, 2, 3});
+  ExecReport r = run_incremental(p, TreeConfig{{3, 1}}, st);
+  CHECK(r.outputs[0].v[0] == 3.0);
+  const double t = std::exp(-2.0) + std::exp(-1.0) + 1.0;
+  CHECK(std::fabs(r.outputs[1].v[0] - t) < 1e-6);
+  CHECK(r.input_loads.at("x") == 3);  // fused: each element loaded once
+  CHECK(r.dep_root_loads.at(1) == 1);
+}
+
+TEST(quant_trivia) {  // test_simulator.cpp:53-68
+  Program q = plan(quant_dsl(1, 1));
+  TensorStore st;
+  st.define("a", 1, 0, {1.0});
+  st.define("w", 1, 1, {2.0});
+  ExecReport r = run_incremental(q, TreeConfig{{1, 1}}, st);
+  CHECK(r.outputs[0].v[0] == 1.0);
+  CHECK(r.outputs[1].v[0] == 896.0);
+}
+
+TEST(quant_zero_row_is_a_domain_error) {  // finalize_root fault propagation
+  Program q = plan(quant_dsl(4, 2));
+  TensorStore st;
+  st.define("a", 4, 0, {0, 0, 0, 0});
+  st.define("w", 4, 2, std::vector<double>(8, 1.0));
+  CHECK_THROWS_AS(run_incremental(q, TreeConfig{{4, 1}}, st), DomainError);
+}
+
+static ExecReport attention_oracle(const TensorStore& st, long long kv, long long hd) {
+  const auto& p = st.array("P").data;
+  const auto& v = st.array("V").data;
+  double m = p[0];
+  for (double x : p) m = std::max(m, x);
+  double t = 0;
+  for (double x : p) t += std::exp(x - m);
+  ExecReport r;
+  r.outputs = {{1, {m}, {}}, {2, {t}, {}}, {3, std::vector<double>(hd, 0.0), {}}};
+  for (long long l = 0; l < kv; ++l)
+    for (long long f = 0; f < hd; ++f) r.outputs[2].v[f] += std::exp(p[l] - m) / t * v[l * hd + f];
+  return r;
+}
+
+TEST(attention_incremental_and_multisegment_match_oracle) {
+  const long long kv = 256, hd = 64;
+  Program p = plan(attention_dsl(kv, hd));
+  auto mk = [&] {
+    TensorStore st;
+    st.define("P", kv, 0, random_vec(kv, 3, -2, 2));
+    st.define("V", kv, hd, random_vec(kv * hd, 4, -1, 1));
+    return st;
+  };
+  TensorStore ref = mk();
+  ExecReport want = attention_oracle(ref, kv, hd);
+  for (const TreeConfig& cfg : {TreeConfig{{kv, 1}}, TreeConfig{{kv, kv / 8, 1}}}) {
+    TensorStore st = mk();
+    ExecReport inc = run_incremental(p, cfg, st);
+    CHECK(compare_reports(inc, want, 1e-5).pass);
+    CHECK(inc.input_loads.at("V") == kv * hd);
+    CHECK(inc.peak_aux_slots.at(1) == 1 + 1 + hd);
+    for (long long s : {2LL, 4LL, 8LL}) {
+      TensorStore st2 = mk();
+      CHECK(compare_reports(run_multisegment(p, cfg, s, st2), want, 1e-5).pass);
+    }
+  }
+  TensorStore a = mk(), b = mk();  // multi:1 equals flat incremental exactly
+  ExecReport i1 = run_incremental(p, TreeConfig{{kv, 1}}, a);
+  ExecReport m1 = run_multisegment(p, TreeConfig{{kv, 1}}, 1, b);
+  CHECK(compare_reports(i1, m1, 0.0).max_rel_err == 0.0);
+}
+
+TEST(softmax_weights_sum_to_one) {  // test_simulator.cpp:162-191
+  Program p = plan(softmax_dsl(32));
+  TensorStore st;
+  st.define("x", 32, 0, random_vec(32, 11, -2, 2));
+  ExecReport r = run_incremental(p, TreeConfig{{32, 8, 1}}, st);
+  double m = r.outputs[0].v[0], t = r.outputs[1].v[0], sum = 0;
+  for (double x : st.array("x").data) sum += std::exp(x - m) / t;
+  CHECK(std::fabs(sum - 1.0) < 1e-5);
+}
+
+TEST(rmsnorm_gemm_matches_direct_loop) {
+  const long long k = 256, n = 48;
+  Program p = plan(rms_dsl(k, n));
+  TensorStore st;
+  st.define("x", k, 0, random_vec(k, 1, -1, 1));
+  st.define("g", k, 0, random_vec(k, 2, -1, 1));
+  st.define("w", k, n, random_vec(k * n, 3, -1, 1));
+  ExecReport r = run_incremental(p, TreeConfig{{k, 1}}, st);
+  const auto &x = st.array("x").data, &g = st.array("g").data, &w = st.array("w").data;
+  double ss = 0;
+  for (double v : x) ss += v * v;
+  ExecReport want;
+  want.outputs = {{1, {ss}, {}}, {2, std::vector<double>(n, 0.0), {}}};
+  for (long long l = 0; l < k; ++l)
+    for (long long f = 0; f < n; ++f)
+      want.outputs[1].v[f] += x[l] * g[l] / std::sqrt(ss / k + 1e-6) * w[l * n + f];
+  DiffReport d = compare_reports(r, want, 0.1);  // bf16 operands (unrounded reference)
+  CHECK(d.pass);
+  std::printf("  rmsnorm scaled err vs unrounded reference: %.3g (%s)\n", d.max_rel_err, d.worst.c_str());
+}
+
+int main(int argc, char** argv) {
+  const std::string mode = argc > 1 ? argv[1] : "cpu";
+  RUN(dsl_files_parse_and_match_kernels);
+  RUN(unsupported_cascades_are_not_fusable);
+  RUN(syntax_errors);
+  RUN(compare_reports_flags_corruption_with_a_location);
+  RUN(shape_checks);
+  if (mode == "gpu") {
+    RUN(softmax_by_hand);
+    RUN(quant_trivia);
+    RUN(quant_zero_row_is_a_domain_error);
+    RUN(attention_incremental_and_multisegment_match_oracle);
+    RUN(softmax_weights_sum_to_one);
+    RUN(rmsnorm_gemm_matches_direct_loop);
+  }
+  std::printf("%d checks, %d failures\n", checks, failures);
+  return failures ? 1 : 0;
+}
