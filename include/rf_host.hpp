@@ -494,9 +494,8 @@ inline Program plan(const CascadeSpec& spec) {
       return p;
     }
   }
-  if (R.size() == 2 && R[0].op == "max" && R[1].op == "sum" && R[0].free_len == 1 &&
-      R[1].free_len > 1) {
-    Binding b;
+  if (R.size() == 2 && R[0].op == "max" && R[1].op == "sum" && R[0].free_len == 1) {
+    Binding b;  // free_len may be 1: a one-lane free axis (test_simulator.cpp:53-68)
     if (unify(un("abs", X), R[0].body, b) &&
         unify(bin("*", bin("/", bin("*", cvar("fmax"), X), dep(1)), Wf), R[1].body, b)) {
       p.pattern = RF_PATTERN_QUANT_GEMM_E4M3;
@@ -507,8 +506,7 @@ inline Program plan(const CascadeSpec& spec) {
       return p;
     }
   }
-  if (R.size() == 2 && R[0].op == "sum" && R[1].op == "sum" && R[0].free_len == 1 &&
-      R[1].free_len > 1) {
+  if (R.size() == 2 && R[0].op == "sum" && R[1].op == "sum" && R[0].free_len == 1) {
     Binding b;
     // x g / sqrt(d1 * INVK + EPS) * w   (or d1 / K)
     const Expr body_mul = bin("*", bin("/", bin("*", X, G), un("sqrt", bin("+", bin("*", dep(1), cvar("ik")), cvar("eps")))), Wf);

@@ -1,0 +1,58 @@
+// Reference-side binding: redfuse::run_cuda over librf_cuda (see redfuse_cuda.hpp).
+// The cascade travels through the reference's own DSL serializer
+// (cascade.hpp:93 serialize) into the host layer's parser + pattern matcher;
+// the TensorStore arrays are handed over as-is and the ExecReport is returned
+// with the reference's field meanings.
+#include "redfuse_cuda.hpp"
+
+#include "redfuse/cascade.hpp"
+#include "rf_host.hpp"
+
+namespace redfuse {
+namespace {
+
+ExecReport run(const FusedProgram& prog, const TreeConfig& cfg, long long segments,
+               TensorStore& store) {
+  rfcuda::Program p;
+  try {
+    p = rfcuda::plan(serialize(prog.spec));
+  } catch (const rfcuda::NotFusable& e) {
+    throw NotFusable(0, e.what());
+  }
+  rfcuda::TensorStore st;
+  for (const auto& in : prog.spec.inputs) {
+    const auto& a = store.array(in.name);  // ShapeMismatch if absent
+    st.define(in.name, a.len, a.free_len, a.data);
+  }
+  rfcuda::ExecReport r;
+  try {
+    r = segments == 1 ? rfcuda::run_incremental(p, rfcuda::TreeConfig{cfg.levels}, st)
+                      : rfcuda::run_multisegment(p, rfcuda::TreeConfig{cfg.levels}, segments, st);
+  } catch (const rfcuda::ShapeMismatch& e) {
+    throw ShapeMismatch(e.what());
+  } catch (const rfcuda::IncompatibleSegmentation& e) {
+    throw IncompatibleSegmentation(e.what());
+  } catch (const rfcuda::DomainError& e) {
+    throw DomainError(e.what());
+  }
+  ExecReport out;
+  out.strategy = "cuda:" + r.strategy;
+  for (const auto& o : r.outputs) out.outputs.push_back(OutputVal{o.id, o.v, o.topk});
+  out.input_loads = r.input_loads;
+  out.dep_root_loads = r.dep_root_loads;
+  out.peak_aux_slots = r.peak_aux_slots;
+  return out;
+}
+
+}  // namespace
+
+ExecReport run_cuda(const FusedProgram& prog, const TreeConfig& cfg, TensorStore& store) {
+  return run(prog, cfg, 1, store);
+}
+
+ExecReport run_cuda_multisegment(const FusedProgram& prog, const TreeConfig& cfg,
+                                 long long num_segments, TensorStore& store) {
+  return run(prog, cfg, num_segments, store);
+}
+
+}  // namespace redfuse

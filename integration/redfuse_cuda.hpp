@@ -1,0 +1,19 @@
+// Reference-side binding (what a RedFuser maintainer adds to proj/): a CUDA
+// executor with the exact signature of the reference's executors
+// (proj/include/redfuse/simulator.hpp:76-82), backed by librf_cuda through
+// the C++ host layer include/rf_host.hpp. See INTEGRATION.md.
+#pragma once
+
+#include "redfuse/acrf.hpp"
+#include "redfuse/simulator.hpp"
+
+namespace redfuse {
+
+// Same contract as run_incremental / run_multisegment; throws the reference's
+// ShapeMismatch / IncompatibleSegmentation / DomainError, and NotFusable when
+// librf_cuda has no kernel for the cascade (there is no CPU fallback).
+ExecReport run_cuda(const FusedProgram& prog, const TreeConfig& cfg, TensorStore& store);
+ExecReport run_cuda_multisegment(const FusedProgram& prog, const TreeConfig& cfg,
+                                 long long num_segments, TensorStore& store);
+
+}  // namespace redfuse

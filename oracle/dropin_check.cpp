@@ -1,0 +1,116 @@
+// TEST INFRASTRUCTURE: the drop-in check. Runs the reference's own workloads
+// (generators from proj/src/workloads.cpp, the RMSNorm DSL cascade) through
+// BOTH the reference executors (run_incremental / run_multisegment) and the
+// reference-side CUDA binding (integration/redfuse_cuda.cpp -> librf_cuda),
+// and compares them with the reference's own compare_reports — values AND the
+// load counters (input_load_delta / dep_root_delta must be 0).
+// Built by oracle/Makefile into oracle/_ref/dropin_check; run on the GPU box
+// by tests/test_gpu_dropin.py. Prints one JSON object per case.
+#include <cmath>
+#include <cstdio>
+#include <sstream>
+#include <string>
+
+#include "../integration/redfuse_cuda.hpp"
+#include "redfuse/workloads.hpp"
+
+using namespace redfuse;
+
+static int failures = 0;
+
+// tol > 0: gate on compare_reports' scaled max error (fp32 paths).
+// tol < 0: low-precision operands vs the UNROUNDED reference: gate on the RMS
+// relative error of the last output (|tol|), report the scaled max error.
+static void report(const std::string& name, const std::string& mode, const ExecReport& ref,
+                   const ExecReport& cuda, double tol) {
+  DiffReport d = compare_reports(cuda, ref, tol > 0 ? tol : 1e300);
+  long long dl = 0, dd = 0;
+  for (const auto& [k, v] : d.input_load_delta) dl += v < 0 ? -v : v;
+  for (const auto& [k, v] : d.dep_root_delta) dd += v < 0 ? -v : v;
+  double num = 0, den = 0;
+  const auto& a = cuda.outputs.back().v;
+  const auto& b = ref.outputs.back().v;
+  for (std::size_t i = 0; i < a.size() && i < b.size(); ++i) {
+    num += (a[i] - b[i]) * (a[i] - b[i]);
+    den += b[i] * b[i];
+  }
+  const double rms = den > 0 ? std::sqrt(num / den) : std::sqrt(num);
+  const bool ok = (tol > 0 ? d.pass : rms <= -tol) && dl == 0 && dd == 0;
+  if (!ok) ++failures;
+  std::printf(
+      "{\"case\": \"%s\", \"mode\": \"%s\", \"max_rel_err\": %.3e, \"rms_rel_err\": %.3e, "
+      "\"gate\": \"%s %.1e\", \"worst\": \"%s\", \"input_load_delta\": %lld, \"dep_root_delta\": "
+      "%lld, \"pass\": %s}\n",
+      name.c_str(), mode.c_str(), d.max_rel_err, rms, tol > 0 ? "max_rel" : "rms_rel",
+      tol > 0 ? tol : -tol, d.worst.c_str(), dl, dd, ok ? "true" : "false");
+}
+
+static void check_workload(const std::string& name, const Workload& w, double tol,
+                           std::initializer_list<long long> segs, int seeds) {
+  FusedProgram prog = derive_fused(w.spec);
+  const long long l0 = w.spec.axis_len();
+  for (int seed = 100; seed < 100 + seeds; ++seed) {
+    for (const TreeConfig& cfg : {TreeConfig{{l0, 1}}, TreeConfig{{l0, l0 / 8, 1}}}) {
+      TensorStore a = w.generate(seed), b = w.generate(seed);
+      report(name + "/s" + std::to_string(seed) + "/L" + std::to_string(cfg.depth()), "incremental",
+             run_incremental(prog, cfg, a), run_cuda(prog, cfg, b), tol);
+      for (long long s : segs) {
+        TensorStore c = w.generate(seed), d = w.generate(seed);
+        report(name + "/s" + std::to_string(seed), "multi:" + std::to_string(s),
+               run_multisegment(prog, cfg, s, c), run_cuda_multisegment(prog, cfg, s, d), tol);
+      }
+    }
+  }
+}
+
+int main() {
+  // fp32 paths: the north_star's 1e-5
+  check_workload("attention_256x64", make_attention(256, 64), 1e-5, {2, 4, 8}, 3);
+  check_workload("attention_1024x64", make_attention(1024, 64), 1e-5, {8}, 1);
+  check_workload("attention_128x128", make_attention(128, 128), 1e-5, {2}, 1);
+  check_workload("safe_softmax_1024", make_safe_softmax(1024), 1e-5, {2, 4, 8}, 3);
+  // bf16 / e4m3 operand paths: the reference here is evaluated on UNROUNDED
+  // inputs, so the gap is the operands' rounding (e4m3: 3 mantissa bits); the
+  // 2e-2 same-rounded-input gate is tests/test_gpu_gemm.py. Gated on RMS
+  // relative error.
+  check_workload("quant_gemm_512x256", make_quant_gemm(512, 256), -0.06, {}, 2);
+  {
+    std::ostringstream os;
+    os << "cascade rmsnorm_gemm\ninput x len 256\ninput g len 256\ninput w len 256 free 48\n"
+       << "const INVK = 0.00390625\nconst EPS = 1e-6\nreduce 1 op sum\n    x[l] * x[l]\n"
+       << "reduce 2 op sum free 48\n    x[l] * g[l] / sqrt(d1 * INVK + EPS) * w[l, f]\n";
+    CascadeSpec spec = parse_cascade(os.str());
+    Workload w;
+    w.name = "rmsnorm_gemm";
+    w.spec = spec;
+    w.generate = [spec](std::uint64_t seed) {
+      TensorStore st;
+      std::mt19937_64 rng(seed);
+      std::uniform_real_distribution<double> u(-1.0, 1.0);
+      for (const auto& in : spec.inputs) {
+        std::vector<double> v(in.len * (in.free_len > 0 ? in.free_len : 1));
+        for (auto& x : v) x = u(rng);
+        st.define(in.name, in.len, in.free_len, v);
+      }
+      return st;
+    };
+    check_workload("rmsnorm_gemm_256x48", w, -0.02, {}, 2);
+  }
+  // no kernel for these: NotFusable from the binding (no CPU fallback)
+  for (const char* nm : {"variance", "moe_routing"}) {
+    Workload w = builtin(nm);
+    FusedProgram prog = derive_fused(w.spec);
+    TensorStore st = w.generate(1);
+    bool threw = false;
+    try {
+      run_cuda(prog, TreeConfig{{w.spec.axis_len(), 1}}, st);
+    } catch (const NotFusable&) {
+      threw = true;
+    }
+    if (!threw) ++failures;
+    std::printf("{\"case\": \"%s\", \"mode\": \"no-kernel\", \"not_fusable\": %s}\n", nm,
+                threw ? "true" : "false");
+  }
+  std::printf("{\"failures\": %d}\n", failures);
+  return failures ? 1 : 0;
+}

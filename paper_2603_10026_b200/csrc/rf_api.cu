@@ -431,8 +431,10 @@ rf_status rf_run_host(rf_plan* p, const rf_host_io* io) {
   const int64_t units = units_of(p);
   // Chunking: 8 chunks over independent units, alternating two streams, so
   // the H2D of chunk c+1 and the D2H of chunk c-1 overlap chunk c's kernels.
-  const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(8, units));
-  const int64_t per = (units + nchunk - 1) / nchunk;
+  // GEMM chunks are whole 128-row tiles.
+  const int64_t gran = gemm ? 128 : 1;
+  const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(8, units / gran));
+  const int64_t per = ((units + nchunk - 1) / nchunk + gran - 1) / gran * gran;
   for (int64_t c = 0; c < nchunk; ++c) {
     const int64_t u0 = c * per, nu = std::min(per, units - u0);
     if (nu <= 0) break;
