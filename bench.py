@@ -180,7 +180,7 @@ class Workload:
     """Plan + device/host buffers for one BASELINE config (plan-time work, e.g.
     weight packing, happens here — outside every timed region)."""
 
-    def __init__(self, cfg, dev):
+    def __init__(self, cfg, dev, world=1):
         import torch
 
         from paper_2603_10026_b200 import Desc, Plan
@@ -205,6 +205,11 @@ class Workload:
             self.outputs = [m, torch.empty_like(m), torch.empty_like(q)]
             self.step_inputs = [0, 1, 2]  # all inputs are per-step data
             self.data = "synthetic (uniform, make_attention distributions; q pre-scaled by 1/sqrt(D))"
+            # split-KV decode over G GPUs: this rank's K/V are its shard of a
+            # G x Skv sequence (weak scaling); partials are all-gathered (NCCL)
+            # and merged in slice order inside every step
+            self.split_kv = Sq == 1 and world > 1
+            self.segments_global = cfg.get("segments", 1) * world
         else:
             M, K, Nn = cfg["M"], cfg["K"], cfg["N"]
             if pat == "quant":
@@ -232,7 +237,13 @@ class Workload:
         torch.cuda.synchronize()
 
     def run(self, stream):
-        self.plan.run(self.inputs, self.outputs, stream)
+        if getattr(self, "split_kv", False):
+            from paper_2603_10026_b200.distributed import split_kv_decode
+
+            q, k, v = self.inputs
+            split_kv_decode(q, k, v, self.segments_global, stream=stream)
+        else:
+            self.plan.run(self.inputs, self.outputs, stream)
 
     def host_buffers(self):
         import torch
@@ -249,7 +260,7 @@ def run_ours(args, cfg):
 
     world, rank, local = dist_setup(args)
     dev = torch.device("cuda", torch.cuda.current_device())
-    wl = Workload(cfg, dev)
+    wl = Workload(cfg, dev, world)
     plan = wl.plan
     stream = torch.cuda.Stream(device=dev)
     flops, nbytes = work_of(cfg)
@@ -329,8 +340,10 @@ def run_ours(args, cfg):
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
         traffic = json.load(open(prof)).get(cfg["name"].split(":")[0])
-    conf = {"workload": cfg["name"], "kernel": plan.info["kernel"],
-            "parallelism": f"batch/head (or token) shards x{world}, no data-path collective",
+    par = (f"split-KV over {world} GPUs: local partials + NCCL all-gather + slice-ordered merge"
+           if getattr(wl, "split_kv", False)
+           else f"batch/head (or token) shards x{world}, no data-path collective")
+    conf = {"workload": cfg["name"], "kernel": plan.info["kernel"], "parallelism": par,
             "l2": f"step inputs {sum(wl.inputs[i].numel() * wl.inputs[i].element_size() for i in wl.step_inputs) / 1e6:.0f} MB"
                   " vs 126 MB L2, no flush"}
     conf.update({k: v for k, v in cfg.items() if k not in ("name", "pattern", "dtype")})

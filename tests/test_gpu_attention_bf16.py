@@ -79,3 +79,46 @@ def test_decode_odd_slice_uses_generic_path():
 def test_bf16_ragged_prefill_generic_path():
     errs, _ = _run(1, 2, 100, 300, 64)
     assert max(errs) < TOL
+
+
+@pytest.mark.parametrize("dtype_name,shape,S", [("bf16", (2, 4, 1, 8192, 128), 8),
+                                                 ("f32", (1, 2, 64, 1024, 64), 4)])
+def test_split_kv_shards_merge_equals_multisegment(dtype_name, shape, S):
+    """Two KV shards (as two GPUs would hold them): rf_run_partials on each
+    local shard, concatenation in rank = slice order (what the NCCL all-gather
+    produces), rf_merge_partials == single-device run_multisegment(S)."""
+    import torch
+    from paper_2603_10026_b200 import Desc, Plan, _native as N
+    from paper_2603_10026_b200.distributed import kv_shard, split_kv_decode
+
+    dt = torch.bfloat16 if dtype_name == "bf16" else torch.float32
+    B, H, Sq, Skv, D = shape
+    q, k, v = _inputs(B, H, Sq, Skv, D, 21, dt)
+    qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
+    G = 2
+    parts = []
+    for r in range(G):
+        kv0, kv1, s0, local = kv_shard(r, G, Skv, S)
+        p = Plan(Desc(N.RF_PATTERN_ATTENTION, dtype_name, rows=Sq, len=kv1 - kv0, free_len=D,
+                      batch=B, heads=H, segments=local))
+        rows = B * H * Sq
+        pm = torch.empty(local, rows, device="cuda")
+        pl = torch.empty_like(pm)
+        po = torch.empty(local, rows, D, device="cuda")
+        p.run_partials([qd, kd[:, :, kv0:kv1].contiguous(), vd[:, :, kv0:kv1].contiguous()], 0,
+                       pm, pl, po)
+        parts.append((pm, pl, po))
+    pm = torch.cat([x[0] for x in parts])
+    pl = torch.cat([x[1] for x in parts])
+    po = torch.cat([x[2] for x in parts])
+    m = torch.empty(B, H, Sq, device="cuda")
+    l = torch.empty_like(m)
+    o = torch.empty_like(qd)
+    p.merge_partials(pm, pl, po, [m, l, o])
+    torch.cuda.synchronize()
+    tol = 2e-2 if dt == torch.bfloat16 else 1e-5
+    _check(q, k, v, m, l, o, tol)
+    # the single-rank path of split_kv_decode (no process group) is the same plan
+    m1, l1, o1 = split_kv_decode(qd, kd, vd, S)
+    torch.cuda.synchronize()
+    _check(q, k, v, m1, l1, o1, tol)
