@@ -60,7 +60,7 @@ typedef enum rf_status {
 } rf_status;
 
 /* Fusible cascade patterns with a kernel (plan layer matches FusedPrograms
- * onto these; see paper_2603_10026_b200/plan.py and DESIGN.md). */
+ * onto these; see include/rf_host.hpp plan() and DESIGN.md). */
 typedef enum rf_pattern {
   /* d1 = max x, d2 = sum exp(x - d1)          (make_safe_softmax, workloads.cpp:38-62) */
   RF_PATTERN_SAFE_SOFTMAX = 1,

@@ -215,10 +215,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int c = 0; c < 4; ++c) tmem_ld32(tSk + c * 32, sr[c]);
       tmem_ld_wait();
 #define SV(j) __uint_as_float(sr[(j) >> 5][(j) & 31])
-      // reduction 1: d1 = max(d1, max_tile)   (store-prev in m_ref / m_true)
-      float tmax = SV(0);
+      // reduction 1: d1 = max(d1, max_tile)   (8 independent chains)
+      float mx[8];
 #pragma unroll
-      for (int j = 1; j < BN; ++j) tmax = fmaxf(tmax, SV(j));
+      for (int j = 0; j < 8; ++j) mx[j] = SV(j);
+#pragma unroll
+      for (int j = 8; j < BN; ++j) mx[j & 7] = fmaxf(mx[j & 7], SV(j));
+      const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
       m_true = fmaxf(m_true, tmax * p.scale);
       // correction exp(d1' - d1): lazily re-base the accumulators
       const bool need = (m_true - m_ref) * kLog2e > kRescaleThreshold;
@@ -228,24 +232,36 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         l *= alpha;
         m_ref = m_true;
       }
-      // reductions 2 and 3: P = exp(S - d1) in bf16 into TMEM, row sum in fp32
-      const float mb = m_ref * kLog2e;
-      float rs = 0.f;
+      // reductions 2 and 3: P = exp(S - d1) in bf16 into TMEM, row sum in fp32.
+      // Pairs in packed f32x2; one pair in four on the FMA pipe (MUFU offload).
+      const uint64_t c12 = f2(c1, c1), nmb2 = f2(-m_ref * kLog2e, -m_ref * kLog2e);
+      uint64_t acc2[4] = {0, 0, 0, 0};
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint32_t pk[32];
+      for (int c = 0; c < 4; ++c) {  // per 32-column chunk: its S registers die here
+        uint32_t pk[16];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int c0 = 64 * h + 2 * j;
-          const float x0 = fmaf(SV(c0), c1, -mb), x1 = fmaf(SV(c0 + 1), c1, -mb);
-          // one of every four exponentials on the FMA pipe (MUFU offload)
-          const float p0 = ex2_mufu(x0);
-          const float p1 = (j & 1) ? ex2_poly(x1) : ex2_mufu(x1);
-          rs += p0 + p1;
-          pk[j] = pack_bf16x2(p0, p1);
+        for (int jj = 0; jj < 16; ++jj) {
+          const int c0 = 32 * c + 2 * jj;
+          const uint64_t x2 = ffma2(f2(SV(c0), SV(c0 + 1)), c12, nmb2);
+          uint64_t p2;
+          if ((jj & 3) == 3) {
+            p2 = ex2_poly2(x2);
+          } else {
+            float x0, x1;
+            f2split(x2, x0, x1);
+            p2 = f2(ex2_mufu(x0), ex2_mufu(x1));
+          }
+          acc2[jj & 3] = fadd2(acc2[jj & 3], p2);
+          float p0, p1;
+          f2split(p2, p0, p1);
+          pk[jj] = pack_bf16x2(p0, p1);
         }
-        tmem_st32(tSk + 32 * h, pk);
+        tmem_st16(tSk + 16 * c, pk);
       }
+      const uint64_t s01 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
+      float rs0, rs1;
+      f2split(s01, rs0, rs1);
+      const float rs = rs0 + rs1;
 #undef SV
       l += rs;
       if (i > 0 && __any_sync(0xffffffffu, need)) {

@@ -341,6 +341,50 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (static_cast<int>(xi) << 23));
 }
 
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2): two lanes of work per issue slot.
+__device__ __forceinline__ uint64_t f2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2split(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// 2^x for a pair on the FMA/ALU pipes only: n = rint(x) via the 1.5*2^23
+// magic-number add (no F2I/FRND, which would issue on the XU pipe like
+// MUFU), f = x - n in [-0.5, 0.5], p = degree-3 fit of 2^f (max rel err
+// 7.7e-5 < bf16's 3.9e-3), 2^x = p * 2^n by an integer add to the exponent.
+// Inputs are clamped at -127 (result ~1e-38); valid for x <= 127.
+__device__ __forceinline__ uint64_t ex2_poly2(uint64_t x2) {
+  float x0, x1;
+  f2split(x2, x0, x1);
+  x2 = f2(fmaxf(x0, -127.f), fmaxf(x1, -127.f));
+  const uint64_t magic = f2(12582912.f, 12582912.f), nmagic = f2(-12582912.f, -12582912.f);
+  const uint64_t t = fadd2(x2, magic);
+  const uint64_t r = fadd2(t, nmagic);
+  const uint64_t f = ffma2(r, f2(-1.f, -1.f), x2);
+  uint64_t p = ffma2(f, f2(0.05508868396282196f, 0.05508868396282196f),
+                     f2(0.24260404706001282f, 0.24260404706001282f));
+  p = ffma2(p, f, f2(0.6932762265205383f, 0.6932762265205383f));
+  p = ffma2(p, f, f2(0.9999289512634277f, 0.9999289512634277f));
+  float p0, p1, t0, t1;
+  f2split(p, p0, p1);
+  f2split(t, t0, t1);
+  return f2(__int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23)),
+            __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
+}
+
 // ---------------------------------------------------------- packing utils --
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
