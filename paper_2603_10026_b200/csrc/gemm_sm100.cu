@@ -206,6 +206,159 @@ __global__ void __launch_bounds__(NT, 1)
 
 }  // namespace rms
 
+// ----------------------------------------------------- RMSNORM_GEMM, 2-SM --
+//
+// CTA pair (cluster of 2) on one 256 x 256 tile: tcgen05.mma.cta_group::2 with
+// M = 256 issued by the leader; each CTA stages its own 128 rows of X and its
+// half (128 N-rows) of W', so per-SM shared-memory traffic for B halves. The
+// peer's tiles land on its local barrier (its statistics warps need them too)
+// and a relay warp forwards that completion to the leader's barrier.
+
+namespace rms2 {
+
+constexpr int BK = 64;
+constexpr int STAGES = 6;
+constexpr int NT = 192;  // warps 0-3 stats + epilogue, 4 TMA, 5 MMA (leader) / relay (peer)
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB: this CTA's 128 rows
+constexpr int B_BYTES = 128 * BK * 2; // 16 KB: this CTA's half of the 256 N-rows
+
+struct Smem {
+  uint8_t a[STAGES][A_BYTES];
+  uint8_t b[STAGES][B_BYTES];
+  uint64_t full[STAGES];       // leader: own tx + peer relay (count 2); peer: own tx (count 1)
+  uint64_t empty[STAGES];      // MMA multicast commit + 4 stats warps
+  uint64_t acc_full;
+  uint32_t tmem_base;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
+    rms_gemm_2sm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                        const __grid_constant__ CUtensorMap ty, const rms::Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = warp_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  int mt, nt;  // mt: 256-row pair tile
+  tile_of(blockIdx.x >> 1, p.mt_count, p.nt_count, p.group_n, mt, nt);
+  const int n0 = nt * BN;
+  const int m0 = mt * 2 * BM + static_cast<int>(rank) * BM;  // this CTA's 128 rows
+  const int kt = static_cast<int>(p.k / BK);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&s.full[i], leader ? 2 : 1);
+      mbar_init(&s.empty[i], 1 + 4);
+    }
+    mbar_init(&s.acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc_2sm<256>(&s.tmem_base);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+
+  if (warp == 4) {
+    if (elect_one()) {
+      prefetch_tmap(&ta);
+      prefetch_tmap(&tb);
+      prefetch_tmap(&ty);
+      for (int t = 0; t < kt; ++t) {
+        const int st = t % STAGES;
+        mbar_wait(&s.empty[st], ((t / STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&s.full[st], A_BYTES + B_BYTES);
+        tma_load_2d(s.a[st], &ta, &s.full[st], t * BK, m0, kEvictNormal);
+        tma_load_2d(s.b[st], &tb, &s.full[st], t * BK, n0 + static_cast<int>(rank) * 128, kEvictLast);
+      }
+    }
+  } else if (warp == 5) {
+    if (leader) {
+      const uint32_t idesc = idesc_f16(2 * BM, BN, kFmtBF16, false, false);
+      const bool el = elect_one();
+      for (int t = 0; t < kt; ++t) {
+        const int st = t % STAGES;
+        mbar_wait(&s.full[st], (t / STAGES) & 1);  // both halves landed
+        tc_fence_after();
+        if (el) {
+          const uint32_t a = smem_u32(s.a[st]), b = smem_u32(s.b[st]);
+#pragma unroll
+          for (int ks = 0; ks < BK / 16; ++ks)
+            mma_f16_ss_2sm(tmem, sdesc_kmajor_sw128(a + ks * 32), sdesc_kmajor_sw128(b + ks * 32),
+                           idesc, (t | ks) != 0);
+          mma_commit_2sm(&s.empty[st]);
+          if (t + 1 == kt) mma_commit_2sm(&s.acc_full);
+        }
+        __syncwarp();
+      }
+    } else if (elect_one()) {
+      // relay: this CTA's tiles have landed -> the leader's full barrier
+      for (int t = 0; t < kt; ++t) {
+        const int st = t % STAGES;
+        mbar_wait(&s.full[st], (t / STAGES) & 1);
+        mbar_arrive_cluster(mapa_shared(smem_u32(&s.full[st]), 0));
+      }
+    }
+  } else {
+    const int r = threadIdx.x;
+    float ss = 0.f;
+    for (int t = 0; t < kt; ++t) {
+      const int st = t % STAGES;
+      mbar_wait(&s.full[st], (t / STAGES) & 1);
+      const uint32_t row = smem_u32(s.a[st]) + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint4 v = lds128(row + ((u ^ (r & 7)) << 4));
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float lo = bf_lo(w[i]), hi = bf_hi(w[i]);
+          ss = fmaf(lo, lo, ss);
+          ss = fmaf(hi, hi, ss);
+        }
+      }
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&s.empty[st]);
+    }
+    const float inv = rsqrtf(fmaf(ss, p.inv_k, p.eps));
+    if (nt == 0) p.d1[m0 + r] = ss;
+    named_bar_sync(1, 128);
+    mbar_wait(&s.acc_full, 0);
+    tc_fence_after();
+    const uint32_t stage = smem_u32(s.a[0]);  // drained: 64 KB of A stages for the Y tile
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+#pragma unroll
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld32(tmem + lane_off + c * 32, v);
+      tmem_ld_wait();
+      const uint32_t chunk = stage + (c >> 1) * (BM * 128);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
+        w.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
+        w.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
+        w.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
+        sts128(chunk + sw128(r, (c & 1) * 4 + q), w);
+      }
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int c = 0; c < BN / 64; ++c) tma_store_2d(&ty, s.a[0] + c * (BM * 128), n0 + 64 * c, m0);
+      bulk_commit();
+      bulk_wait0();
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 5) tmem_dealloc_2sm<256>(tmem);
+}
+
+}  // namespace rms2
+
 
 // ========================================================= QUANT_GEMM_E4M3 ==
 
@@ -495,7 +648,7 @@ cudaError_t launch_rms_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
   {
     const uint64_t dims[2] = {static_cast<uint64_t>(g.k), static_cast<uint64_t>(g.n)};
     const uint64_t str[1] = {static_cast<uint64_t>(g.k) * 2};
-    const uint32_t box[2] = {rms::BK, BN};
+    const uint32_t box[2] = {rms::BK, g.m % (2 * BM) == 0 ? 128u : static_cast<uint32_t>(BN)};
     if (!make_tmap(&tb, g.b, 2, dims, str, box, 2)) return cudaErrorInvalidValue;
   }
   {
@@ -503,6 +656,18 @@ cudaError_t launch_rms_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
     const uint64_t str[1] = {static_cast<uint64_t>(g.n) * 2};
     const uint32_t box[2] = {64, BM};
     if (!make_tmap(&ty, g.c, 2, dims, str, box, 2)) return cudaErrorInvalidValue;
+  }
+  if (g.m % (2 * BM) == 0) {  // 2-SM path
+    rms::Params p{g.d1, g.k, 1.f / static_cast<float>(g.k), g.eps, static_cast<int>(g.m / (2 * BM)),
+                  static_cast<int>(g.n / BN), 8};
+    const size_t smem = sizeof(rms2::Smem) + 1024;
+    cudaError_t e = cudaFuncSetAttribute(rms2::rms_gemm_2sm_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    dim3 grid(static_cast<unsigned>(2 * (g.n / BN) * (g.m / (2 * BM))));
+    rms2::rms_gemm_2sm_kernel<<<grid, rms2::NT, smem, st>>>(ta, tb, ty, p);
+    return cudaGetLastError();
   }
   rms::Params p{g.d1, g.k, 1.f / static_cast<float>(g.k), g.eps, static_cast<int>(g.m / BM),
                 static_cast<int>(g.n / BN), 8};
