@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(NT, 1)
       const int st = t % STAGES;
       mbar_wait(&s.full[st], (t / STAGES) & 1);
       const uint32_t row = smem_u32(s.a[st]) + (r >> 3) * 1024 + (r & 7) * 128;
+      float ts[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         // physical unit u ^ (r & 7): conflict-free across the 8 rows of a phase
@@ -159,10 +160,11 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const float lo = bf_lo(w[i]), hi = bf_hi(w[i]);
-          ss = fmaf(lo, lo, ss);
-          ss = fmaf(hi, hi, ss);
+          ts[i] = fmaf(lo, lo, ts[i]);
+          ts[i] = fmaf(hi, hi, ts[i]);
         }
       }
+      ss += (ts[0] + ts[1]) + (ts[2] + ts[3]);  // per-tile partials: pairwise accumulation
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(&s.empty[st]);
     }
@@ -306,6 +308,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       const int st = t % STAGES;
       mbar_wait(&s.full[st], (t / STAGES) & 1);
       const uint32_t row = smem_u32(s.a[st]) + (r >> 3) * 1024 + (r & 7) * 128;
+      float ts[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const uint4 v = lds128(row + ((u ^ (r & 7)) << 4));
@@ -313,10 +316,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const float lo = bf_lo(w[i]), hi = bf_hi(w[i]);
-          ss = fmaf(lo, lo, ss);
-          ss = fmaf(hi, hi, ss);
+          ts[i] = fmaf(lo, lo, ts[i]);
+          ts[i] = fmaf(hi, hi, ts[i]);
         }
       }
+      ss += (ts[0] + ts[1]) + (ts[2] + ts[3]);  // per-tile partials: pairwise accumulation
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(&s.empty[st]);
     }
@@ -596,6 +600,227 @@ __global__ void __launch_bounds__(NT, 1)
 
 }  // namespace qnt
 
+// ------------------------------------------------------ QUANT_GEMM, 2-SM --
+//
+// CTA pair on a 256 x 512 tile: each CTA quantises its own 128 rows of A into
+// e4m3 (the in-loop correction stays CTA-local: each CTA rescales the TMEM
+// rows it owns) and stages half of each 256-wide W block; the leader issues
+// tcgen05.mma.cta_group::2 (M = 256, N = 256, twice per K step). The peer
+// relays "my W half landed and my A rows are quantised" for every K step.
+
+namespace qnt2 {
+
+using qnt::BK;
+using qnt::BNQ;
+constexpr int SA = 2, SW = 3, S8 = 2;
+constexpr int NT = 192;  // warps 0-3 quantiser + epilogue, 4 TMA, 5 MMA (leader) / relay (peer)
+constexpr int ABF_BYTES = BM * BK * 2;  // 32 KB
+constexpr int W_BYTES = 2 * 128 * BK;   // 32 KB: this CTA's halves of the two 256-row blocks
+constexpr int A8_BYTES = BM * BK;       // 16 KB
+
+struct Smem {
+  uint8_t abf[SA][ABF_BYTES];
+  uint8_t w[SW][W_BYTES];
+  uint8_t a8[S8][A8_BYTES];
+  uint64_t abf_full[SA], abf_empty[SA], w_full[SW], w_empty[SW], a8_full[S8], a8_empty[S8];
+  uint64_t acc_full;
+  uint32_t tmem_base;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
+    quant_gemm_2sm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tw,
+                          const __grid_constant__ CUtensorMap tc, const qnt::Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = warp_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  int mt, nt;
+  tile_of(blockIdx.x >> 1, p.mt_count, p.nt_count, p.group_n, mt, nt);
+  const int n0 = nt * BNQ;
+  const int m0 = mt * 2 * BM + static_cast<int>(rank) * BM;
+  const int kt = static_cast<int>(p.k / BK);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < SA; ++i) {
+      mbar_init(&s.abf_full[i], 1);
+      mbar_init(&s.abf_empty[i], 4);
+    }
+    for (int i = 0; i < SW; ++i) {
+      mbar_init(&s.w_full[i], 1);
+      mbar_init(&s.w_empty[i], 1);
+    }
+    for (int i = 0; i < S8; ++i) {
+      mbar_init(&s.a8_full[i], leader ? 4 + 1 : 4);  // leader: + peer relay
+      mbar_init(&s.a8_empty[i], 1);
+    }
+    mbar_init(&s.acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc_2sm<512>(&s.tmem_base);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+
+  if (warp == 4) {
+    if (elect_one()) {
+      prefetch_tmap(&ta);
+      prefetch_tmap(&tw);
+      prefetch_tmap(&tc);
+      for (int t = 0; t < kt; ++t) {
+        const int sa = t % SA, sw = t % SW;
+        mbar_wait(&s.abf_empty[sa], ((t / SA) & 1) ^ 1);
+        mbar_arrive_expect_tx(&s.abf_full[sa], ABF_BYTES);
+        tma_load_2d(s.abf[sa], &ta, &s.abf_full[sa], t * BK, m0, kEvictFirst);
+        tma_load_2d(s.abf[sa] + BM * 128, &ta, &s.abf_full[sa], t * BK + 64, m0, kEvictFirst);
+        mbar_wait(&s.w_empty[sw], ((t / SW) & 1) ^ 1);
+        mbar_arrive_expect_tx(&s.w_full[sw], W_BYTES);
+        for (int h = 0; h < 2; ++h)
+          tma_load_2d(s.w[sw] + h * 128 * 128, &tw, &s.w_full[sw], t * BK,
+                      n0 + 256 * h + 128 * static_cast<int>(rank), kEvictLast);
+      }
+    }
+  } else if (warp == 5) {
+    if (leader) {
+      const uint32_t idesc = idesc_f8(2 * BM, 256);
+      const bool el = elect_one();
+      for (int t = 0; t < kt; ++t) {
+        const int sw = t % SW, s8 = t % S8;
+        mbar_wait(&s.w_full[sw], (t / SW) & 1);
+        mbar_wait(&s.a8_full[s8], (t / S8) & 1);  // own A8 + peer (W half + A8) relay
+        tc_fence_after();
+        if (el) {
+          const uint32_t a = smem_u32(s.a8[s8]), b = smem_u32(s.w[sw]);
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int ks = 0; ks < BK / 32; ++ks)
+              mma_f8_ss_2sm(tmem + h * 256, sdesc_kmajor_sw128(a + ks * 32),
+                            sdesc_kmajor_sw128(b + h * 128 * 128 + ks * 32), idesc, (t | ks) != 0);
+          mma_commit_2sm(&s.w_empty[sw]);
+          mma_commit_2sm(&s.a8_empty[s8]);
+          if (t + 1 == kt) mma_commit_2sm(&s.acc_full);
+        }
+        __syncwarp();
+      }
+    } else if (elect_one()) {
+      for (int t = 0; t < kt; ++t) {
+        const int sw = t % SW, s8 = t % S8;
+        mbar_wait(&s.w_full[sw], (t / SW) & 1);
+        mbar_wait(&s.a8_full[s8], (t / S8) & 1);
+        mbar_arrive_cluster(mapa_shared(smem_u32(&s.a8_full[s8]), 0));
+      }
+    }
+  } else {
+    const int r = threadIdx.x;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    float amax = 0.f, ref = 0.f;
+    for (int t = 0; t < kt; ++t) {
+      const int sa = t % SA, s8 = t % S8;
+      mbar_wait(&s.abf_full[sa], (t / SA) & 1);
+      uint32_t x[64];
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const uint4 q = lds128(smem_u32(s.abf[sa]) + c * (BM * 128) + sw128(r, v));
+          x[32 * c + 4 * v + 0] = q.x;
+          x[32 * c + 4 * v + 1] = q.y;
+          x[32 * c + 4 * v + 2] = q.z;
+          x[32 * c + 4 * v + 3] = q.w;
+        }
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&s.abf_empty[sa]);
+      uint32_t mx = qnt::absmax_bf16x2(x[0], x[1]);
+#pragma unroll
+      for (int i = 2; i < 64; ++i) mx = qnt::absmax_bf16x2(mx, x[i]);
+      const float tile_max = fmaxf(__uint_as_float((mx << 16) & 0x7fffffffu),
+                                   __uint_as_float(mx & 0x7fff0000u));
+      amax = fmaxf(amax, tile_max);
+      const float nref = qnt::pow2_ceil(amax);
+      const bool changed = t > 0 && nref != ref;
+      if (__any_sync(0xffffffffu, changed)) {
+        const int sp = (t - 1) % S8;
+        mbar_wait(&s.a8_empty[sp], ((t - 1) / S8) & 1);  // MMA of tile t-1 complete
+        tc_fence_after();
+        const float f = changed ? ref / nref : 1.f;
+#pragma unroll 1
+        for (int c = 0; c < 2 * 256 / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tmem + lane_off + c * 32, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * f);
+          tmem_st32(tmem + lane_off + c * 32, v);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+      }
+      ref = nref;
+      const float sc = p.fmax / ref;
+      uint64_t sc2;
+      asm("mov.b64 %0, {%1, %1};" : "=l"(sc2) : "f"(sc));
+      mbar_wait(&s.a8_empty[s8], ((t / S8) & 1) ^ 1);
+      const uint32_t dst = smem_u32(s.a8[s8]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        uint32_t w[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const uint32_t lo = qnt::quant_pair(x[8 * u + 2 * h], sc2);
+          const uint32_t hi = qnt::quant_pair(x[8 * u + 2 * h + 1], sc2);
+          w[h] = (lo & 0xffffu) | (hi << 16);
+        }
+        sts128(dst + sw128(r, u), make_uint4(w[0], w[1], w[2], w[3]));
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&s.a8_full[s8]);
+    }
+    const float fin = ref / amax;
+    if (!(amax > 0.f)) atomicExch(p.domain_flag, 1);
+    if (nt == 0) p.d1[m0 + r] = amax;
+    named_bar_sync(1, 128);
+    mbar_wait(&s.acc_full, 0);
+    tc_fence_after();
+    const uint32_t stage = smem_u32(s.abf[0]);  // abf + w: 160 KB drained, C half-tile = 128 KB
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_off + h * 256 + c * 32, v);
+        tmem_ld_wait();
+        const uint32_t chunk = stage + c * (BM * 128);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          sts128(chunk + sw128(r, u),
+                 make_uint4(__float_as_uint(__uint_as_float(v[4 * u]) * fin),
+                            __float_as_uint(__uint_as_float(v[4 * u + 1]) * fin),
+                            __float_as_uint(__uint_as_float(v[4 * u + 2]) * fin),
+                            __float_as_uint(__uint_as_float(v[4 * u + 3]) * fin)));
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          tma_store_2d(&tc, s.abf[0] + c * (BM * 128), n0 + h * 256 + 32 * c, m0);
+        bulk_commit();
+        bulk_wait_read0();
+      }
+      named_bar_sync(1, 128);
+    }
+    if (threadIdx.x == 0) bulk_wait0();
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 5) tmem_dealloc_2sm<512>(tmem);
+}
+
+}  // namespace qnt2
+
 // ============================================================== packing ====
 
 // w [K,N] f32 (reduce-axis major) -> out [N,K]: transposed, g folded (rms) or
@@ -692,7 +917,7 @@ cudaError_t launch_quant_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
   {
     const uint64_t dims[2] = {static_cast<uint64_t>(g.k), static_cast<uint64_t>(g.n)};
     const uint64_t str[1] = {static_cast<uint64_t>(g.k)};
-    const uint32_t box[2] = {qnt::BK, 256};
+    const uint32_t box[2] = {qnt::BK, g.m % (2 * BM) == 0 ? 128u : 256u};
     if (!make_tmap(&tw, g.b, 2, dims, str, box, 1)) return cudaErrorInvalidValue;
   }
   {
@@ -700,6 +925,18 @@ cudaError_t launch_quant_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
     const uint64_t str[1] = {static_cast<uint64_t>(g.n) * 4};
     const uint32_t box[2] = {32, BM};
     if (!make_tmap(&tc, g.c, 2, dims, str, box, 4)) return cudaErrorInvalidValue;
+  }
+  if (g.m % (2 * BM) == 0) {  // 2-SM path
+    qnt::Params p{g.d1, g.domain_flag, g.k, g.fmax, static_cast<int>(g.m / (2 * BM)),
+                  static_cast<int>(g.n / qnt::BNQ), 4};
+    const size_t smem = sizeof(qnt2::Smem) + 1024;
+    cudaError_t e = cudaFuncSetAttribute(qnt2::quant_gemm_2sm_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    dim3 grid(static_cast<unsigned>(2 * (g.n / qnt::BNQ) * (g.m / (2 * BM))));
+    qnt2::quant_gemm_2sm_kernel<<<grid, qnt2::NT, smem, st>>>(ta, tw, tc, p);
+    return cudaGetLastError();
   }
   qnt::Params p{g.d1, g.domain_flag, g.k, g.fmax, static_cast<int>(g.m / BM),
                 static_cast<int>(g.n / qnt::BNQ), 4};

@@ -31,7 +31,8 @@ def _rms_run(x, g, w, eps=1e-6):
     return ss.double().cpu().numpy(), y.double().cpu().numpy(), wp.double().cpu().numpy()
 
 
-@pytest.mark.parametrize("shape", [(128, 64, 256), (256, 512, 512), (384, 1024, 768)])
+@pytest.mark.parametrize("shape", [(128, 64, 256), (256, 512, 512), (384, 1024, 768),
+                                   (512, 4096, 512)])
 def test_rmsnorm_gemm_vs_oracle(shape):
     T, K, N = shape
     rng = np.random.default_rng(T + K + N)
@@ -116,10 +117,11 @@ def test_quant_gemm_vs_oracle(shape):
     assert rel < 0.06
 
 
-def test_quant_gemm_rescale_path():
+@pytest.mark.parametrize("M", [128, 256])  # 1-SM and 2-SM (cta_group::2) kernels
+def test_quant_gemm_rescale_path(M):
     """Magnitudes growing along K force ref (power of two >= running absmax) to
     change on many tiles: the in-loop accumulator correction ref'/ref runs."""
-    M, K, N = 128, 1024, 512
+    K, N = 1024, 512
     rng = np.random.default_rng(3)
     grow = 2.0 ** (np.arange(K) // 128)  # x2 per tile
     a = O.round_bf16(rng.uniform(-1, 1, (M, K)) * grow)
@@ -130,13 +132,14 @@ def test_quant_gemm_rescale_path():
     assert _err(c, cr) < 1e-3
 
 
-def test_quant_gemm_known_answer_and_domain_error():
+@pytest.mark.parametrize("M", [128, 256])
+def test_quant_gemm_known_answer_and_domain_error(M):
     """test_simulator.cpp:53-68: a=[1], w=[[2]] -> d1 = 1, d2 = 896 (padded to a
     tile); an all-zero row is the reference's DomainError (0/0) at finalize."""
     import torch
     from paper_2603_10026_b200 import DomainError
 
-    a = np.zeros((128, 128))
+    a = np.zeros((M, 128))
     a[0, 0] = 1.0
     a[1, :] = 0.0  # all-zero row
     a[2:, :] = 0.5
