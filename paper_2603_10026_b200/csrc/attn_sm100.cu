@@ -37,6 +37,15 @@
 #include "rf_internal.h"
 #include "sm100.cuh"
 
+#ifdef RF_ATTN_TRACE
+// Test-only timeline (tools/trace_attention.py): clock64 stamps of CTA (0,0,0).
+__device__ long long g_attn_trace[4096];
+#define RF_TRACE(idx) \
+  do { if ((blockIdx.x | blockIdx.y | blockIdx.z) == 0) g_attn_trace[(idx)] = clock64(); } while (0)
+#else
+#define RF_TRACE(idx) do {} while (0)
+#endif
+
 namespace rf {
 namespace {
 
@@ -48,6 +57,8 @@ constexpr int NSLOT = 4;      // K/V ring slots
 constexpr int NTHREADS = 320;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+// Pairs of exponentials evaluated by the FMA-pipe polynomial instead of MUFU.
+__device__ __forceinline__ constexpr bool kPolyPairs(int jj) { return (jj & 3) == 3; }
 
 template <int D>
 struct Smem {
@@ -122,6 +133,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int slot = t % NSLOT;
         const uint32_t ph = (t / NSLOT) & 1;
         mbar_wait(&s.kv_empty[slot], ph ^ 1);
+        RF_TRACE(1536 + t);
         mbar_arrive_expect_tx(&s.kv_full[slot], Smem<D>::kTile);
         const CUtensorMap* m = (t & 1) ? &tv : &tk;
         const int32_t y = ky + (t >> 1) * BN;
@@ -180,15 +192,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // tile 0: PV0_i then S0_{i+1}
       mbar_wait(&s.p_full[0], ph);
       tc_fence_after();
+      if (leader) RF_TRACE(1024 + 4 * i + 0);
       issue_pv(0, sV, i > 0, last);
       if (!last) {
         mbar_wait(&s.kv_full[sK], phK);
         tc_fence_after();
+        if (leader) RF_TRACE(1024 + 4 * i + 1);
         issue_s(0, sK);
       }
       // tile 1: PV1_i then S1_{i+1}
       mbar_wait(&s.p_full[1], ph);
       tc_fence_after();
+      if (leader) RF_TRACE(1024 + 4 * i + 2);
       issue_pv(1, sV, i > 0, last);
       release(sV);
       if (!last) {
@@ -210,6 +225,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int i = 0; i < n_tiles; ++i) {
       mbar_wait(&s.s_full[k], i & 1);
       tc_fence_after();
+      if ((threadIdx.x & 127) == 0) RF_TRACE(512 * k + 4 * i + 0);
       uint32_t sr[4][32];
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld32(tSk + c * 32, sr[c]);
@@ -223,6 +239,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int j = 8; j < BN; ++j) mx[j & 7] = fmaxf(mx[j & 7], SV(j));
       const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      if ((threadIdx.x & 127) == 0) RF_TRACE(512 * k + 4 * i + 3);
       m_true = fmaxf(m_true, tmax * p.scale);
       // correction exp(d1' - d1): lazily re-base the accumulators
       const bool need = (m_true - m_ref) * kLog2e > kRescaleThreshold;
@@ -244,7 +261,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int c0 = 32 * c + 2 * jj;
           const uint64_t x2 = ffma2(f2(SV(c0), SV(c0 + 1)), c12, nmb2);
           uint64_t p2;
-          if ((jj & 3) == 3) {
+          if (kPolyPairs(jj)) {
             p2 = ex2_poly2(x2);
           } else {
             float x0, x1;
@@ -275,9 +292,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tmem_st32(tOk + c * 32, r);
         }
       }
+      if ((threadIdx.x & 127) == 0) RF_TRACE(512 * k + 4 * i + 1);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
+      if ((threadIdx.x & 127) == 0) RF_TRACE(512 * k + 4 * i + 2);
       if ((threadIdx.x & 31) == 0) mbar_arrive(&s.p_full[k]);
     }
     // ---- finalize (finalize_root): d2 re-based to the true d1, d3 = O / d2 ----
