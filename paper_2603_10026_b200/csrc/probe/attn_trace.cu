@@ -16,3 +16,4 @@ extern "C" int rf_probe_attn_trace(const void* q, const void* k, const void* v, 
   cudaMemcpyFromSymbol(out, g_attn_trace, sizeof(long long) * 4096);
   return 0;
 }
+

@@ -36,3 +36,22 @@ per = [(t[4 * (i + 1)] - t[4 * i]) for i in range(n - 1)]
 print("cycles per tile (softmax0 S-ready to S-ready):", sorted(per)[len(per) // 2])
 sm = [t[4 * i + 2] - t[4 * i] for i in range(n)]
 print("softmax0 busy per tile (S ready -> P released):", sorted(sm)[len(sm) // 2])
+
+# ---- the 2-SM (CTA pair) kernel: first cluster ----
+h.rf_probe_attn2_trace.restype = ctypes.c_int
+for _ in range(3):
+    rc = h.rf_probe_attn2_trace(*(ctypes.c_void_p(t.data_ptr()) for t in (q, k, v, o, m, l)),
+                                ctypes.c_longlong(B * H), ctypes.c_longlong(S), buf)
+assert rc == 0, rc
+t = list(buf)
+t0 = t[2048]
+print("2-SM: tile | S issue, PV issue | CTA0 Srdy maxd Prel | CTA1 Srdy maxd Prel | peer P relay")
+for i in range(n):
+    mm = [t[2048 + 4 * i + j] - t0 for j in range(2)]
+    a = [t[4 * i + j] - t0 for j in range(3)]
+    b = [t[1024 + 4 * i + j] - t0 for j in range(3)]
+    print(f"{i:3d} | {mm} | {a} | {b} | {t[3072 + i] - t0}")
+per = [(t[4 * (i + 1)] - t[4 * i]) for i in range(n - 1)]
+print("2-SM cycles per tile (CTA0 S-ready to S-ready):", sorted(per)[len(per) // 2])
+sm = [t[4 * i + 2] - t[4 * i] for i in range(n)]
+print("2-SM softmax busy per tile:", sorted(sm)[len(sm) // 2])
