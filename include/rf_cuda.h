@@ -71,7 +71,10 @@ typedef enum rf_pattern {
    * the running d1                            (make_quant_gemm, workloads.cpp:173-209) */
   RF_PATTERN_QUANT_GEMM_E4M3 = 3,
   /* d1 = sum x^2, d2[f] = sum x g / sqrt(d1/K + eps) w[l,f]   (DSL cascade) */
-  RF_PATTERN_RMSNORM_GEMM = 4
+  RF_PATTERN_RMSNORM_GEMM = 4,
+  /* d1 = max s, d2 = sum exp(s - d1), d3 = top-K' of s, ties to the lowest index
+   *                                           (make_moe_routing, workloads.cpp:124-169) */
+  RF_PATTERN_MOE_ROUTING = 5
 } rf_pattern;
 
 typedef enum rf_dtype { RF_F32 = 0, RF_BF16 = 1, RF_E4M3 = 2 } rf_dtype;
@@ -105,7 +108,10 @@ typedef struct rf_desc {
  *   QUANT_GEMM     in[0] = A [M,K] bf16, in[1] = packed W (rf_pack_weight, e4m3 [N,K]);
  *                  d1 = amax [M] f32, d2 = C [M,N] f32
  *   RMSNORM_GEMM   in[0] = X [T,K] bf16, in[1] = packed W (rf_pack_weight: g folded,
- *                  bf16 [N,K]); d1 = sum x^2 [T] f32, d2 = Y [T,N] bf16        */
+ *                  bf16 [N,K]); d1 = sum x^2 [T] f32, d2 = Y [T,N] bf16
+ *   MOE_ROUTING    in[0] = logits [rows, experts] f32 (len = experts, free_len = K' <= 8);
+ *                  d1, d2 [rows] f32; d3 = [rows, K'] records {f32 value, i32 index}
+ *                  (1-based expert index like OutputVal.topk; 0 = empty slot)          */
 typedef struct rf_io {
   const void* in[4];
   void* d[3];

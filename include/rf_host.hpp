@@ -481,6 +481,17 @@ inline Program plan(const CascadeSpec& spec) {
       return p;
     }
   }
+  if (R.size() == 3 && R[0].op == "max" && R[1].op == "sum" && R[2].op == "topk" &&
+      R[0].free_len == 1 && R[1].free_len == 1 && R[2].topk >= 1 && R[2].topk <= 8) {
+    Binding b;  // make_moe_routing (workloads.cpp:124-169)
+    if (unify(X, R[0].body, b) && unify(un("exp", bin("-", X, dep(1))), R[1].body, b) &&
+        unify(X, R[2].body, b)) {
+      p.pattern = RF_PATTERN_MOE_ROUTING;
+      p.x = b.in["?X"];
+      p.free_len = R[2].topk;
+      return p;
+    }
+  }
   if (R.size() == 3 && R[0].op == "max" && R[1].op == "sum" && R[2].op == "sum" &&
       R[0].free_len == 1 && R[1].free_len == 1 && R[2].free_len > 1) {
     Binding b;
@@ -529,7 +540,7 @@ inline Program plan(const CascadeSpec& spec) {
       }
     }
   }
-  return none("not one of safe_softmax / attention / quant_gemm / rmsnorm_gemm");
+  return none("not one of safe_softmax / attention / moe_routing / quant_gemm / rmsnorm_gemm");
 }
 
 inline Program plan(const std::string& dsl) { return plan(parse_cascade(dsl)); }
@@ -753,6 +764,36 @@ inline ExecReport execute(const Program& prog, const TreeConfig& cfg, long long 
       out(1, {m});
       out(2, {t});
       out(3, std::vector<double>(o.begin(), o.begin() + hd));
+      break;
+    }
+    case RF_PATTERN_MOE_ROUTING: {
+      const int K = static_cast<int>(prog.free_len);
+      rf_desc d = base_desc(RF_PATTERN_MOE_ROUTING, RF_F32);
+      d.rows = 1;
+      d.len = L0;
+      d.free_len = K;
+      PlanHandle h(d);
+      const auto& x = st.array(prog.x).data;
+      std::vector<float> xf(x.begin(), x.end());
+      float m = 0, t = 0;
+      std::vector<int32_t> rec(2 * K);
+      rf_host_io io{};
+      io.in[0] = xf.data();
+      io.d[0] = &m;
+      io.d[1] = &t;
+      io.d[2] = rec.data();
+      check(rf_run_host(h.p, &io));
+      out(1, {m});
+      out(2, {t});
+      OutputVal o;
+      o.id = 3;
+      for (int j = 0; j < K; ++j) {
+        if (rec[2 * j + 1] == 0) break;  // fewer experts than K'
+        float v;
+        std::memcpy(&v, &rec[2 * j], 4);
+        o.topk.emplace_back(static_cast<double>(v), static_cast<long long>(rec[2 * j + 1]));
+      }
+      rep.outputs.push_back(std::move(o));
       break;
     }
     case RF_PATTERN_QUANT_GEMM_E4M3:

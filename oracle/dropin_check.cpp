@@ -97,7 +97,10 @@ int main() {
     check_workload("rmsnorm_gemm_256x48", w, -0.02, {}, 2);
   }
   // no kernel for these: NotFusable from the binding (no CPU fallback)
-  for (const char* nm : {"variance", "moe_routing"}) {
+  // MoE routing: top-k indices must match exactly (compare_reports' index check)
+  check_workload("moe_routing_128x8", make_moe_routing(128, 8), 1e-5, {2, 4}, 3);
+  check_workload("moe_routing_64x6", make_moe_routing(64, 6), 1e-5, {2}, 2);
+  for (const char* nm : {"variance", "sum_sum"}) {
     Workload w = builtin(nm);
     FusedProgram prog = derive_fused(w.spec);
     TensorStore st = w.generate(1);

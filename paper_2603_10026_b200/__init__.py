@@ -15,6 +15,7 @@ from .executors import (  # noqa: F401
     ShapeMismatch,
     UnsupportedPattern,
     attention,
+    moe_routing,
     plan,
     quant_gemm,
     quant_gemm_plan,

@@ -28,6 +28,7 @@ RF_PATTERN_SAFE_SOFTMAX = 1
 RF_PATTERN_ATTENTION = 2
 RF_PATTERN_QUANT_GEMM_E4M3 = 3
 RF_PATTERN_RMSNORM_GEMM = 4
+RF_PATTERN_MOE_ROUTING = 5
 
 # rf_dtype
 RF_F32 = 0

@@ -85,6 +85,11 @@ void io_sizes(const rf_plan* p, size_t in[4], size_t out[3]) {
       out[0] = sizeof(float) * d.rows;
       out[1] = 2 * d.rows * d.free_len;
       break;
+    case RF_PATTERN_MOE_ROUTING:
+      in[0] = sizeof(float) * d.rows * d.len;
+      out[0] = out[1] = sizeof(float) * d.rows;
+      out[2] = 8 * d.rows * d.free_len;
+      break;
   }
 }
 
@@ -97,6 +102,7 @@ const char* kernel_name(rf::Kernel k) {
     case rf::Kernel::AttentionDecode: return "attention_decode (bf16 split-KV, TMA bulk)";
     case rf::Kernel::QuantGemmSm100: return "quant_gemm_sm100 (e4m3 tcgen05 kind::f8f6f4)";
     case rf::Kernel::RmsGemmSm100: return "rmsnorm_gemm_sm100 (bf16 tcgen05 kind::f16)";
+    case rf::Kernel::MoeRouting: return "moe_routing (SIMT, warp per token, bit-exact top-k)";
   }
   return "?";
 }
@@ -188,6 +194,14 @@ rf_status run_range(const rf_plan* p, const rf_io* io, int64_t u0, int64_t nu, c
       return RF_OK;
     }
     case RF_PATTERN_ATTENTION: return attention_run(p, io, u0, nu, st);
+    case RF_PATTERN_MOE_ROUTING: {
+      cudaError_t e = rf::launch_moe_routing(
+          static_cast<const float*>(io->in[0]) + u0 * p->d.len, nu, p->d.len,
+          static_cast<int>(p->d.free_len), static_cast<float*>(io->d[0]) + u0,
+          static_cast<float*>(io->d[1]) + u0, static_cast<char*>(io->d[2]) + 8 * u0 * p->d.free_len, st);
+      if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("moe launch: ") + cudaGetErrorString(e));
+      return RF_OK;
+    }
     default: return gemm_run(p, io, u0, nu, st);
   }
 }
@@ -297,6 +311,13 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
         return bail(RF_ERR_UNSUPPORTED, "GEMM shape has no tcgen05 tiling (need M%128, N%256, K%128)");
       p->kernel = d.pattern == RF_PATTERN_QUANT_GEMM_E4M3 ? rf::Kernel::QuantGemmSm100
                                                           : rf::Kernel::RmsGemmSm100;
+      p->rows_total = d.rows;
+      break;
+    case RF_PATTERN_MOE_ROUTING:
+      if (d.dtype != RF_F32) return bail(RF_ERR_UNSUPPORTED, "moe_routing: f32 logits");
+      if (d.free_len < 1 || d.free_len > 8)
+        return bail(RF_ERR_UNSUPPORTED, "moe_routing: top-k size must be 1..8");
+      p->kernel = rf::Kernel::MoeRouting;
       p->rows_total = d.rows;
       break;
     default:

@@ -31,6 +31,7 @@ enum class Kernel {
   AttentionDecode,    // attn_decode.cu (bf16 split-KV streaming, cfg3)
   QuantGemmSm100,     // gemm_sm100.cu (e4m3 kind::f8f6f4, cfg4)
   RmsGemmSm100,       // gemm_sm100.cu (bf16 kind::f16, cfg5)
+  MoeRouting,         // moe.cu (softmax stats + top-k, bit-exact indices)
 };
 
 // ---- kernel launchers (stream-ordered; return cudaGetLastError()) ----------
@@ -71,6 +72,9 @@ cudaError_t launch_attention_merge(const float* pm, const float* pl, const float
                                    int64_t nslices, int64_t rows, int64_t stride, int64_t d,
                                    float* m, float* l, void* o, int out_dtype,
                                    cudaStream_t st);
+
+cudaError_t launch_moe_routing(const float* s, int64_t rows, int64_t experts, int k, float* d1,
+                               float* d2, void* topk, cudaStream_t st);
 
 // GEMM patterns.
 struct GemmArgs {

@@ -270,3 +270,21 @@ def rmsnorm_gemm(x, w_packed, eps: float = 1e-6, stream=None):
     y = torch.empty((T, Nn), dtype=torch.bfloat16, device=x.device)
     p.run([x.contiguous(), w_packed], [ss, y], stream)
     return ss, y
+
+
+def moe_routing(logits, k: int, stream=None):
+    """MoE routing cascade per token row: d1 = max, d2 = sum exp(s - d1) and the
+    top-k experts (ties to the lowest index). logits: [rows, experts] float32.
+    Returns (d1 [rows], d2 [rows], values [rows, k] f32, indices [rows, k] int32,
+    1-based like the reference's OutputVal.topk; 0 marks an empty slot)."""
+    import torch
+
+    _require(logits.dim() == 2 and logits.dtype == torch.float32, "logits must be float32 [rows, experts]")
+    rows, experts = logits.shape
+    p = plan(Desc(N.RF_PATTERN_MOE_ROUTING, "f32", rows=rows, len=experts, free_len=k,
+                  device=logits.device.index or 0))
+    d1 = torch.empty(rows, dtype=torch.float32, device=logits.device)
+    d2 = torch.empty_like(d1)
+    rec = torch.empty(rows, k, 2, dtype=torch.int32, device=logits.device)
+    p.run([logits.contiguous()], [d1, d2, rec], stream)
+    return d1, d2, rec[..., 0].view(torch.float32), rec[..., 1]

@@ -84,14 +84,20 @@ TEST(dsl_files_parse_and_match_kernels) {
   CHECK(std::fabs(r.inv_k * 4096 - 1.0) < 1e-15);
 }
 
+TEST(moe_routing_matches) {  // proj/data/moe_routing.cascade
+  Program p = plan("cascade moe_routing\ninput s len 128\nreduce 1 op max\n    s[l]\nreduce 2 op sum\n"
+                   "    exp(s[l] - d1)\nreduce 3 op topk 8\n    s[l]\n");
+  CHECK(p.pattern == RF_PATTERN_MOE_ROUTING && p.free_len == 8 && p.x == "s");
+}
+
 TEST(unsupported_cascades_are_not_fusable) {
   // variance / moe_routing / moment_of_inertia have no kernel: NotFusable, no CPU fallback
   CHECK_THROWS_AS(plan("cascade variance\ninput x len 8\nreduce 1 op sum\n    x[l]\n"
                        "reduce 2 op sum\n    x[l] * x[l]\n"),
                   NotFusable);
   CHECK_THROWS_AS(plan("cascade moe\ninput s len 8\nreduce 1 op max\n    s[l]\nreduce 2 op sum\n"
-                       "    exp(s[l] - d1)\nreduce 3 op topk 2\n    s[l]\n"),
-                  NotFusable);
+                       "    exp(s[l] - d1)\nreduce 3 op topk 9\n    s[l]\n"),
+                  NotFusable);  // top-k > 8: no kernel
   // RMS statistic that is not the mean over L0
   CHECK_THROWS_AS(plan("cascade r\ninput x len 8\ninput g len 8\ninput w len 8 free 4\n"
                        "reduce 1 op sum\n    x[l] * x[l]\nreduce 2 op sum free 4\n"
@@ -225,6 +231,19 @@ TEST(softmax_weights_sum_to_one) {  // test_simulator.cpp:162-191
   CHECK(std::fabs(sum - 1.0) < 1e-5);
 }
 
+TEST(topk_reduction_ties_lowest_index) {  // test_simulator.cpp:254-271
+  Program p = plan("cascade route\ninput g len 8\nreduce 1 op max\n    g[l]\nreduce 2 op sum\n"
+                   "    exp(g[l] - d1)\nreduce 3 op topk 3\n    g[l]\n");
+  TensorStore st;
+  st.define("g", 8, 0, {0.3, 0.9, 0.9, -1.0, 0.5, 2.0, 0.1, 0.9});
+  ExecReport r = run_incremental(p, TreeConfig{{8, 4, 1}}, st);
+  CHECK(r.outputs[2].topk.size() == 3);
+  CHECK(r.outputs[2].topk[0].second == 6 && r.outputs[2].topk[0].first == 2.0);
+  CHECK(r.outputs[2].topk[1].second == 2 && std::fabs(r.outputs[2].topk[1].first - 0.9) < 1e-7);
+  CHECK(r.outputs[2].topk[2].second == 3);
+  CHECK(r.outputs[0].v[0] == 2.0);
+}
+
 TEST(rmsnorm_gemm_matches_direct_loop) {
   const long long k = 256, n = 48;
   Program p = plan(rms_dsl(k, n));
@@ -249,6 +268,7 @@ TEST(rmsnorm_gemm_matches_direct_loop) {
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "cpu";
   RUN(dsl_files_parse_and_match_kernels);
+  RUN(moe_routing_matches);
   RUN(unsupported_cascades_are_not_fusable);
   RUN(syntax_errors);
   RUN(compare_reports_flags_corruption_with_a_location);
@@ -260,6 +280,7 @@ int main(int argc, char** argv) {
     RUN(attention_incremental_and_multisegment_match_oracle);
     RUN(softmax_weights_sum_to_one);
     RUN(rmsnorm_gemm_matches_direct_loop);
+    RUN(topk_reduction_ties_lowest_index);
   }
   std::printf("%d checks, %d failures\n", checks, failures);
   return failures ? 1 : 0;
