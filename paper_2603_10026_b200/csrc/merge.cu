@@ -9,8 +9,9 @@
 // tile combine (proj/src/tile_ir.cpp:706-712) the raw partial l_c is read
 // before any rescale (no in-place double count, PAPER.md:1953-1958 caveat).
 //
-// One warp per row, lanes over the head dimension; the fold is sequential in
-// slice order so the result does not depend on scheduling.
+// One warp per row, lanes over the head dimension; the evaluation order is
+// fixed for a given slice count, so results do not depend on scheduling
+// (SPEC.md:407).
 #include <cuda_bf16.h>
 
 #include "rf_internal.h"
@@ -21,45 +22,61 @@ namespace {
 template <typename TO>
 __global__ void merge_kernel(const float* __restrict__ pm, const float* __restrict__ pl,
                              const float* __restrict__ po, int64_t nslices, int64_t rows,
-                             int64_t stride, int64_t d, float* __restrict__ m_out, float* __restrict__ l_out,
-                             TO* __restrict__ o_out) {
+                             int64_t stride, int64_t d, float* __restrict__ m_out,
+                             float* __restrict__ l_out, TO* __restrict__ o_out) {
+  // The slice-ordered fold of incr_push_child has the closed form
+  //   m = max_s m_s,  l = sum_s l_s e^(m_s - m),  O = sum_s O_s l_s e^(m_s - m) / l
+  // (acceptance.cpp:162-178); evaluating it with every slice's loads in flight
+  // (a lane per slice for m_s, l_s; independent O_s loads) keeps the merge off
+  // the latency path. Untouched (empty) slices have l_s = 0 and drop out.
   const int lane = threadIdx.x & 31;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (row >= rows) return;
+  float m = -INFINITY;
+  for (int64_t s0 = 0; s0 < nslices; s0 += 32) {
+    const int64_t s = s0 + lane;
+    const float ms = s < nslices ? pm[s * stride + row] : -INFINITY;
+    m = fmaxf(m, ms);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
   constexpr int MAXC = 8;  // d <= 256
   float o[MAXC];
 #pragma unroll
   for (int i = 0; i < MAXC; ++i) o[i] = 0.f;
-  float m = -INFINITY, l = 0.f;
-  bool touched = false;
-  for (int64_t s = 0; s < nslices; ++s) {
-    const float mc = pm[s * stride + row];
-    const float lc = pl[s * stride + row];
-    if (lc == 0.f && mc == -INFINITY) continue;  // untouched child: merge_plain skips it
-    const float mn = fmaxf(m, mc);
-    const float ar = touched ? __expf(m - mn) : 0.f;
-    const float ac = __expf(mc - mn);
-    const float ln = l * ar + lc * ac;
-    const float inv = 1.f / ln;
-    const float cr = ar * l * inv, cc = ac * lc * inv;
-    const float* oc = po + (s * stride + row) * d;
-#pragma unroll
-    for (int i = 0; i < MAXC; ++i) {
-      int64_t f = lane + 32 * i;
-      if (f < d) o[i] = (touched ? o[i] * cr : 0.f) + oc[f] * cc;
+  float l = 0.f;
+  for (int64_t s0 = 0; s0 < nslices; s0 += 32) {
+    const int64_t s = s0 + lane;
+    float ws = 0.f;
+    if (s < nslices) {
+      const float ls = pl[s * stride + row];
+      if (ls != 0.f) ws = ls * __expf(pm[s * stride + row] - m);
     }
-    m = mn;
-    l = ln;
-    touched = true;
+    float lw = ws;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, off);
+    l += lw;
+    const int nloc = static_cast<int>(nslices - s0 < 32 ? nslices - s0 : 32);
+#pragma unroll 4
+    for (int j = 0; j < nloc; ++j) {
+      const float w = __shfl_sync(0xffffffffu, ws, j);
+      const float* oc = po + ((s0 + j) * stride + row) * d;
+#pragma unroll
+      for (int i = 0; i < MAXC; ++i) {
+        const int64_t f = lane + 32 * i;
+        if (f < d) o[i] = fmaf(oc[f], w, o[i]);
+      }
+    }
   }
+  const float inv = 1.f / l;
 #pragma unroll
   for (int i = 0; i < MAXC; ++i) {
-    int64_t f = lane + 32 * i;
+    const int64_t f = lane + 32 * i;
     if (f < d) {
       if constexpr (sizeof(TO) == 2)
-        o_out[row * d + f] = __float2bfloat16_rn(o[i]);
+        o_out[row * d + f] = __float2bfloat16_rn(o[i] * inv);
       else
-        o_out[row * d + f] = o[i];
+        o_out[row * d + f] = o[i] * inv;
     }
   }
   if (lane == 0) {
