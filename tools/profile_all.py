@@ -14,7 +14,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KERNELS = {0: "attn_f32_kernel", 1: "attn_sm100_kernel", 2: "attn_decode_kernel",
-           3: "quant_gemm_kernel", 4: "rms_gemm_kernel"}
+           3: "quant_gemm", 4: "rms_gemm"}
 METRICS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
@@ -59,10 +59,9 @@ def main():
             summary[f"cfg{c + 1}"] = {"error": str(e)}
             continue
         summary[f"cfg{c + 1}"] = {"kernel": KERNELS[c], **{k: v for k, v in m.items()}}
-        rd = float(m["dram__bytes_read.sum"][0]) * (1e6 if m["dram__bytes_read.sum"][1] == "Mbyte" else
-                                                   1e9 if m["dram__bytes_read.sum"][1] == "Gbyte" else 1)
-        wr = float(m["dram__bytes_write.sum"][0]) * (1e6 if m["dram__bytes_write.sum"][1] == "Mbyte" else
-                                                    1e9 if m["dram__bytes_write.sum"][1] == "Gbyte" else 1)
+        unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        rd = float(m["dram__bytes_read.sum"][0]) * unit[m["dram__bytes_read.sum"][1]]
+        wr = float(m["dram__bytes_write.sum"][0]) * unit[m["dram__bytes_write.sum"][1]]
         traffic[f"cfg{c + 1}"] = rd + wr
     # launch list of the default bench (cold-cache, serialised: shares, not absolutes)
     lcsv = os.path.join(ROOT, "gpurun_out", f"{a.tag}_launches_cfg2.csv")
@@ -72,7 +71,8 @@ def main():
                     "--no-cpu-baseline"], capture_output=True, timeout=900)
     json.dump(summary, open(os.path.join(ROOT, "gpurun_out", f"{a.tag}_ncu_summary.json"), "w"),
               indent=1)
-    json.dump(traffic, open(os.path.join(ROOT, "gpurun_out", f"{a.tag}_traffic.json"), "w"), indent=1)
+    json.dump({k: int(v) for k, v in traffic.items()},
+              open(os.path.join(ROOT, "gpurun_out", f"{a.tag}_traffic.json"), "w"), indent=1)
     print(json.dumps(traffic))
 
 
