@@ -44,6 +44,9 @@ CONFIGS = {
             pattern="quant", M=8192, K=8192, N=8192, dtype="bf16"),
     4: dict(name="cfg5: RMSNorm stats + GEMM T16384 K4096 N11008",
             pattern="rms", M=16384, K=4096, N=11008, dtype="bf16"),
+    # not a BASELINE.json config: the north_star's LayerNorm variant of cfg5
+    5: dict(name="cfg6: LayerNorm stats + GEMM T16384 K4096 N11008 (extra, north_star)",
+            pattern="ln", M=16384, K=4096, N=11008, dtype="bf16"),
 }
 
 
@@ -68,6 +71,8 @@ def work_of(cfg):
     flops = 2.0 * M * N * K
     if cfg["pattern"] == "quant":
         bytes_ = 2 * M * K + N * K + 4 * M * N + 4 * M
+    elif cfg["pattern"] == "ln":  # d3 and d4 both written (bf16), d1/d2 f32
+        bytes_ = 2 * M * K + 2 * N * K + 4 * N + 4 * M * N + 8 * M
     else:
         bytes_ = 2 * M * K + 2 * N * K + 2 * M * N + 4 * M
     return flops, bytes_
@@ -140,7 +145,7 @@ def cpu_reference(cfg, budget_s=12.0, threads=None):
         args = ["quant", str(cfg["K"]), str(cfg["N"]), str(threads), str(threads), "1"]
         sample = f"rows = tokens of K={cfg['K']}, N={cfg['N']}"
     else:
-        args = ["rms", str(cfg["K"]), str(cfg["N"]), str(threads), str(threads), "1"]
+        args = [cfg["pattern"], str(cfg["K"]), str(cfg["N"]), str(threads), str(threads), "1"]
         sample = f"rows = tokens of K={cfg['K']}, N={cfg['N']}"
     out = subprocess.run([REF_DRIVER, "bench"] + args + [f"{budget_s}"], capture_output=True,
                          text=True, timeout=600)
@@ -221,6 +226,18 @@ class Workload:
                 del w
                 self.outputs = [torch.empty(M, device=dev), torch.empty(M, Nn, device=dev)]
                 self.data = "synthetic (make_quant_gemm distributions: a~U(-2,2), w~U(-1,1) packed e4m3)"
+            elif pat == "ln":
+                a = (rnd(M, K) * 2 - 1).bfloat16()
+                self.plan = Plan(Desc(N.RF_PATTERN_LAYERNORM_GEMM, "bf16", rows=M, len=K,
+                                      free_len=Nn, eps=1e-5, device=dev.index))
+                w = rnd(K, Nn) * 2 - 1
+                gam = rnd(K) * 2 - 1
+                wp = self.plan.pack_weight(w, gam)
+                del w
+                self.outputs = [torch.empty(M, device=dev), torch.empty(M, device=dev),
+                                torch.empty(M, Nn, dtype=torch.bfloat16, device=dev),
+                                torch.empty(M, Nn, dtype=torch.bfloat16, device=dev)]
+                self.data = "synthetic (DSL wrap_spec convention: x, g, w ~ U(-1,1); g folded into bf16 W)"
             else:
                 a = (rnd(M, K) * 2 - 1).bfloat16()
                 self.plan = Plan(Desc(N.RF_PATTERN_RMSNORM_GEMM, "bf16", rows=M, len=K,

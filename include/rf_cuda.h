@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define RF_CUDA_ABI_VERSION 1
+#define RF_CUDA_ABI_VERSION 2
 
 typedef enum rf_status {
   RF_OK = 0,
@@ -74,7 +74,12 @@ typedef enum rf_pattern {
   RF_PATTERN_RMSNORM_GEMM = 4,
   /* d1 = max s, d2 = sum exp(s - d1), d3 = top-K' of s, ties to the lowest index
    *                                           (make_moe_routing, workloads.cpp:124-169) */
-  RF_PATTERN_MOE_ROUTING = 5
+  RF_PATTERN_MOE_ROUTING = 5,
+  /* LayerNorm statistics -> GEMM, the variance cascade (workloads.cpp:246-277) extended:
+   * d1 = sum x, d2 = sum x^2, sigma = sqrt(d2/K - (d1/K)^2 + eps),
+   * d3[f] = sum x g w[l,f] / sigma, d4[f] = sum (d1/K) g w[l,f] / sigma;
+   * LayerNorm(x) . W = d3 - d4                    (DSL cascade) */
+  RF_PATTERN_LAYERNORM_GEMM = 6
 } rf_pattern;
 
 typedef enum rf_dtype { RF_F32 = 0, RF_BF16 = 1, RF_E4M3 = 2 } rf_dtype;
@@ -109,12 +114,15 @@ typedef struct rf_desc {
  *                  d1 = amax [M] f32, d2 = C [M,N] f32
  *   RMSNORM_GEMM   in[0] = X [T,K] bf16, in[1] = packed W (rf_pack_weight: g folded,
  *                  bf16 [N,K]); d1 = sum x^2 [T] f32, d2 = Y [T,N] bf16
+ *   LAYERNORM_GEMM in[0] = X [T,K] bf16, in[1] = packed W (rf_pack_weight: bf16 [N,K] of
+ *                  g*w followed by N f32 column sums); d1 = sum x [T] f32, d2 = sum x^2
+ *                  [T] f32, d3 = [T,N] bf16, d4 = [T,N] bf16 (optional: may be null)
  *   MOE_ROUTING    in[0] = logits [rows, experts] f32 (len = experts, free_len = K' <= 8);
  *                  d1, d2 [rows] f32; d3 = [rows, K'] records {f32 value, i32 index}
  *                  (1-based expert index like OutputVal.topk; 0 = empty slot)          */
 typedef struct rf_io {
   const void* in[4];
-  void* d[3];
+  void* d[4];
 } rf_io;
 
 /* Host-memory variant of rf_io (the reference's TensorStore lives on the host):
@@ -152,9 +160,13 @@ int64_t rf_plan_launches_per_run(const rf_plan* plan);
  *   QUANT_GEMM:   w [K,N] f32 (reduce-axis major, the reference layout) ->
  *                 packed e4m3 [N,K] (RNE, satfinite; the static pre-rounded W)
  *   RMSNORM_GEMM: w [K,N] f32, g [K] f32 -> packed bf16 [N,K] of g[l]*w[l,f]
- * `packed` must hold N*K elements of the packed type. Stream-ordered. */
+ *   LAYERNORM_GEMM: as RMSNORM_GEMM, followed by N f32 column sums of the packed
+ *                 (bf16-rounded) g*w, at byte offset 2*N*K
+ * `packed` must hold rf_packed_bytes(plan) bytes. Stream-ordered. */
 rf_status rf_pack_weight(const rf_plan* plan, const void* w, const void* g, void* packed,
                          void* stream);
+/* Bytes of the packed weight buffer for the plan's pattern (0 if none). */
+size_t rf_packed_bytes(const rf_plan* plan);
 
 /* Host-memory variant: uploads w (and g) from host memory, packs them into a
  * freshly allocated device buffer returned in *packed_dev (free it with

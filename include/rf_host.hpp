@@ -540,7 +540,43 @@ inline Program plan(const CascadeSpec& spec) {
       }
     }
   }
-  return none("not one of safe_softmax / attention / moe_routing / quant_gemm / rmsnorm_gemm");
+  if (R.size() == 4 && R[0].op == "sum" && R[1].op == "sum" && R[2].op == "sum" &&
+      R[3].op == "sum" && R[0].free_len == 1 && R[1].free_len == 1 && R[2].free_len >= 1 &&
+      R[3].free_len == R[2].free_len) {
+    // LayerNorm statistics -> GEMM:
+    //   sigma = sqrt(d2 * INVK - d1 * INVK * d1 * INVK + EPS)
+    //   d3: x g w / sigma      d4: d1 * INVK * g w / sigma
+    // (either "... * w / sigma" or "... / sigma * w" operand order)
+    const Expr ik = cvar("ik");
+    const Expr mean = bin("*", dep(1), ik);
+    const Expr sig = un("sqrt", bin("+", bin("-", bin("*", dep(2), ik), bin("*", bin("*", mean, dep(1)), ik)),
+                                    cvar("eps")));
+    const Expr xg = bin("*", X, G), mg = bin("*", mean, G);
+    auto try_form = [&](bool w_first, Binding& b) {
+      const Expr b3 = w_first ? bin("/", bin("*", xg, Wf), sig) : bin("*", bin("/", xg, sig), Wf);
+      const Expr b4 = w_first ? bin("/", bin("*", mg, Wf), sig) : bin("*", bin("/", mg, sig), Wf);
+      return unify(X, R[0].body, b) && unify(bin("*", X, X), R[1].body, b) &&
+             unify(b3, R[2].body, b) && unify(b4, R[3].body, b);
+    };
+    Binding b1, b2;
+    const bool f1 = try_form(true, b1);
+    const bool f2 = !f1 && try_form(false, b2);
+    if (f1 || f2) {
+      Binding& bb = f1 ? b1 : b2;
+      p.pattern = RF_PATTERN_LAYERNORM_GEMM;
+      p.x = bb.in["?X"];
+      p.g = bb.in["?G"];
+      p.w = bb.in["?W"];
+      p.eps = bb.c["eps"];
+      p.inv_k = bb.c["ik"];
+      if (std::fabs(p.inv_k * static_cast<double>(p.L0) - 1.0) > 1e-12)
+        return none("LayerNorm statistics must be means over the reduce axis");
+      p.free_len = R[2].free_len;
+      return p;
+    }
+  }
+  return none("not one of safe_softmax / attention / moe_routing / quant_gemm / rmsnorm_gemm / "
+              "layernorm_gemm");
 }
 
 inline Program plan(const std::string& dsl) { return plan(parse_cascade(dsl)); }
@@ -844,6 +880,54 @@ inline ExecReport execute(const Program& prog, const TreeConfig& cfg, long long 
       out(2, c);
       if (quant && !(d1[0] > 0.0f))  // finalize_root: 0/0 faults propagate
         throw DomainError("division by zero");
+      break;
+    }
+    case RF_PATTERN_LAYERNORM_GEMM: {
+      if (segments != 1) throw NotFusable("GEMM patterns: multi-segment not kernelised");
+      // pad: M to one 256-row pair tile (copies of the row), K with zeros —
+      // which would shift the mean, so K must already be a multiple of 64
+      // (padding changes d1/K and d2/K) — and N with zero weight columns.
+      const long long N = prog.free_len;
+      if (L0 % 64) throw NotFusable("layernorm_gemm: reduce length must be a multiple of 64");
+      const long long Np = round_up(N, 256), M = 256;
+      rf_desc d = base_desc(RF_PATTERN_LAYERNORM_GEMM, RF_BF16);
+      d.rows = M;
+      d.len = L0;
+      d.free_len = Np;
+      d.eps = prog.eps;
+      PlanHandle h(d);
+      const auto& A = st.array(prog.x).data;
+      const auto& W = st.array(prog.w).data;
+      const auto& g = st.array(prog.g).data;
+      std::vector<float> wf(L0 * Np, 0.f), gf(g.begin(), g.end());
+      for (long long l = 0; l < L0; ++l)
+        for (long long f = 0; f < N; ++f) wf[l * Np + f] = static_cast<float>(W[l * N + f]);
+      void* packed = nullptr;
+      check(rf_pack_weight_host(h.p, wf.data(), gf.data(), &packed));
+      std::vector<uint16_t> a(M * L0);
+      for (long long r = 0; r < M; ++r)
+        for (long long l = 0; l < L0; ++l) a[r * L0 + l] = to_bf16(static_cast<float>(A[l]));
+      std::vector<float> d1(M), d2(M);
+      std::vector<uint16_t> c3(M * Np), c4(M * Np);
+      rf_host_io io{};
+      io.in[0] = a.data();
+      io.in[1] = packed;
+      io.d[0] = d1.data();
+      io.d[1] = d2.data();
+      io.d[2] = c3.data();
+      io.d[3] = c4.data();
+      const rf_status s = rf_run_host(h.p, &io);
+      rf_buffer_free(packed);
+      check(s);
+      std::vector<double> y3(N), y4(N);
+      for (long long f = 0; f < N; ++f) {
+        y3[f] = from_bf16(c3[f]);
+        y4[f] = from_bf16(c4[f]);
+      }
+      out(1, {d1[0]});
+      out(2, {d2[0]});
+      out(3, y3);
+      out(4, y4);
       break;
     }
     default: throw NotFusable("unknown pattern");

@@ -63,6 +63,26 @@ static void check_workload(const std::string& name, const Workload& w, double to
   }
 }
 
+// A DSL cascade with uniform(-1, 1) inputs (the reference CLI's generator).
+Workload dsl_workload(const std::string& name, const std::string& dsl) {
+  CascadeSpec spec = parse_cascade(dsl);
+  Workload w;
+  w.name = name;
+  w.spec = spec;
+  w.generate = [spec](std::uint64_t seed) {
+    TensorStore st;
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> u(-1.0, 1.0);
+    for (const auto& in : spec.inputs) {
+      std::vector<double> v(in.len * (in.free_len > 0 ? in.free_len : 1));
+      for (auto& x : v) x = u(rng);
+      st.define(in.name, in.len, in.free_len, v);
+    }
+    return st;
+  };
+  return w;
+}
+
 int main() {
   // fp32 paths: the north_star's 1e-5
   check_workload("attention_256x64", make_attention(256, 64), 1e-5, {2, 4, 8}, 3);
@@ -74,27 +94,25 @@ int main() {
   // 2e-2 same-rounded-input gate is tests/test_gpu_gemm.py. Gated on RMS
   // relative error.
   check_workload("quant_gemm_512x256", make_quant_gemm(512, 256), -0.06, {}, 2);
+  check_workload("rmsnorm_gemm_256x48",
+                 dsl_workload("rmsnorm_gemm",
+                              "cascade rmsnorm_gemm\ninput x len 256\ninput g len 256\n"
+                              "input w len 256 free 48\nconst INVK = 0.00390625\nconst EPS = 1e-6\n"
+                              "reduce 1 op sum\n    x[l] * x[l]\nreduce 2 op sum free 48\n"
+                              "    x[l] * g[l] / sqrt(d1 * INVK + EPS) * w[l, f]\n"),
+                 -0.02, {}, 2);
   {
-    std::ostringstream os;
-    os << "cascade rmsnorm_gemm\ninput x len 256\ninput g len 256\ninput w len 256 free 48\n"
-       << "const INVK = 0.00390625\nconst EPS = 1e-6\nreduce 1 op sum\n    x[l] * x[l]\n"
-       << "reduce 2 op sum free 48\n    x[l] * g[l] / sqrt(d1 * INVK + EPS) * w[l, f]\n";
-    CascadeSpec spec = parse_cascade(os.str());
-    Workload w;
-    w.name = "rmsnorm_gemm";
-    w.spec = spec;
-    w.generate = [spec](std::uint64_t seed) {
-      TensorStore st;
-      std::mt19937_64 rng(seed);
-      std::uniform_real_distribution<double> u(-1.0, 1.0);
-      for (const auto& in : spec.inputs) {
-        std::vector<double> v(in.len * (in.free_len > 0 ? in.free_len : 1));
-        for (auto& x : v) x = u(rng);
-        st.define(in.name, in.len, in.free_len, v);
-      }
-      return st;
-    };
-    check_workload("rmsnorm_gemm_256x48", w, -0.02, {}, 2);
+    const std::string sig = "sqrt(d2 * INVK - d1 * INVK * d1 * INVK + EPS)";
+    check_workload("layernorm_gemm_256x48",
+                   dsl_workload("layernorm_gemm",
+                                "cascade layernorm_gemm\ninput x len 256\ninput g len 256\n"
+                                "input w len 256 free 48\nconst INVK = 0.00390625\n"
+                                "const EPS = 1e-5\nreduce 1 op sum\n    x[l]\n"
+                                "reduce 2 op sum\n    x[l] * x[l]\nreduce 3 op sum free 48\n"
+                                "    x[l] * g[l] * w[l, f] / " + sig +
+                                    "\nreduce 4 op sum free 48\n    d1 * INVK * g[l] * w[l, f] / " +
+                                    sig + "\n"),
+                   -0.02, {}, 2);
   }
   // no kernel for these: NotFusable from the binding (no CPU fallback)
   // MoE routing: top-k indices must match exactly (compare_reports' index check)

@@ -149,6 +149,24 @@ std::string rms_dsl(long long k, long long n, double eps) {
   return os.str();
 }
 
+// LayerNorm statistics -> GEMM: four reductions, two of them
+// free-axis. d3 - d4 = LayerNorm(x) @ W (with g folded in).
+std::string ln_dsl(long long k, long long n, double eps) {
+  std::ostringstream os;
+  os.precision(17);
+  const std::string sig = "sqrt(d2 * INVK - d1 * INVK * d1 * INVK + EPS)";
+  os << "cascade layernorm_gemm\n"
+     << "input x len " << k << "\ninput g len " << k << "\n"
+     << "input w len " << k << " free " << n << "\n"
+     << "const INVK = " << 1.0 / static_cast<double>(k) << "\n"
+     << "const EPS = " << eps << "\n"
+     << "reduce 1 op sum\n    x[l]\n"
+     << "reduce 2 op sum\n    x[l] * x[l]\n"
+     << "reduce 3 op sum free " << n << "\n    x[l] * g[l] * w[l, f] / " << sig << "\n"
+     << "reduce 4 op sum free " << n << "\n    d1 * INVK * g[l] * w[l, f] / " << sig << "\n";
+  return os.str();
+}
+
 void golden_workload(const std::string& dir, const std::string& name,
                      const Workload& w, std::uint64_t seed,
                      const std::vector<long long>& segs) {
@@ -191,18 +209,30 @@ int cmd_golden(const std::string& dir) {
   golden_workload(dir, "sum_sum_1024_s100", make_sum_sum(1024), 100, {2, 8});
   golden_workload(dir, "moe_routing_128x8_s100", make_moe_routing(128, 8), 100, {2, 4});
 
-  // RMSNorm -> GEMM through the reference engine on the DSL spec
+  // RMSNorm / LayerNorm -> GEMM through the reference engine on the DSL spec
   // (no builtin: run_unfused is the oracle, as the reference CLI does).
-  for (auto [k, n, seed] : std::vector<std::tuple<long long, long long, std::uint64_t>>{
-           {64, 32, 100}, {256, 48, 101}}) {
-    CascadeSpec spec = parse_cascade(rms_dsl(k, n, 1e-6));
+  struct DslCase {
+    std::string kind;
+    long long k, n;
+    std::uint64_t seed;
+    double eps;
+  };
+  for (const DslCase& dc : std::vector<DslCase>{{"rmsnorm_gemm", 64, 32, 100, 1e-6},
+                                                {"rmsnorm_gemm", 256, 48, 101, 1e-6},
+                                                {"layernorm_gemm", 64, 32, 100, 1e-5},
+                                                {"layernorm_gemm", 256, 48, 101, 1e-5}}) {
+    const long long k = dc.k, n = dc.n;
+    const std::uint64_t seed = dc.seed;
+    const bool ln = dc.kind == "layernorm_gemm";
+    CascadeSpec spec = parse_cascade(ln ? ln_dsl(k, n, dc.eps) : rms_dsl(k, n, dc.eps));
     FusedProgram prog = derive_fused(spec);
     Case c;
-    c.name = "rmsnorm_gemm_" + std::to_string(k) + "x" + std::to_string(n) + "_s" +
+    c.name = dc.kind + "_" + std::to_string(k) + "x" + std::to_string(n) + "_s" +
              std::to_string(seed);
-    c.note("workload", "rmsnorm_gemm (DSL)");
-    c.note("eps", "1e-6");
-    c.note("corr", prog.decomp(2).corr ? render(prog.decomp(2).corr) : "");
+    c.note("workload", dc.kind + " (DSL)");
+    c.note("eps", ln ? "1e-5" : "1e-6");
+    const int last = ln ? 4 : 2;
+    c.note("corr", prog.decomp(last).corr ? render(prog.decomp(last).corr) : "");
     TensorStore st = dsl_inputs(spec, seed);
     add_store(c, st);
     {
@@ -233,6 +263,10 @@ int cmd_golden(const std::string& dir) {
     FusedProgram p = derive_fused(parse_cascade(rms_dsl(64, 32, 1e-6)));
     for (const auto& d : p.decomps)
       os << "rmsnorm_gemm d" << d.id << " " << (d.corr ? render(d.corr) : "<identity>")
+         << "\n";
+    FusedProgram q = derive_fused(parse_cascade(ln_dsl(64, 32, 1e-5)));
+    for (const auto& d : q.decomps)
+      os << "layernorm_gemm d" << d.id << " " << (d.corr ? render(d.corr) : "<identity>")
          << "\n";
   }
   std::printf("{\"golden\": \"%s\"}\n", dir.c_str());
@@ -312,6 +346,21 @@ struct RmsJob : RowJob {
   double flops_per_row() const override { return 2.0 * k * n + 2.0 * k; }
 };
 
+struct LnJob : RowJob {
+  long long k, n;
+  CascadeSpec spec;
+  FusedProgram prog;
+  LnJob(long long k_, long long n_)
+      : k(k_), n(n_), spec(parse_cascade(ln_dsl(k_, n_, 1e-5))), prog(derive_fused(spec)) {}
+  TensorStore make(std::uint64_t seed) const override { return dsl_inputs(spec, seed); }
+  void run(TensorStore& st) const override {
+    ExecReport r = run_incremental(prog, TreeConfig{{k, 1}}, st);
+    if (r.outputs.size() != 4) std::abort();
+  }
+  // the GEMM (d3); d4 is the rank-1 mean term, counted like the statistics
+  double flops_per_row() const override { return 2.0 * k * n + 3.0 * k; }
+};
+
 struct SoftmaxJob : RowJob {
   long long n;
   Workload w;
@@ -327,7 +376,7 @@ struct SoftmaxJob : RowJob {
 
 int cmd_bench(int argc, char** argv) {
   if (argc < 7) {
-    std::fprintf(stderr, "bench <attention|quant|rms|softmax> <L0> <free> <rows> <threads> [segments]\n");
+    std::fprintf(stderr, "bench <attention|quant|rms|ln|softmax> <L0> <free> <rows> <threads> [segments]\n");
     return 2;
   }
   std::string pat = argv[2];
@@ -340,6 +389,7 @@ int cmd_bench(int argc, char** argv) {
   if (pat == "attention") job = std::make_unique<AttentionJob>(l0, fr, segs);
   else if (pat == "quant") job = std::make_unique<QuantJob>(l0, fr);
   else if (pat == "rms") job = std::make_unique<RmsJob>(l0, fr);
+  else if (pat == "ln") job = std::make_unique<LnJob>(l0, fr);
   else if (pat == "softmax") job = std::make_unique<SoftmaxJob>(l0);
   else return 2;
   if (threads < 1) threads = 1;

@@ -356,6 +356,78 @@ void rfo_rmsnorm_gemm_incremental(const double* x, const double* g, const double
   *d1 = ss;
 }
 
+/* --------------------------------------------------------- layernorm --- */
+
+typedef struct {
+  const double *x, *g, *w;
+  int64_t K, N;
+  double eps;
+  double *d1, *d2, *d3, *d4;
+} ln_ctx;
+
+/* run_unfused order (simulator.cpp:377-421): d1, d2 over the whole row, then
+ * d3[f] = sum x g w / sigma and d4[f] = sum (d1/K) g w / sigma with
+ * sigma = sqrt(d2/K - (d1/K)^2 + eps), exactly the DSL's expression tree. */
+static void ln_row(void* vctx, int64_t row) {
+  ln_ctx* c = (ln_ctx*)vctx;
+  const double* xr = c->x + row * c->K;
+  const double invk = 1.0 / (double)c->K;
+  double s1 = 0, s2 = 0;
+  for (int64_t l = 0; l < c->K; ++l) s1 += xr[l];
+  for (int64_t l = 0; l < c->K; ++l) s2 += xr[l] * xr[l];
+  double sig = sqrt(s2 * invk - s1 * invk * s1 * invk + c->eps);
+  double* y3 = c->d3 + row * c->N;
+  double* y4 = c->d4 + row * c->N;
+  for (int64_t f = 0; f < c->N; ++f) y3[f] = y4[f] = 0.0;
+  for (int64_t l = 0; l < c->K; ++l) {
+    double a3 = xr[l] * c->g[l] / sig;
+    double a4 = s1 * invk * c->g[l] / sig;
+    const double* wr = c->w + l * c->N;
+    for (int64_t f = 0; f < c->N; ++f) {
+      y3[f] += a3 * wr[f];
+      y4[f] += a4 * wr[f];
+    }
+  }
+  c->d1[row] = s1;
+  c->d2[row] = s2;
+}
+
+void rfo_layernorm_gemm(const double* x, const double* g, const double* w, int64_t T,
+                        int64_t K, int64_t N, double eps, double* d1, double* d2, double* d3,
+                        double* d4, int threads) {
+  ln_ctx c = {x, g, w, K, N, eps, d1, d2, d3, d4};
+  for_rows(ln_row, &c, T, threads);
+}
+
+void rfo_layernorm_gemm_incremental(const double* x, const double* g, const double* w,
+                                    int64_t K, int64_t N, double eps, double* d1, double* d2,
+                                    double* d3, double* d4) {
+  const double invk = 1.0 / (double)K;
+  double s1 = 0, s2 = 0;
+  for (int64_t f = 0; f < N; ++f) d3[f] = d4[f] = 0.0;
+  for (int64_t l = 0; l < K; ++l) {
+    double p1 = s1, p2 = s2;
+    s1 += x[l];
+    s2 += x[l] * x[l];
+    double sig = sqrt(s2 * invk - s1 * invk * s1 * invk + eps);
+    if (l > 0) { /* corr3 = sigma'/sigma; corr4 = (d1/d1') * sigma'/sigma */
+      double sigp = sqrt(p2 * invk - p1 * invk * p1 * invk + eps);
+      double c3 = sigp / sig, c4 = (s1 / p1) * sigp / sig;
+      for (int64_t f = 0; f < N; ++f) {
+        d3[f] *= c3;
+        d4[f] *= c4;
+      }
+    }
+    double a3 = x[l] * g[l] / sig, a4 = s1 * invk * g[l] / sig;
+    for (int64_t f = 0; f < N; ++f) {
+      d3[f] += a3 * w[l * N + f];
+      d4[f] += a4 * w[l * N + f];
+    }
+  }
+  *d1 = s1;
+  *d2 = s2;
+}
+
 /* --------------------------------------------------------- moe routing --- */
 
 void rfo_moe_routing(const double* s, int64_t rows, int64_t experts, int64_t k,

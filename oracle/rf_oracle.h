@@ -104,6 +104,21 @@ void rfo_rmsnorm_gemm_incremental(const double* x, const double* g, const double
                                   int64_t K, int64_t N, double eps, double* d1,
                                   double* y);
 
+/* ---- LayerNorm statistics -> GEMM -----------------------------------------
+ * The 4-reduction DSL cascade, run_unfused order:
+ *   d1 = sum x; d2 = sum x^2; sigma = sqrt(d2/K - (d1/K)^2 + eps)
+ *   d3[f] = sum x g w[l,f] / sigma; d4[f] = sum (d1/K) g w[l,f] / sigma
+ * (LayerNorm(x) @ W = d3 - d4). x: [T, K]; g: [K]; w: [K, N].               */
+void rfo_layernorm_gemm(const double* x, const double* g, const double* w, int64_t T,
+                        int64_t K, int64_t N, double eps, double* d1, double* d2, double* d3,
+                        double* d4, int threads);
+
+/* Incremental form for one token with the corrections derive_fused produces
+ * (d3: sigma'/sigma; d4: (d1/d1') sigma'/sigma).                            */
+void rfo_layernorm_gemm_incremental(const double* x, const double* g, const double* w,
+                                    int64_t K, int64_t N, double eps, double* d1, double* d2,
+                                    double* d3, double* d4);
+
 /* ---- MoE routing: softmax stats + top-k (workloads.cpp:124-169) -----------
  * Descending value, ties to the lowest index (test_workloads.cpp:210-224).
  * idx is 1-based like the reference's OutputVal.topk.                       */

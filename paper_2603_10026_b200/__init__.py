@@ -15,6 +15,8 @@ from .executors import (  # noqa: F401
     ShapeMismatch,
     UnsupportedPattern,
     attention,
+    layernorm_gemm,
+    layernorm_gemm_plan,
     moe_routing,
     plan,
     quant_gemm,
@@ -29,6 +31,8 @@ __all__ = [
     "safe_softmax",
     "quant_gemm",
     "rmsnorm_gemm",
+    "layernorm_gemm",
+    "moe_routing",
     "Plan",
     "Desc",
     "plan",

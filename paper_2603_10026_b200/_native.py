@@ -29,6 +29,9 @@ RF_PATTERN_ATTENTION = 2
 RF_PATTERN_QUANT_GEMM_E4M3 = 3
 RF_PATTERN_RMSNORM_GEMM = 4
 RF_PATTERN_MOE_ROUTING = 5
+RF_PATTERN_LAYERNORM_GEMM = 6
+
+ABI_VERSION = 2
 
 # rf_dtype
 RF_F32 = 0
@@ -57,7 +60,7 @@ class rf_desc(ctypes.Structure):
 
 
 class rf_io(ctypes.Structure):
-    _fields_ = [("in_", ctypes.c_void_p * 4), ("d", ctypes.c_void_p * 3)]
+    _fields_ = [("in_", ctypes.c_void_p * 4), ("d", ctypes.c_void_p * 4)]
 
 
 class rf_partials(ctypes.Structure):
@@ -81,6 +84,7 @@ SIGNATURES = {
     "rf_plan_launches_per_run": (ctypes.c_int64, [_P]),
     "rf_pack_weight": (ctypes.c_int, [_P, _P, _P, _P, _P]),
     "rf_pack_weight_host": (ctypes.c_int, [_P, _P, _P, ctypes.POINTER(_P)]),
+    "rf_packed_bytes": (ctypes.c_size_t, [_P]),
     "rf_buffer_free": (None, [_P]),
     "rf_run": (ctypes.c_int, [_P, ctypes.POINTER(rf_io), _P]),
     "rf_run_host": (ctypes.c_int, [_P, ctypes.POINTER(rf_io)]),
@@ -119,7 +123,7 @@ def lib() -> ctypes.CDLL:
                 fn = getattr(h, name)
                 fn.restype = res
                 fn.argtypes = args
-            if h.rf_abi_version() != 1:
+            if h.rf_abi_version() != ABI_VERSION:
                 raise NativeLibraryMissing("librf_cuda ABI version mismatch")
             _lib = h
         return _lib

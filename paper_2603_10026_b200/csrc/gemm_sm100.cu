@@ -83,6 +83,9 @@ struct Params {
   int64_t k;
   float inv_k, eps;
   int mt_count, nt_count, group_n;
+  float* d2;            // layernorm: sum x^2 (d1 then holds sum x)
+  const float* colsum;  // layernorm: column sums of the packed g*w
+  int write_d4;         // layernorm: d4 requested
 };
 
 __global__ void __launch_bounds__(NT, 1)
@@ -233,9 +236,14 @@ struct Smem {
   uint32_t tmem_base;
 };
 
+// LN = false: RMSNORM_GEMM; LN = true: LAYERNORM_GEMM (the variance cascade
+// d1 = sum x, d2 = sum x^2 from the same tiles; d3 = acc / sigma and
+// d4 = (d1/K) / sigma * colsum in the epilogue — both corrections telescope).
+template <bool LN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     rms_gemm_2sm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-                        const __grid_constant__ CUtensorMap ty, const rms::Params p) {
+                        const __grid_constant__ CUtensorMap ty, const __grid_constant__ CUtensorMap ty4,
+                        const rms::Params p) {
   extern __shared__ uint8_t smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = warp_id();
@@ -266,6 +274,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       prefetch_tmap(&ta);
       prefetch_tmap(&tb);
       prefetch_tmap(&ty);
+      if (LN) prefetch_tmap(&ty4);
       for (int t = 0; t < kt; ++t) {
         const int st = t % STAGES;
         mbar_wait(&s.empty[st], ((t / STAGES) & 1) ^ 1);
@@ -303,12 +312,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     }
   } else {
     const int r = threadIdx.x;
-    float ss = 0.f;
+    float ss = 0.f, sx = 0.f;
     for (int t = 0; t < kt; ++t) {
       const int st = t % STAGES;
       mbar_wait(&s.full[st], (t / STAGES) & 1);
       const uint32_t row = smem_u32(s.a[st]) + (r >> 3) * 1024 + (r & 7) * 128;
-      float ts[4] = {0.f, 0.f, 0.f, 0.f};
+      float ts[4] = {0.f, 0.f, 0.f, 0.f}, tx[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const uint4 v = lds128(row + ((u ^ (r & 7)) << 4));
@@ -318,14 +327,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
           const float lo = bf_lo(w[i]), hi = bf_hi(w[i]);
           ts[i] = fmaf(lo, lo, ts[i]);
           ts[i] = fmaf(hi, hi, ts[i]);
+          if (LN) tx[i] += lo + hi;
         }
       }
       ss += (ts[0] + ts[1]) + (ts[2] + ts[3]);  // per-tile partials: pairwise accumulation
+      if (LN) sx += (tx[0] + tx[1]) + (tx[2] + tx[3]);
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(&s.empty[st]);
     }
-    const float inv = rsqrtf(fmaf(ss, p.inv_k, p.eps));
-    if (nt == 0) p.d1[m0 + r] = ss;
+    float inv, mean = 0.f;
+    if (LN) {
+      mean = sx * p.inv_k;
+      inv = rsqrtf(fmaf(ss, p.inv_k, -mean * mean) + p.eps);  // 1/sigma
+      if (nt == 0) {
+        p.d1[m0 + r] = sx;
+        p.d2[m0 + r] = ss;
+      }
+    } else {
+      inv = rsqrtf(fmaf(ss, p.inv_k, p.eps));
+      if (nt == 0) p.d1[m0 + r] = ss;
+    }
     named_bar_sync(1, 128);
     mbar_wait(&s.acc_full, 0);
     tc_fence_after();
@@ -353,8 +374,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
 #pragma unroll
       for (int c = 0; c < BN / 64; ++c) tma_store_2d(&ty, s.a[0] + c * (BM * 128), n0 + 64 * c, m0);
       bulk_commit();
-      bulk_wait0();
+      bulk_wait_read0();
     }
+    if (LN && p.write_d4) {
+      // d4 = (d1/K) / sigma * colsum[f]: a rank-1 tile, staged the same way
+      named_bar_sync(1, 128);  // staging area free again
+      const float mi = mean * inv;
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        const uint32_t chunk = stage + (c >> 1) * (BM * 128);
+        const float* cs = p.colsum + n0 + c * 32;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 c0 = __ldg(reinterpret_cast<const float4*>(cs + 8 * q));
+          const float4 c1 = __ldg(reinterpret_cast<const float4*>(cs + 8 * q + 4));
+          uint4 w;
+          w.x = pack_bf16x2(mi * c0.x, mi * c0.y);
+          w.y = pack_bf16x2(mi * c0.z, mi * c0.w);
+          w.z = pack_bf16x2(mi * c1.x, mi * c1.y);
+          w.w = pack_bf16x2(mi * c1.z, mi * c1.w);
+          sts128(chunk + sw128(r, (c & 1) * 4 + q), w);
+        }
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int c = 0; c < BN / 64; ++c) tma_store_2d(&ty4, s.a[0] + c * (BM * 128), n0 + 64 * c, m0);
+        bulk_commit();
+      }
+    }
+    if (threadIdx.x == 0) bulk_wait0();
   }
   tc_fence_before();
   cluster_sync();
@@ -857,13 +907,16 @@ __global__ void pack_kernel(const float* __restrict__ w, const float* __restrict
 bool gemm_sm100_supports(int pattern, int64_t m, int64_t n, int64_t k) {
   if (m % BM || n % BN) return false;
   if (pattern == RF_PATTERN_RMSNORM_GEMM) return k % rms::BK == 0;
+  if (pattern == RF_PATTERN_LAYERNORM_GEMM) return k % rms::BK == 0 && m % (2 * BM) == 0;
   if (pattern == RF_PATTERN_QUANT_GEMM_E4M3) return n % qnt::BNQ == 0 && k % qnt::BK == 0;
   return false;
 }
 
-cudaError_t launch_rms_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
-  if (!gemm_sm100_supports(RF_PATTERN_RMSNORM_GEMM, g.m, g.n, g.k)) return cudaErrorNotSupported;
-  CUtensorMap ta, tb, ty;
+static cudaError_t launch_rms_like(const GemmArgs& g, cudaStream_t st, bool ln) {
+  if (!gemm_sm100_supports(ln ? RF_PATTERN_LAYERNORM_GEMM : RF_PATTERN_RMSNORM_GEMM, g.m, g.n, g.k))
+    return cudaErrorNotSupported;
+  const bool pair = g.m % (2 * BM) == 0;
+  CUtensorMap ta, tb, ty, ty4;
   {
     const uint64_t dims[2] = {static_cast<uint64_t>(g.k), static_cast<uint64_t>(g.m)};
     const uint64_t str[1] = {static_cast<uint64_t>(g.k) * 2};
@@ -873,7 +926,7 @@ cudaError_t launch_rms_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
   {
     const uint64_t dims[2] = {static_cast<uint64_t>(g.k), static_cast<uint64_t>(g.n)};
     const uint64_t str[1] = {static_cast<uint64_t>(g.k) * 2};
-    const uint32_t box[2] = {rms::BK, g.m % (2 * BM) == 0 ? 128u : static_cast<uint32_t>(BN)};
+    const uint32_t box[2] = {rms::BK, pair ? 128u : static_cast<uint32_t>(BN)};
     if (!make_tmap(&tb, g.b, 2, dims, str, box, 2)) return cudaErrorInvalidValue;
   }
   {
@@ -881,21 +934,23 @@ cudaError_t launch_rms_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
     const uint64_t str[1] = {static_cast<uint64_t>(g.n) * 2};
     const uint32_t box[2] = {64, BM};
     if (!make_tmap(&ty, g.c, 2, dims, str, box, 2)) return cudaErrorInvalidValue;
+    if (!make_tmap(&ty4, ln && g.c4 ? g.c4 : g.c, 2, dims, str, box, 2)) return cudaErrorInvalidValue;
   }
-  if (g.m % (2 * BM) == 0) {  // 2-SM path
+  if (pair) {  // 2-SM path
     rms::Params p{g.d1, g.k, 1.f / static_cast<float>(g.k), g.eps, static_cast<int>(g.m / (2 * BM)),
-                  static_cast<int>(g.n / BN), 8};
+                  static_cast<int>(g.n / BN), 8, g.d2, g.colsum, g.c4 != nullptr};
     const size_t smem = sizeof(rms2::Smem) + 1024;
-    cudaError_t e = cudaFuncSetAttribute(rms2::rms_gemm_2sm_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+    auto kern = ln ? rms2::rms_gemm_2sm_kernel<true> : rms2::rms_gemm_2sm_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     dim3 grid(static_cast<unsigned>(2 * (g.n / BN) * (g.m / (2 * BM))));
-    rms2::rms_gemm_2sm_kernel<<<grid, rms2::NT, smem, st>>>(ta, tb, ty, p);
+    kern<<<grid, rms2::NT, smem, st>>>(ta, tb, ty, ty4, p);
     return cudaGetLastError();
   }
+  if (ln) return cudaErrorNotSupported;  // layernorm: 2-SM tiles only (M % 256)
   rms::Params p{g.d1, g.k, 1.f / static_cast<float>(g.k), g.eps, static_cast<int>(g.m / BM),
-                static_cast<int>(g.n / BN), 8};
+                static_cast<int>(g.n / BN), 8, nullptr, nullptr, 0};
   const size_t smem = sizeof(rms::Smem) + 1024;
   cudaError_t e = cudaFuncSetAttribute(rms::rms_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -903,6 +958,14 @@ cudaError_t launch_rms_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
   dim3 grid(static_cast<unsigned>((g.n / BN) * (g.m / BM)));
   rms::rms_gemm_kernel<<<grid, rms::NT, smem, st>>>(ta, tb, ty, p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_rms_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
+  return launch_rms_like(g, st, false);
+}
+
+cudaError_t launch_layernorm_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
+  return launch_rms_like(g, st, true);
 }
 
 cudaError_t launch_quant_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
@@ -953,6 +1016,26 @@ cudaError_t launch_quant_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
 cudaError_t launch_pack_e4m3(const float* w, int64_t k, int64_t n, uint8_t* packed, cudaStream_t st) {
   dim3 grid(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((k + 31) / 32));
   pack_kernel<true><<<grid, dim3(32, 8), 0, st>>>(w, nullptr, k, n, packed);
+  return cudaGetLastError();
+}
+
+namespace {
+// one warp per column n of the packed [N,K] bf16 weight: colsum[n] = sum_k W'[n,k]
+__global__ void colsum_kernel(const __nv_bfloat16* __restrict__ w, int64_t k, int64_t n,
+                              float* __restrict__ out) {
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (col >= n) return;
+  float acc = 0.f;
+  for (int64_t i = threadIdx.x & 31; i < k; i += 32) acc += __bfloat162float(w[col * k + i]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) out[col] = acc;
+}
+}  // namespace
+
+cudaError_t launch_colsum(const void* packed, int64_t k, int64_t n, float* colsum, cudaStream_t st) {
+  colsum_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(packed), k, n, colsum);
   return cudaGetLastError();
 }
 

@@ -40,7 +40,7 @@ struct rf_plan {
   // Host-path staging (rf_run_host), allocated on first use.
   bool staged = false;
   void* dev_in[4] = {nullptr, nullptr, nullptr, nullptr};
-  void* dev_out[3] = {nullptr, nullptr, nullptr};
+  void* dev_out[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaStream_t streams[2] = {nullptr, nullptr};
   std::string describe;
 };
@@ -56,11 +56,16 @@ rf_status fail(rf_status s, const std::string& msg) {
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+bool is_gemm(int pattern) {
+  return pattern == RF_PATTERN_QUANT_GEMM_E4M3 || pattern == RF_PATTERN_RMSNORM_GEMM ||
+         pattern == RF_PATTERN_LAYERNORM_GEMM;
+}
+
 // Input/output byte sizes per pattern, for the host path and shape checks.
-void io_sizes(const rf_plan* p, size_t in[4], size_t out[3]) {
+void io_sizes(const rf_plan* p, size_t in[4], size_t out[4]) {
   const rf_desc& d = p->d;
   for (int i = 0; i < 4; ++i) in[i] = 0;
-  for (int i = 0; i < 3; ++i) out[i] = 0;
+  for (int i = 0; i < 4; ++i) out[i] = 0;
   const size_t es = dtype_size(d.dtype);
   switch (d.pattern) {
     case RF_PATTERN_SAFE_SOFTMAX:
@@ -85,6 +90,11 @@ void io_sizes(const rf_plan* p, size_t in[4], size_t out[3]) {
       out[0] = sizeof(float) * d.rows;
       out[1] = 2 * d.rows * d.free_len;
       break;
+    case RF_PATTERN_LAYERNORM_GEMM:
+      in[0] = 2 * d.rows * d.len;
+      out[0] = out[1] = sizeof(float) * d.rows;
+      out[2] = out[3] = 2 * d.rows * d.free_len;
+      break;
     case RF_PATTERN_MOE_ROUTING:
       in[0] = sizeof(float) * d.rows * d.len;
       out[0] = out[1] = sizeof(float) * d.rows;
@@ -103,6 +113,7 @@ const char* kernel_name(rf::Kernel k) {
     case rf::Kernel::QuantGemmSm100: return "quant_gemm_sm100 (e4m3 tcgen05 kind::f8f6f4)";
     case rf::Kernel::RmsGemmSm100: return "rmsnorm_gemm_sm100 (bf16 tcgen05 kind::f16)";
     case rf::Kernel::MoeRouting: return "moe_routing (SIMT, warp per token, bit-exact top-k)";
+    case rf::Kernel::LayerNormGemmSm100: return "layernorm_gemm_sm100 (bf16 tcgen05 cta_group::2)";
   }
   return "?";
 }
@@ -171,7 +182,15 @@ rf_status gemm_run(const rf_plan* p, const rf_io* io, int64_t m0, int64_t nm, cu
   g.b = io->in[1];
   g.d1 = static_cast<float*>(io->d[0]) + m0;
   const size_t cs = d.pattern == RF_PATTERN_QUANT_GEMM_E4M3 ? 4 : 2;
-  g.c = static_cast<char*>(io->d[1]) + cs * m0 * d.free_len;
+  if (d.pattern == RF_PATTERN_LAYERNORM_GEMM) {
+    g.d2 = static_cast<float*>(io->d[1]) + m0;
+    g.c = static_cast<char*>(io->d[2]) + cs * m0 * d.free_len;
+    g.c4 = io->d[3] ? static_cast<char*>(io->d[3]) + cs * m0 * d.free_len : nullptr;
+    g.colsum = reinterpret_cast<const float*>(static_cast<const char*>(io->in[1]) +
+                                              2 * d.free_len * d.len);
+  } else {
+    g.c = static_cast<char*>(io->d[1]) + cs * m0 * d.free_len;
+  }
   g.domain_flag = p->domain_flag;
   g.m = nm;
   g.n = d.free_len;
@@ -179,7 +198,8 @@ rf_status gemm_run(const rf_plan* p, const rf_io* io, int64_t m0, int64_t nm, cu
   g.fmax = static_cast<float>(d.fmax);
   g.eps = static_cast<float>(d.eps);
   cudaError_t e = d.pattern == RF_PATTERN_QUANT_GEMM_E4M3 ? rf::launch_quant_gemm_sm100(g, st)
-                                                          : rf::launch_rms_gemm_sm100(g, st);
+                  : d.pattern == RF_PATTERN_LAYERNORM_GEMM  ? rf::launch_layernorm_gemm_sm100(g, st)
+                                                            : rf::launch_rms_gemm_sm100(g, st);
   if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
   return RF_OK;
 }
@@ -304,13 +324,17 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
       break;
     case RF_PATTERN_QUANT_GEMM_E4M3:
     case RF_PATTERN_RMSNORM_GEMM:
+    case RF_PATTERN_LAYERNORM_GEMM:
       if (d.dtype != RF_BF16) return bail(RF_ERR_UNSUPPORTED, "GEMM patterns take bf16 activations");
       if (d.segments != 1)
         return bail(RF_ERR_UNSUPPORTED, "GEMM patterns: single-segment (run_incremental) only");
       if (!rf::gemm_sm100_supports(d.pattern, d.rows, d.free_len, d.len))
-        return bail(RF_ERR_UNSUPPORTED, "GEMM shape has no tcgen05 tiling (need M%128, N%256, K%128)");
+        return bail(RF_ERR_UNSUPPORTED,
+                    "GEMM shape has no tcgen05 tiling (quant: M%128, N%512, K%128; rms: M%128, "
+                    "N%256, K%64; layernorm: M%256, N%256, K%64)");
       p->kernel = d.pattern == RF_PATTERN_QUANT_GEMM_E4M3 ? rf::Kernel::QuantGemmSm100
-                                                          : rf::Kernel::RmsGemmSm100;
+                  : d.pattern == RF_PATTERN_LAYERNORM_GEMM ? rf::Kernel::LayerNormGemmSm100
+                                                           : rf::Kernel::RmsGemmSm100;
       p->rows_total = d.rows;
       break;
     case RF_PATTERN_MOE_ROUTING:
@@ -378,10 +402,15 @@ rf_status rf_pack_weight(const rf_plan* p, const void* w, const void* g, void* p
   if (p->d.pattern == RF_PATTERN_QUANT_GEMM_E4M3) {
     e = rf::launch_pack_e4m3(static_cast<const float*>(w), p->d.len, p->d.free_len,
                              static_cast<uint8_t*>(packed), as_stream(stream));
-  } else if (p->d.pattern == RF_PATTERN_RMSNORM_GEMM) {
-    if (!g) return fail(RF_ERR_ARG, "rmsnorm pack needs g");
+  } else if (p->d.pattern == RF_PATTERN_RMSNORM_GEMM || p->d.pattern == RF_PATTERN_LAYERNORM_GEMM) {
+    if (!g) return fail(RF_ERR_ARG, "rmsnorm/layernorm pack needs g");
     e = rf::launch_pack_rms(static_cast<const float*>(w), static_cast<const float*>(g), p->d.len,
                             p->d.free_len, packed, as_stream(stream));
+    if (e == cudaSuccess && p->d.pattern == RF_PATTERN_LAYERNORM_GEMM)
+      e = rf::launch_colsum(packed, p->d.len, p->d.free_len,
+                            reinterpret_cast<float*>(static_cast<char*>(packed) +
+                                                     2 * p->d.free_len * p->d.len),
+                            as_stream(stream));
   } else {
     return fail(RF_ERR_UNSUPPORTED, "pattern has no packed weight");
   }
@@ -389,12 +418,22 @@ rf_status rf_pack_weight(const rf_plan* p, const void* w, const void* g, void* p
   return RF_OK;
 }
 
+size_t rf_packed_bytes(const rf_plan* p) {
+  if (!p) return 0;
+  const size_t nk = static_cast<size_t>(p->d.len) * p->d.free_len;
+  switch (p->d.pattern) {
+    case RF_PATTERN_QUANT_GEMM_E4M3: return nk;
+    case RF_PATTERN_RMSNORM_GEMM: return 2 * nk;
+    case RF_PATTERN_LAYERNORM_GEMM: return 2 * nk + 4 * static_cast<size_t>(p->d.free_len);
+    default: return 0;
+  }
+}
+
 rf_status rf_pack_weight_host(const rf_plan* p, const float* w, const float* g, void** packed) {
   if (!p || !w || !packed) return fail(RF_ERR_ARG, "null plan/w/packed");
   *packed = nullptr;
   const bool quant = p->d.pattern == RF_PATTERN_QUANT_GEMM_E4M3;
-  if (!quant && p->d.pattern != RF_PATTERN_RMSNORM_GEMM)
-    return fail(RF_ERR_UNSUPPORTED, "pattern has no packed weight");
+  if (rf_packed_bytes(p) == 0) return fail(RF_ERR_UNSUPPORTED, "pattern has no packed weight");
   if (!quant && !g) return fail(RF_ERR_ARG, "rmsnorm pack needs g");
   int prev = 0;
   cudaGetDevice(&prev);
@@ -403,7 +442,7 @@ rf_status rf_pack_weight_host(const rf_plan* p, const float* w, const float* g, 
   float *dw = nullptr, *dg = nullptr;
   void* out = nullptr;
   RF_CUDA_TRY(cudaMalloc(&dw, kn * sizeof(float)));
-  RF_CUDA_TRY(cudaMalloc(&out, kn * (quant ? 1 : 2)));
+  RF_CUDA_TRY(cudaMalloc(&out, rf_packed_bytes(p)));
   RF_CUDA_TRY(cudaMemcpy(dw, w, kn * sizeof(float), cudaMemcpyHostToDevice));
   if (g) {
     RF_CUDA_TRY(cudaMalloc(&dg, p->d.len * sizeof(float)));
@@ -426,14 +465,13 @@ void rf_buffer_free(void* dev_ptr) { cudaFree(dev_ptr); }
 
 rf_status rf_run(const rf_plan* p, const rf_io* io, void* stream) {
   if (!p || !io) return fail(RF_ERR_ARG, "null plan/io");
-  size_t in[4], out[3];
+  size_t in[4], out[4];
   io_sizes(p, in, out);
   for (int i = 0; i < 4; ++i)
     if (in[i] && !io->in[i]) return fail(RF_ERR_SHAPE, "missing input " + std::to_string(i));
-  for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < 3; ++i)  // d4 (layernorm) is optional
     if (out[i] && !io->d[i]) return fail(RF_ERR_SHAPE, "missing output d" + std::to_string(i + 1));
-  if ((p->d.pattern == RF_PATTERN_QUANT_GEMM_E4M3 || p->d.pattern == RF_PATTERN_RMSNORM_GEMM) &&
-      !io->in[1])
+  if (is_gemm(p->d.pattern) && !io->in[1])
     return fail(RF_ERR_SHAPE, "missing packed weight in[1]");
   if (units_of(p) == 0 || p->d.rows == 0) return RF_OK;  // empty batch
   return run_range(p, io, 0, units_of(p), as_stream(stream));
@@ -441,30 +479,29 @@ rf_status rf_run(const rf_plan* p, const rf_io* io, void* stream) {
 
 rf_status rf_run_host(rf_plan* p, const rf_host_io* io) {
   if (!p || !io) return fail(RF_ERR_ARG, "null plan/io");
-  size_t in[4], out[3];
+  size_t in[4], out[4];
   io_sizes(p, in, out);
-  const bool gemm =
-      p->d.pattern == RF_PATTERN_QUANT_GEMM_E4M3 || p->d.pattern == RF_PATTERN_RMSNORM_GEMM;
+  const bool gemm = is_gemm(p->d.pattern);
   int prev_dev = 0;
   cudaGetDevice(&prev_dev);
   RF_CUDA_TRY(cudaSetDevice(p->d.device));
   if (!p->staged) {
     for (int i = 0; i < 4; ++i)
       if (in[i]) RF_CUDA_TRY(cudaMalloc(&p->dev_in[i], in[i]));
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < 4; ++i)
       if (out[i]) RF_CUDA_TRY(cudaMalloc(&p->dev_out[i], out[i]));
     for (auto& s : p->streams) RF_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     p->staged = true;
   }
   rf_io dio{};
   for (int i = 0; i < 4; ++i) dio.in[i] = p->dev_in[i];
-  for (int i = 0; i < 3; ++i) dio.d[i] = p->dev_out[i];
+  for (int i = 0; i < 4; ++i) dio.d[i] = io->d[i] ? p->dev_out[i] : nullptr;
   if (gemm) dio.in[1] = io->in[1];  // packed weight: plan-time resident device buffer
   const int64_t units = units_of(p);
   // Chunking: 8 chunks over independent units, alternating two streams, so
   // the H2D of chunk c+1 and the D2H of chunk c-1 overlap chunk c's kernels.
   // GEMM chunks are whole 128-row tiles.
-  const int64_t gran = gemm ? 128 : 1;
+  const int64_t gran = p->d.pattern == RF_PATTERN_LAYERNORM_GEMM ? 256 : gemm ? 128 : 1;
   const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(8, units / gran));
   const int64_t per = ((units + nchunk - 1) / nchunk + gran - 1) / gran * gran;
   for (int64_t c = 0; c < nchunk; ++c) {
@@ -480,7 +517,7 @@ rf_status rf_run_host(rf_plan* p, const rf_host_io* io) {
     }
     rf_status s = run_range(p, &dio, u0, nu, st);
     if (s != RF_OK) return s;
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 4; ++i) {
       if (!out[i] || !io->d[i]) continue;
       const size_t chunk = out[i] / units * nu, off = out[i] / units * u0;
       RF_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(io->d[i]) + off,

@@ -32,6 +32,7 @@ enum class Kernel {
   QuantGemmSm100,     // gemm_sm100.cu (e4m3 kind::f8f6f4, cfg4)
   RmsGemmSm100,       // gemm_sm100.cu (bf16 kind::f16, cfg5)
   MoeRouting,         // moe.cu (softmax stats + top-k, bit-exact indices)
+  LayerNormGemmSm100, // gemm_sm100.cu (bf16, 2-SM; variance cascade + GEMM)
 };
 
 // ---- kernel launchers (stream-ordered; return cudaGetLastError()) ----------
@@ -81,13 +82,17 @@ struct GemmArgs {
   const void* a;       // [M,K] bf16
   const void* b;       // packed [N,K] (e4m3 or bf16)
   float* d1;           // [M]
-  void* c;             // [M,N] (f32 for quant, bf16 for rms)
+  float* d2;           // [M] (layernorm: sum x^2)
+  void* c;             // [M,N] (f32 for quant, bf16 for rms / layernorm d3)
+  void* c4;            // [M,N] bf16 (layernorm d4; may be null)
+  const float* colsum; // [N] (layernorm: column sums of the packed g*w)
   int* domain_flag;    // device int, set to 1 on 0/0 at finalize
   int64_t m, n, k;
   float fmax, eps;
 };
 cudaError_t launch_quant_gemm_sm100(const GemmArgs& g, cudaStream_t st);
 cudaError_t launch_rms_gemm_sm100(const GemmArgs& g, cudaStream_t st);
+cudaError_t launch_layernorm_gemm_sm100(const GemmArgs& g, cudaStream_t st);
 bool gemm_sm100_supports(int pattern, int64_t m, int64_t n, int64_t k);
 
 // Weight packing (plan time).
@@ -95,5 +100,8 @@ cudaError_t launch_pack_e4m3(const float* w, int64_t k, int64_t n, uint8_t* pack
                              cudaStream_t st);
 cudaError_t launch_pack_rms(const float* w, const float* g, int64_t k, int64_t n,
                             void* packed_bf16, cudaStream_t st);
+// column sums of a packed bf16 [N,K] weight -> colsum [N] f32
+cudaError_t launch_colsum(const void* packed_bf16, int64_t k, int64_t n, float* colsum,
+                          cudaStream_t st);
 
 }  // namespace rf

@@ -165,13 +165,19 @@ class Plan:
         k, n = self.desc.len, self.desc.free_len
         if tuple(w.shape) != (k, n) or w.dtype != torch.float32:
             raise ShapeMismatch(f"w must be float32 [{k}, {n}] (reduce-axis major)")
-        if self.desc.pattern == N.RF_PATTERN_QUANT_GEMM_E4M3:
-            out = torch.empty((n, k), dtype=torch.uint8, device=w.device)
-        else:
-            out = torch.empty((n, k), dtype=torch.bfloat16, device=w.device)
-        check(N.lib().rf_pack_weight(self._h, _ptr(w.contiguous()), _ptr(g), _ptr(out),
+        nbytes = int(N.lib().rf_packed_bytes(self._h))
+        if nbytes == 0:
+            raise UnsupportedPattern("pattern has no packed weight")
+        raw = torch.empty(nbytes, dtype=torch.uint8, device=w.device)
+        check(N.lib().rf_pack_weight(self._h, _ptr(w.contiguous()), _ptr(g), _ptr(raw),
                                      _stream_ptr(stream)))
-        return out
+        if self.desc.pattern == N.RF_PATTERN_QUANT_GEMM_E4M3:
+            return raw.view(n, k)
+        if self.desc.pattern == N.RF_PATTERN_RMSNORM_GEMM:
+            return raw.view(torch.bfloat16).view(n, k)
+        # layernorm: bf16 [N, K] (g folded) followed by N f32 column sums; the
+        # returned tensor is the whole buffer (rf_run reads both parts)
+        return raw
 
     def check_domain(self, stream=None) -> None:
         check(N.lib().rf_check_domain(self._h, _stream_ptr(stream)))
@@ -270,6 +276,31 @@ def rmsnorm_gemm(x, w_packed, eps: float = 1e-6, stream=None):
     y = torch.empty((T, Nn), dtype=torch.bfloat16, device=x.device)
     p.run([x.contiguous(), w_packed], [ss, y], stream)
     return ss, y
+
+
+def layernorm_gemm_plan(t: int, k: int, n: int, eps: float = 1e-5, device: int = 0) -> Plan:
+    return plan(Desc(N.RF_PATTERN_LAYERNORM_GEMM, "bf16", rows=t, len=k, free_len=n, eps=eps,
+                     device=device))
+
+
+def layernorm_gemm(x, w_packed, n: int, eps: float = 1e-5, with_d4: bool = True, stream=None):
+    """LayerNorm statistics fused with the following GEMM (the 4-reduction
+    cascade d1 = sum x, d2 = sum x^2, d3 = (x*g) @ W / sigma,
+    d4 = mean * colsum(g*W) / sigma; normalised output = d3 - d4).
+    x: [T,K] bf16; w_packed from Plan.pack_weight (raw bytes). Returns
+    (d1 [T] f32, d2 [T] f32, d3 [T,N] bf16, d4 [T,N] bf16 or None)."""
+    import torch
+
+    T, K = x.shape
+    p = layernorm_gemm_plan(T, K, n, eps, x.device.index or 0)
+    _require(w_packed.numel() * w_packed.element_size() == N.lib().rf_packed_bytes(p._h),
+             "w_packed size does not match the plan")
+    d1 = torch.empty(T, dtype=torch.float32, device=x.device)
+    d2 = torch.empty_like(d1)
+    d3 = torch.empty((T, n), dtype=torch.bfloat16, device=x.device)
+    d4 = torch.empty_like(d3) if with_d4 else None
+    p.run([x.contiguous(), w_packed], [d1, d2, d3, d4], stream)
+    return d1, d2, d3, d4
 
 
 def moe_routing(logits, k: int, stream=None):

@@ -62,6 +62,19 @@ static std::string rms_dsl(long long k, long long n) {
          "\nconst K = " + std::to_string(k) + "\nconst EPS = 1e-6\nreduce 1 op sum\n    x[l] * x[l]\n"
          "reduce 2 op sum free " + std::to_string(n) + "\n    x[l] * g[l] / sqrt(d1 / K + EPS) * w[l, f]\n";
 }
+static std::string ln_dsl(long long k, long long n, bool w_first = true) {
+  const std::string sig = "sqrt(d2 * INVK - d1 * INVK * d1 * INVK + EPS)";
+  const std::string kk = std::to_string(k), nn = std::to_string(n);
+  char invk[64];
+  std::snprintf(invk, sizeof invk, "%.17g", 1.0 / static_cast<double>(k));
+  return "cascade layernorm_gemm\ninput x len " + kk + "\ninput g len " + kk + "\ninput w len " + kk +
+         " free " + nn + "\nconst INVK = " + invk + "\nconst EPS = 1e-5\nreduce 1 op sum\n    x[l]\n" +
+         "reduce 2 op sum\n    x[l] * x[l]\nreduce 3 op sum free " + nn + "\n    " +
+         (w_first ? "x[l] * g[l] * w[l, f] / " + sig : "x[l] * g[l] / " + sig + " * w[l, f]") +
+         "\nreduce 4 op sum free " + nn + "\n    " +
+         (w_first ? "d1 * INVK * g[l] * w[l, f] / " + sig : "d1 * INVK * g[l] / " + sig + " * w[l, f]") +
+         "\n";
+}
 static std::vector<double> random_vec(std::size_t n, std::uint64_t seed, double lo, double hi) {
   std::mt19937_64 rng(seed);
   std::uniform_real_distribution<double> d(lo, hi);
@@ -82,6 +95,18 @@ TEST(dsl_files_parse_and_match_kernels) {
   Program r = plan(rms_dsl(4096, 11008));
   CHECK(r.pattern == RF_PATTERN_RMSNORM_GEMM && r.eps == 1e-6 && r.g == "g");
   CHECK(std::fabs(r.inv_k * 4096 - 1.0) < 1e-15);
+}
+
+TEST(layernorm_gemm_matches) {
+  for (bool wf : {true, false}) {
+    Program p = plan(ln_dsl(4096, 11008, wf));
+    CHECK(p.pattern == RF_PATTERN_LAYERNORM_GEMM && p.eps == 1e-5 && p.g == "g" && p.w == "w");
+    CHECK(p.free_len == 11008 && std::fabs(p.inv_k * 4096 - 1.0) < 1e-15);
+  }
+  // a d4 that does not subtract the mean of the same statistic: not LayerNorm
+  std::string bad = ln_dsl(64, 8);
+  bad.replace(bad.rfind("d1 * INVK * g"), 13, "d2 * INVK * g");
+  CHECK_THROWS_AS(plan(bad), NotFusable);
 }
 
 TEST(moe_routing_matches) {  // proj/data/moe_routing.cascade
@@ -265,10 +290,43 @@ TEST(rmsnorm_gemm_matches_direct_loop) {
   std::printf("  rmsnorm scaled err vs unrounded reference: %.3g (%s)\n", d.max_rel_err, d.worst.c_str());
 }
 
+TEST(layernorm_gemm_matches_direct_loop) {
+  const long long k = 256, n = 48;
+  Program p = plan(ln_dsl(k, n));
+  TensorStore st;
+  st.define("x", k, 0, random_vec(k, 4, -1, 2));
+  st.define("g", k, 0, random_vec(k, 5, -1, 1));
+  st.define("w", k, n, random_vec(k * n, 6, -1, 1));
+  ExecReport r = run_incremental(p, TreeConfig{{k, 1}}, st);
+  const auto &x = st.array("x").data, &g = st.array("g").data, &w = st.array("w").data;
+  double s1 = 0, s2 = 0;
+  for (double v : x) s1 += v, s2 += v * v;
+  const double sig = std::sqrt(s2 / k - (s1 / k) * (s1 / k) + 1e-5);
+  ExecReport want;
+  want.outputs = {{1, {s1}, {}}, {2, {s2}, {}}, {3, std::vector<double>(n, 0.0), {}},
+                  {4, std::vector<double>(n, 0.0), {}}};
+  for (long long l = 0; l < k; ++l)
+    for (long long f = 0; f < n; ++f) {
+      want.outputs[2].v[f] += x[l] * g[l] * w[l * n + f] / sig;
+      want.outputs[3].v[f] += s1 / k * g[l] * w[l * n + f] / sig;
+    }
+  DiffReport d = compare_reports(r, want, 0.1);  // bf16 operands (unrounded reference)
+  CHECK(d.pass);
+  std::printf("  layernorm scaled err vs unrounded reference: %.3g (%s)\n", d.max_rel_err, d.worst.c_str());
+  // matched, but K % 64 has no tiling (zero padding would shift the mean)
+  Program p96 = plan(ln_dsl(96, 8));
+  TensorStore s96;
+  s96.define("x", 96, 0, random_vec(96, 7, -1, 1));
+  s96.define("g", 96, 0, random_vec(96, 8, -1, 1));
+  s96.define("w", 96, 8, random_vec(96 * 8, 9, -1, 1));
+  CHECK_THROWS_AS(run_incremental(p96, TreeConfig{{96, 1}}, s96), NotFusable);
+}
+
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "cpu";
   RUN(dsl_files_parse_and_match_kernels);
   RUN(moe_routing_matches);
+  RUN(layernorm_gemm_matches);
   RUN(unsupported_cascades_are_not_fusable);
   RUN(syntax_errors);
   RUN(compare_reports_flags_corruption_with_a_location);
@@ -281,6 +339,7 @@ int main(int argc, char** argv) {
     RUN(softmax_weights_sum_to_one);
     RUN(rmsnorm_gemm_matches_direct_loop);
     RUN(topk_reduction_ties_lowest_index);
+    RUN(layernorm_gemm_matches_direct_loop);
   }
   std::printf("%d checks, %d failures\n", checks, failures);
   return failures ? 1 : 0;

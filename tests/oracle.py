@@ -40,6 +40,9 @@ def lib():
             "rfo_quant_gemm_e4m3": (None, [D, D, I, I, I, ctypes.c_double, I, D, D, ctypes.c_int]),
             "rfo_rmsnorm_gemm": (None, [D, D, D, I, I, I, ctypes.c_double, D, D, ctypes.c_int]),
             "rfo_rmsnorm_gemm_incremental": (None, [D, D, D, I, I, ctypes.c_double, D, D]),
+            "rfo_layernorm_gemm": (None, [D, D, D, I, I, I, ctypes.c_double, D, D, D, D,
+                                          ctypes.c_int]),
+            "rfo_layernorm_gemm_incremental": (None, [D, D, D, I, I, ctypes.c_double, D, D, D, D]),
             "rfo_moe_routing": (None, [D, I, I, I, D, D, D, ctypes.POINTER(ctypes.c_int64)]),
             "rfo_scaled_max_err": (ctypes.c_double, [D, D, I, ctypes.POINTER(ctypes.c_int64)]),
         }
@@ -152,6 +155,29 @@ def rmsnorm_gemm_incremental(x, g, w, eps=1e-6):
     y = np.empty(Nn)
     lib().rfo_rmsnorm_gemm_incremental(_p(x), _p(g), _p(w), K, Nn, eps, _p(d1), _p(y))
     return d1[0], y
+
+
+def layernorm_gemm(x, g, w, eps=1e-5):
+    """(d1 = sum x, d2 = sum x^2, d3, d4) with LayerNorm(x*g) @ W = d3 - d4."""
+    x, g, w = _f64(x), _f64(g), _f64(w)
+    T, K = x.shape
+    Nn = w.shape[1]
+    d1, d2 = np.empty(T), np.empty(T)
+    d3, d4 = np.empty((T, Nn)), np.empty((T, Nn))
+    lib().rfo_layernorm_gemm(_p(x), _p(g), _p(w), T, K, Nn, eps, _p(d1), _p(d2), _p(d3), _p(d4),
+                             THREADS)
+    return d1, d2, d3, d4
+
+
+def layernorm_gemm_incremental(x, g, w, eps=1e-5):
+    x, g, w = _f64(x), _f64(g), _f64(w)
+    K = x.shape[0]
+    Nn = w.shape[1]
+    d1, d2 = np.empty(1), np.empty(1)
+    d3, d4 = np.empty(Nn), np.empty(Nn)
+    lib().rfo_layernorm_gemm_incremental(_p(x), _p(g), _p(w), K, Nn, eps, _p(d1), _p(d2),
+                                         _p(d3), _p(d4))
+    return d1[0], d2[0], d3, d4
 
 
 def moe_routing(s, k):

@@ -81,6 +81,90 @@ def test_rmsnorm_gemm_unsupported_shape_raises():
         rmsnorm_gemm_plan(100, 64, 256)
 
 
+# --------------------------------------------------------------- layernorm --
+
+
+def _ln_run(x, g, w, eps=1e-5, with_d4=True):
+    import torch
+    from paper_2603_10026_b200 import layernorm_gemm, layernorm_gemm_plan
+
+    T, K = x.shape
+    N = w.shape[1]
+    p = layernorm_gemm_plan(T, K, N, eps)
+    assert "layernorm" in p.info["kernel"]
+    raw = p.pack_weight(torch.tensor(w, dtype=torch.float32).cuda(),
+                        torch.tensor(g, dtype=torch.float32).cuda())
+    wp = raw[: 2 * N * K].view(torch.bfloat16).view(N, K)
+    colsum = raw[2 * N * K:].view(torch.float32)
+    xd = torch.tensor(x).to(torch.bfloat16).cuda()
+    d1, d2, d3, d4 = layernorm_gemm(xd, raw, N, eps, with_d4=with_d4)
+    torch.cuda.synchronize()
+    f = lambda t: None if t is None else t.double().cpu().numpy()  # noqa: E731
+    return f(d1), f(d2), f(d3), f(d4), f(wp), f(colsum)
+
+
+@pytest.mark.parametrize("shape", [(256, 64, 256), (256, 512, 512), (512, 1024, 768),
+                                   (768, 4096, 512)])
+@pytest.mark.parametrize("offset", [0.0, 1.5])
+def test_layernorm_gemm_vs_oracle(shape, offset):
+    T, K, N = shape
+    rng = np.random.default_rng(T + K + N)
+    x = O.round_bf16(rng.uniform(-1, 1, (T, K)) + offset)
+    g = rng.uniform(-1, 1, K)
+    w = rng.uniform(-1, 1, (K, N))
+    d1, d2, d3, d4, wp, colsum = _ln_run(x, g, w)
+    # the packed operand: W' = bf16(g w) and its exact f32 column sums
+    assert np.abs(colsum - wp.sum(axis=1)).max() < 1e-4 * max(1.0, np.abs(colsum).max())
+    r1, r2, r3, r4 = O.layernorm_gemm(x, np.ones(K), wp.T)
+    assert _err(d1, r1) < 1e-5
+    assert _err(d2, r2) < 1e-5
+    assert _err(d3, r3) < TOL
+    assert _err(d4, r4) < TOL
+    # the normalised product d3 - d4, RMS-relative (bf16 outputs cancel)
+    diff, ref = d3 - d4, r3 - r4
+    assert np.sqrt(np.mean((diff - ref) ** 2)) < TOL * np.sqrt(np.mean(ref ** 2))
+
+
+def test_layernorm_gemm_d4_optional():
+    rng = np.random.default_rng(5)
+    T, K, N = 256, 128, 256
+    x = O.round_bf16(rng.uniform(-1, 1, (T, K)))
+    g, w = rng.uniform(-1, 1, K), rng.uniform(-1, 1, (K, N))
+    a1, a2, a3, a4, _, _ = _ln_run(x, g, w, with_d4=True)
+    b1, b2, b3, b4, _, _ = _ln_run(x, g, w, with_d4=False)
+    assert b4 is None
+    assert np.array_equal(a1, b1) and np.array_equal(a2, b2) and np.array_equal(a3, b3)
+
+
+@pytest.mark.parametrize("name", O.golden_names("layernorm_gemm_"))
+def test_layernorm_gemm_against_reference_goldens(name):
+    gd = O.load_golden(name)
+    K, N = gd["in.w"].shape
+    x = np.zeros((256, K))
+    x[0] = gd["in.x"]
+    w = np.zeros((K, 256))
+    w[:, :N] = gd["in.w"]
+    d1, d2, d3, d4, wp, _ = _ln_run(x, gd["in.g"], w)
+    xr = O.round_bf16(x[:1])
+    r1, r2, r3, r4 = O.layernorm_gemm(xr, np.ones(K), wp.T)
+    assert _err(d1[:1], r1) < 1e-5 and _err(d2[:1], r2) < 1e-5
+    assert _err(d3[0, :N], r3[0, :N]) < TOL
+    assert _err(d4[0, :N], r4[0, :N]) < TOL
+    for tag in ["oracle", "incremental", "multi2"]:
+        assert _err(d1[:1], gd[f"{tag}.d1"]) < 1e-2
+        assert _err(d2[:1], gd[f"{tag}.d2"]) < 1e-2
+        assert _err(d3[0, :N], gd[f"{tag}.d3"]) < 0.1
+        assert _err(d4[0, :N], gd[f"{tag}.d4"]) < 0.1
+    assert np.all(d3[1:] == 0) and np.all(d4[1:] == 0)
+
+
+def test_layernorm_gemm_unsupported_shape_raises():
+    from paper_2603_10026_b200 import UnsupportedPattern, layernorm_gemm_plan
+
+    with pytest.raises(UnsupportedPattern):
+        layernorm_gemm_plan(128, 64, 256)  # the LN kernel is the 2-SM M=256 tile
+
+
 # ------------------------------------------------------------------- quant --
 
 def _quant_run(a, w, fmax=448.0):

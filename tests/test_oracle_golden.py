@@ -74,6 +74,28 @@ def test_rmsnorm_oracle_matches_reference_engine(name):
     assert _err(yi, g["incremental.d2"]) < 1e-12
 
 
+@pytest.mark.parametrize("name", O.golden_names("layernorm_gemm_"))
+def test_layernorm_oracle_matches_reference_engine(name):
+    g = O.load_golden(name)
+    x, gg, w = g["in.x"], g["in.g"], g["in.w"]
+    d1, d2, d3, d4 = O.layernorm_gemm(x.reshape(1, -1), gg, w)
+    for tag in ["oracle", "incremental", "multi2", "multi4"]:
+        assert _err(d1, g[f"{tag}.d1"]) < TOL, tag
+        assert _err(d2, g[f"{tag}.d2"]) < TOL, tag
+        assert _err(d3.ravel(), g[f"{tag}.d3"]) < 1e-10, tag
+        assert _err(d4.ravel(), g[f"{tag}.d4"]) < 1e-10, tag
+    i1, i2, i3, i4 = O.layernorm_gemm_incremental(x, gg, w)
+    assert _err(np.array([i1, i2]), np.concatenate([g["incremental.d1"], g["incremental.d2"]])) < TOL
+    assert _err(i3, g["incremental.d3"]) < 1e-12
+    assert _err(i4, g["incremental.d4"]) < 1e-12
+    # the normalised product: d3 - d4 == ((x - mean) / sigma * g) @ W
+    K = x.size
+    mu = x.mean()
+    sig = np.sqrt((x * x).mean() - mu * mu + 1e-5)
+    ref = ((x - mu) / sig * gg) @ w
+    assert np.abs((d3 - d4).ravel() - ref).max() < 1e-9 * max(1.0, np.abs(ref).max())
+
+
 def test_moe_routing_oracle_matches_reference():
     g = O.load_golden("moe_routing_128x8_s100")
     d1, d2, tv, ti = O.moe_routing(g["in.s"].reshape(1, -1), 8)
