@@ -79,7 +79,15 @@ typedef enum rf_pattern {
    * d1 = sum x, d2 = sum x^2, sigma = sqrt(d2/K - (d1/K)^2 + eps),
    * d3[f] = sum x g w[l,f] / sigma, d4[f] = sum (d1/K) g w[l,f] / sigma;
    * LayerNorm(x) . W = d3 - d4                    (DSL cascade) */
-  RF_PATTERN_LAYERNORM_GEMM = 6
+  RF_PATTERN_LAYERNORM_GEMM = 6,
+  /* d1 = sum x, d2 = sum x^2                      (make_variance, workloads.cpp:246-277) */
+  RF_PATTERN_VARIANCE = 7,
+  /* d1 = sum x1^2, d2 = sum x1 x2 / sqrt(max(d1 - c, eps)), c = desc.offset
+   *                                               (make_sum_sum, workloads.cpp:213-242)   */
+  RF_PATTERN_SUM_SUM = 8,
+  /* d1 = sum m, d2[f] = sum m p[l,f], d3[f] = sum m p[l,f]^2, free_len <= 8
+   *                                               (data/moment_of_inertia.cascade)        */
+  RF_PATTERN_MOMENTS = 9
 } rf_pattern;
 
 typedef enum rf_dtype { RF_F32 = 0, RF_BF16 = 1, RF_E4M3 = 2 } rf_dtype;
@@ -97,8 +105,9 @@ typedef struct rf_desc {
   int64_t free_len;  /* lanes of the free axis: head_dim D or N (softmax: 0) */
   int64_t segments;  /* Multi-Segment strategy S (run_multisegment); 1 = single segment */
   double fmax;       /* quant: FMAX (448 for e4m3) */
-  double eps;        /* rmsnorm: epsilon */
+  double eps;        /* rmsnorm / layernorm / sum_sum: epsilon */
   double softmax_scale; /* attention: P = scale * Q K^T (reference stores Q pre-scaled: 1.0) */
+  double offset;        /* sum_sum: c in sqrt(max(d1 - c, eps)) */
   int32_t tile_rows;    /* 0 = kernel default (reference pick_tile: 128) */
   int32_t tile_stream;  /* 0 = kernel default */
   int32_t device;       /* CUDA ordinal the plan is bound to */
@@ -119,7 +128,11 @@ typedef struct rf_desc {
  *                  [T] f32, d3 = [T,N] bf16, d4 = [T,N] bf16 (optional: may be null)
  *   MOE_ROUTING    in[0] = logits [rows, experts] f32 (len = experts, free_len = K' <= 8);
  *                  d1, d2 [rows] f32; d3 = [rows, K'] records {f32 value, i32 index}
- *                  (1-based expert index like OutputVal.topk; 0 = empty slot)          */
+ *                  (1-based expert index like OutputVal.topk; 0 = empty slot)
+ *   VARIANCE       in[0] = x [rows, len] f32; d1, d2 [rows] f32
+ *   SUM_SUM        in[0] = x1, in[1] = x2 [rows, len] f32; d1, d2 [rows] f32
+ *   MOMENTS        in[0] = mass [rows, len] f32, in[1] = pos [rows, len, free_len] f32;
+ *                  d1 [rows], d2, d3 [rows, free_len] f32                             */
 typedef struct rf_io {
   const void* in[4];
   void* d[4];

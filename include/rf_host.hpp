@@ -412,7 +412,7 @@ struct Program {
   std::string x, v, g;  // bound input names (softmax x | attention P,V | quant a,w | rms x,g,w)
   std::string w;
   long long L0 = 0, free_len = 0;
-  double fmax = 448.0, eps = 0.0, inv_k = 0.0;
+  double fmax = 448.0, eps = 0.0, inv_k = 0.0, offset = 0.0;
 };
 
 namespace detail {
@@ -575,8 +575,42 @@ inline Program plan(const CascadeSpec& spec) {
       return p;
     }
   }
+  if (R.size() == 2 && R[0].op == "sum" && R[1].op == "sum" && R[0].free_len == 1 &&
+      R[1].free_len == 1) {
+    Binding b;  // make_variance (workloads.cpp:246-277)
+    if (unify(X, R[0].body, b) && unify(bin("*", X, X), R[1].body, b)) {
+      p.pattern = RF_PATTERN_VARIANCE;
+      p.x = b.in["?X"];
+      return p;
+    }
+    Binding b2;  // make_sum_sum (workloads.cpp:213-242): x1 x2 / sqrt(max(d1 - c, eps))
+    const Expr Y = input("?Y");
+    const Expr h = un("sqrt", bin("max", bin("-", dep(1), cvar("c")), cvar("eps")));
+    if (unify(bin("*", X, X), R[0].body, b2) && unify(bin("/", bin("*", X, Y), h), R[1].body, b2)) {
+      p.pattern = RF_PATTERN_SUM_SUM;
+      p.x = b2.in["?X"];
+      p.v = b2.in["?Y"];
+      p.offset = b2.c["c"];
+      p.eps = b2.c["eps"];
+      if (!(p.eps > 0.0)) return none("sum_sum: the H guard max(d1 - c, eps) needs eps > 0");
+      return p;
+    }
+  }
+  if (R.size() == 3 && R[0].op == "sum" && R[1].op == "sum" && R[2].op == "sum" &&
+      R[0].free_len == 1 && R[1].free_len >= 1 && R[1].free_len <= 8 &&
+      R[2].free_len == R[1].free_len) {
+    Binding b;  // moment_of_inertia (workloads.cpp:280-331)
+    if (unify(X, R[0].body, b) && unify(bin("*", X, Vf), R[1].body, b) &&
+        unify(bin("*", bin("*", X, Vf), Vf), R[2].body, b)) {
+      p.pattern = RF_PATTERN_MOMENTS;
+      p.x = b.in["?X"];
+      p.v = b.in["?V"];
+      p.free_len = R[1].free_len;
+      return p;
+    }
+  }
   return none("not one of safe_softmax / attention / moe_routing / quant_gemm / rmsnorm_gemm / "
-              "layernorm_gemm");
+              "layernorm_gemm / variance / sum_sum / moment_of_inertia");
 }
 
 inline Program plan(const std::string& dsl) { return plan(parse_cascade(dsl)); }
@@ -835,7 +869,8 @@ inline ExecReport execute(const Program& prog, const TreeConfig& cfg, long long 
     case RF_PATTERN_QUANT_GEMM_E4M3:
     case RF_PATTERN_RMSNORM_GEMM: {
       const bool quant = prog.pattern == RF_PATTERN_QUANT_GEMM_E4M3;
-      if (segments != 1) throw NotFusable("GEMM patterns: multi-segment not kernelised");
+      // segments: S | L0 was checked above; the kernel's K loop is already a
+      // tile-segmented Eq.16 fold, so S changes nothing but the divisibility.
       // pad to the kernel tiles: M to 128 rows (copies of the row: never an
       // all-zero padding row), K with zeros (neutral for max|a| and sum x^2,
       // zero contributions), N with zero weight columns.
@@ -883,7 +918,8 @@ inline ExecReport execute(const Program& prog, const TreeConfig& cfg, long long 
       break;
     }
     case RF_PATTERN_LAYERNORM_GEMM: {
-      if (segments != 1) throw NotFusable("GEMM patterns: multi-segment not kernelised");
+      // segments: S | L0 was checked above; the kernel's K loop is already a
+      // tile-segmented Eq.16 fold, so S changes nothing but the divisibility.
       // pad: M to one 256-row pair tile (copies of the row), K with zeros —
       // which would shift the mean, so K must already be a multiple of 64
       // (padding changes d1/K and d2/K) — and N with zero weight columns.
@@ -928,6 +964,39 @@ inline ExecReport execute(const Program& prog, const TreeConfig& cfg, long long 
       out(2, {d2[0]});
       out(3, y3);
       out(4, y4);
+      break;
+    }
+    case RF_PATTERN_VARIANCE:
+    case RF_PATTERN_SUM_SUM:
+    case RF_PATTERN_MOMENTS: {
+      const bool mom = prog.pattern == RF_PATTERN_MOMENTS;
+      const long long F = mom ? prog.free_len : 1;
+      rf_desc d = base_desc(prog.pattern, RF_F32);
+      d.rows = 1;
+      d.len = L0;
+      d.free_len = mom ? F : 0;
+      d.segments = segments;
+      d.eps = prog.eps;
+      d.offset = prog.offset;
+      PlanHandle h(d);
+      const auto& x = st.array(prog.x).data;
+      std::vector<float> xf(x.begin(), x.end()), yf;
+      if (prog.pattern != RF_PATTERN_VARIANCE) {
+        const auto& y = st.array(prog.v).data;
+        yf.assign(y.begin(), y.end());
+      }
+      float o1 = 0;
+      std::vector<float> o2(F), o3(F);
+      rf_host_io io{};
+      io.in[0] = xf.data();
+      io.in[1] = yf.empty() ? nullptr : yf.data();
+      io.d[0] = &o1;
+      io.d[1] = o2.data();
+      io.d[2] = mom ? o3.data() : nullptr;
+      check(rf_run_host(h.p, &io));
+      out(1, {o1});
+      out(2, std::vector<double>(o2.begin(), o2.end()));
+      if (mom) out(3, std::vector<double>(o3.begin(), o3.end()));
       break;
     }
     default: throw NotFusable("unknown pattern");

@@ -46,6 +46,27 @@ ExecReport run(const FusedProgram& prog, const TreeConfig& cfg, long long segmen
 
 }  // namespace
 
+CudaPattern cuda_pattern(const FusedProgram& prog) {
+  rfcuda::Program p;
+  try {
+    p = rfcuda::plan(serialize(prog.spec));
+  } catch (const rfcuda::NotFusable& e) {
+    throw NotFusable(0, e.what());
+  }
+  switch (p.pattern) {
+    case RF_PATTERN_SAFE_SOFTMAX: return {"safe_softmax", true};
+    case RF_PATTERN_ATTENTION: return {"attention", true};
+    case RF_PATTERN_MOE_ROUTING: return {"moe_routing", true};
+    case RF_PATTERN_QUANT_GEMM_E4M3: return {"quant_gemm_e4m3", false};
+    case RF_PATTERN_RMSNORM_GEMM: return {"rmsnorm_gemm", false};
+    case RF_PATTERN_LAYERNORM_GEMM: return {"layernorm_gemm", false};
+    case RF_PATTERN_VARIANCE: return {"variance", true};
+    case RF_PATTERN_SUM_SUM: return {"sum_sum", true};
+    case RF_PATTERN_MOMENTS: return {"moment_of_inertia", true};
+  }
+  throw NotFusable(0, "unknown librf_cuda pattern");
+}
+
 ExecReport run_cuda(const FusedProgram& prog, const TreeConfig& cfg, TensorStore& store) {
   return run(prog, cfg, 1, store);
 }

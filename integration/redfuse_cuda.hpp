@@ -4,6 +4,8 @@
 // the C++ host layer include/rf_host.hpp. See INTEGRATION.md.
 #pragma once
 
+#include <string>
+
 #include "redfuse/acrf.hpp"
 #include "redfuse/simulator.hpp"
 
@@ -15,5 +17,15 @@ namespace redfuse {
 ExecReport run_cuda(const FusedProgram& prog, const TreeConfig& cfg, TensorStore& store);
 ExecReport run_cuda_multisegment(const FusedProgram& prog, const TreeConfig& cfg,
                                  long long num_segments, TensorStore& store);
+
+// The librf_cuda pattern a cascade maps onto ("attention", "safe_softmax",
+// "moe_routing", "quant_gemm_e4m3", "rmsnorm_gemm", "layernorm_gemm"), and
+// whether its operands are fp32 (else bf16/e4m3). Throws NotFusable when no
+// kernel implements the cascade.
+struct CudaPattern {
+  std::string name;
+  bool fp32 = true;
+};
+CudaPattern cuda_pattern(const FusedProgram& prog);
 
 }  // namespace redfuse

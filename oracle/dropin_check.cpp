@@ -114,22 +114,27 @@ int main() {
                                     sig + "\n"),
                    -0.02, {}, 2);
   }
-  // no kernel for these: NotFusable from the binding (no CPU fallback)
   // MoE routing: top-k indices must match exactly (compare_reports' index check)
   check_workload("moe_routing_128x8", make_moe_routing(128, 8), 1e-5, {2, 4}, 3);
   check_workload("moe_routing_64x6", make_moe_routing(64, 6), 1e-5, {2}, 2);
-  for (const char* nm : {"variance", "sum_sum"}) {
-    Workload w = builtin(nm);
-    FusedProgram prog = derive_fused(w.spec);
-    TensorStore st = w.generate(1);
+  // the remaining builtins: row-statistics kernels (fp32 path)
+  check_workload("variance_8192", builtin("variance"), 1e-5, {2, 8}, 3);
+  check_workload("sum_sum_1024", builtin("sum_sum"), 1e-5, {2, 8}, 3);
+  check_workload("moment_of_inertia_1024", builtin("moment_of_inertia"), 1e-5, {2, 8}, 3);
+  // a cascade with no kernel: NotFusable from the binding (no CPU fallback)
+  {
+    Workload w = dsl_workload("prod_chain", "cascade prod_chain\ninput x len 64\n"
+                                            "reduce 1 op prod\n    x[l]\nreduce 2 op sum\n    x[l] / d1\n");
     bool threw = false;
     try {
-      run_cuda(prog, TreeConfig{{w.spec.axis_len(), 1}}, st);
+      FusedProgram prog = derive_fused(w.spec);
+      TensorStore st = w.generate(1);
+      run_cuda(prog, TreeConfig{{64, 1}}, st);
     } catch (const NotFusable&) {
       threw = true;
     }
     if (!threw) ++failures;
-    std::printf("{\"case\": \"%s\", \"mode\": \"no-kernel\", \"not_fusable\": %s}\n", nm,
+    std::printf("{\"case\": \"prod_chain\", \"mode\": \"no-kernel\", \"not_fusable\": %s}\n",
                 threw ? "true" : "false");
   }
   std::printf("{\"failures\": %d}\n", failures);

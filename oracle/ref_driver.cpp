@@ -207,6 +207,9 @@ int cmd_golden(const std::string& dir) {
                     make_quant_gemm(64, 32), seed, {2, 4, 8});
   golden_workload(dir, "variance_8192_s100", make_variance(8192), 100, {2, 8});
   golden_workload(dir, "sum_sum_1024_s100", make_sum_sum(1024), 100, {2, 8});
+  golden_workload(dir, "sum_sum_1024_s101", make_sum_sum(1024), 101, {2, 8});
+  golden_workload(dir, "variance_8192_s101", make_variance(8192), 101, {2, 8});
+  golden_workload(dir, "moment_of_inertia_1024_s100", builtin("moment_of_inertia"), 100, {2, 8});
   golden_workload(dir, "moe_routing_128x8_s100", make_moe_routing(128, 8), 100, {2, 4});
 
   // RMSNorm / LayerNorm -> GEMM through the reference engine on the DSL spec

@@ -428,6 +428,52 @@ void rfo_layernorm_gemm_incremental(const double* x, const double* g, const doub
   *d2 = s2;
 }
 
+/* ------------------------------------------------------ row statistics --- */
+
+/* make_variance's oracle (workloads.cpp:246-277), per row */
+void rfo_variance(const double* x, int64_t rows, int64_t n, double* d1, double* d2) {
+  for (int64_t r = 0; r < rows; ++r) {
+    double s = 0, q = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      s += x[r * n + i];
+      q += x[r * n + i] * x[r * n + i];
+    }
+    d1[r] = s;
+    d2[r] = q;
+  }
+}
+
+/* make_sum_sum's oracle (workloads.cpp:213-242): d2 = sum x1 x2 / sqrt(max(d1 - c, eps)) */
+void rfo_sum_sum(const double* x1, const double* x2, int64_t rows, int64_t n, double c,
+                 double eps, double* d1, double* d2) {
+  for (int64_t r = 0; r < rows; ++r) {
+    double m = 0, s = 0;
+    for (int64_t i = 0; i < n; ++i) m += x1[r * n + i] * x1[r * n + i];
+    const double den = sqrt(fmax(m - c, eps));
+    for (int64_t i = 0; i < n; ++i) s += x1[r * n + i] * x2[r * n + i] / den;
+    d1[r] = m;
+    d2[r] = s;
+  }
+}
+
+/* moment_of_inertia's oracle (workloads.cpp:280-331), F position lanes */
+void rfo_moments(const double* mass, const double* pos, int64_t rows, int64_t n, int64_t F,
+                 double* d1, double* d2, double* d3) {
+  for (int64_t r = 0; r < rows; ++r) {
+    const double* m = mass + r * n;
+    const double* p = pos + r * n * F;
+    double t = 0;
+    for (int64_t l = 0; l < n; ++l) t += m[l];
+    d1[r] = t;
+    for (int64_t f = 0; f < F; ++f) d2[r * F + f] = d3[r * F + f] = 0.0;
+    for (int64_t l = 0; l < n; ++l)
+      for (int64_t f = 0; f < F; ++f) {
+        d2[r * F + f] += m[l] * p[l * F + f];
+        d3[r * F + f] += m[l] * p[l * F + f] * p[l * F + f];
+      }
+  }
+}
+
 /* --------------------------------------------------------- moe routing --- */
 
 void rfo_moe_routing(const double* s, int64_t rows, int64_t experts, int64_t k,

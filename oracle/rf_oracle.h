@@ -119,6 +119,13 @@ void rfo_layernorm_gemm_incremental(const double* x, const double* g, const doub
                                     int64_t K, int64_t N, double eps, double* d1, double* d2,
                                     double* d3, double* d4);
 
+/* ---- row statistics: the reference's remaining builtins ------------------- */
+void rfo_variance(const double* x, int64_t rows, int64_t n, double* d1, double* d2);
+void rfo_sum_sum(const double* x1, const double* x2, int64_t rows, int64_t n, double c,
+                 double eps, double* d1, double* d2);
+void rfo_moments(const double* mass, const double* pos, int64_t rows, int64_t n, int64_t F,
+                 double* d1, double* d2, double* d3);
+
 /* ---- MoE routing: softmax stats + top-k (workloads.cpp:124-169) -----------
  * Descending value, ties to the lowest index (test_workloads.cpp:210-224).
  * idx is 1-based like the reference's OutputVal.topk.                       */

@@ -18,12 +18,15 @@ from .executors import (  # noqa: F401
     layernorm_gemm,
     layernorm_gemm_plan,
     moe_routing,
+    moments,
     plan,
     quant_gemm,
     quant_gemm_plan,
     rmsnorm_gemm,
     rmsnorm_gemm_plan,
     safe_softmax,
+    sum_sum,
+    variance,
 )
 
 __all__ = [
@@ -33,6 +36,9 @@ __all__ = [
     "rmsnorm_gemm",
     "layernorm_gemm",
     "moe_routing",
+    "variance",
+    "sum_sum",
+    "moments",
     "Plan",
     "Desc",
     "plan",

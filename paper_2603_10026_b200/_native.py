@@ -30,6 +30,9 @@ RF_PATTERN_QUANT_GEMM_E4M3 = 3
 RF_PATTERN_RMSNORM_GEMM = 4
 RF_PATTERN_MOE_ROUTING = 5
 RF_PATTERN_LAYERNORM_GEMM = 6
+RF_PATTERN_VARIANCE = 7
+RF_PATTERN_SUM_SUM = 8
+RF_PATTERN_MOMENTS = 9
 
 ABI_VERSION = 2
 
@@ -52,6 +55,7 @@ class rf_desc(ctypes.Structure):
         ("fmax", ctypes.c_double),
         ("eps", ctypes.c_double),
         ("softmax_scale", ctypes.c_double),
+        ("offset", ctypes.c_double),
         ("tile_rows", ctypes.c_int32),
         ("tile_stream", ctypes.c_int32),
         ("device", ctypes.c_int32),

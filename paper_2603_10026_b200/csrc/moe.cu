@@ -16,7 +16,6 @@
 namespace rf {
 namespace {
 
-constexpr int MAXK = 8;
 
 struct Cand {
   float v;

@@ -100,6 +100,20 @@ void io_sizes(const rf_plan* p, size_t in[4], size_t out[4]) {
       out[0] = out[1] = sizeof(float) * d.rows;
       out[2] = 8 * d.rows * d.free_len;
       break;
+    case RF_PATTERN_VARIANCE:
+      in[0] = sizeof(float) * d.rows * d.len;
+      out[0] = out[1] = sizeof(float) * d.rows;
+      break;
+    case RF_PATTERN_SUM_SUM:
+      in[0] = in[1] = sizeof(float) * d.rows * d.len;
+      out[0] = out[1] = sizeof(float) * d.rows;
+      break;
+    case RF_PATTERN_MOMENTS:
+      in[0] = sizeof(float) * d.rows * d.len;
+      in[1] = sizeof(float) * d.rows * d.len * d.free_len;
+      out[0] = sizeof(float) * d.rows;
+      out[1] = out[2] = sizeof(float) * d.rows * d.free_len;
+      break;
   }
 }
 
@@ -114,6 +128,7 @@ const char* kernel_name(rf::Kernel k) {
     case rf::Kernel::RmsGemmSm100: return "rmsnorm_gemm_sm100 (bf16 tcgen05 kind::f16)";
     case rf::Kernel::MoeRouting: return "moe_routing (SIMT, warp per token, bit-exact top-k)";
     case rf::Kernel::LayerNormGemmSm100: return "layernorm_gemm_sm100 (bf16 tcgen05 cta_group::2)";
+    case rf::Kernel::RowStats: return "rowstats (SIMT HBM streaming, fp64 accumulation)";
   }
   return "?";
 }
@@ -222,6 +237,28 @@ rf_status run_range(const rf_plan* p, const rf_io* io, int64_t u0, int64_t nu, c
       if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("moe launch: ") + cudaGetErrorString(e));
       return RF_OK;
     }
+    case RF_PATTERN_VARIANCE:
+    case RF_PATTERN_SUM_SUM:
+    case RF_PATTERN_MOMENTS: {
+      const rf_desc& d = p->d;
+      const int64_t fl = d.pattern == RF_PATTERN_MOMENTS ? d.free_len : 0;
+      rf::RowStatsArgs r{};
+      r.pattern = d.pattern;
+      r.a = static_cast<const float*>(io->in[0]) + u0 * d.len;
+      r.b = d.pattern == RF_PATTERN_VARIANCE ? nullptr
+                                             : static_cast<const float*>(io->in[1]) + u0 * d.len * std::max<int64_t>(fl, 1);
+      r.rows = nu;
+      r.len = d.len;
+      r.free_len = fl;
+      r.d1 = static_cast<float*>(io->d[0]) + u0;
+      r.d2 = static_cast<float*>(io->d[1]) + u0 * std::max<int64_t>(fl, 1);
+      r.d3 = fl ? static_cast<float*>(io->d[2]) + u0 * fl : nullptr;
+      r.c = d.offset;
+      r.eps = d.eps;
+      cudaError_t e = rf::launch_rowstats(r, st);
+      if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("rowstats launch: ") + cudaGetErrorString(e));
+      return RF_OK;
+    }
     default: return gemm_run(p, io, u0, nu, st);
   }
 }
@@ -326,8 +363,8 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
     case RF_PATTERN_RMSNORM_GEMM:
     case RF_PATTERN_LAYERNORM_GEMM:
       if (d.dtype != RF_BF16) return bail(RF_ERR_UNSUPPORTED, "GEMM patterns take bf16 activations");
-      if (d.segments != 1)
-        return bail(RF_ERR_UNSUPPORTED, "GEMM patterns: single-segment (run_incremental) only");
+      // segments > 1 (run_multisegment): S | K was checked above; the K-tile loop
+      // is itself a segmented Eq.16 fold, so the kernel is the same.
       if (!rf::gemm_sm100_supports(d.pattern, d.rows, d.free_len, d.len))
         return bail(RF_ERR_UNSUPPORTED,
                     "GEMM shape has no tcgen05 tiling (quant: M%128, N%512, K%128; rms: M%128, "
@@ -342,6 +379,17 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
       if (d.free_len < 1 || d.free_len > 8)
         return bail(RF_ERR_UNSUPPORTED, "moe_routing: top-k size must be 1..8");
       p->kernel = rf::Kernel::MoeRouting;
+      p->rows_total = d.rows;
+      break;
+    case RF_PATTERN_VARIANCE:
+    case RF_PATTERN_SUM_SUM:
+    case RF_PATTERN_MOMENTS:
+      if (d.dtype != RF_F32) return bail(RF_ERR_UNSUPPORTED, "row statistics: f32 inputs");
+      if (d.pattern == RF_PATTERN_MOMENTS && (d.free_len < 1 || d.free_len > 8))
+        return bail(RF_ERR_UNSUPPORTED, "moments: free_len must be 1..8");
+      if (d.pattern == RF_PATTERN_SUM_SUM && !(d.eps > 0.0))
+        return bail(RF_ERR_ARG, "sum_sum: eps must be > 0 (max(d1 - c, eps) is the H guard)");
+      p->kernel = rf::Kernel::RowStats;
       p->rows_total = d.rows;
       break;
     default:

@@ -33,7 +33,21 @@ enum class Kernel {
   RmsGemmSm100,       // gemm_sm100.cu (bf16 kind::f16, cfg5)
   MoeRouting,         // moe.cu (softmax stats + top-k, bit-exact indices)
   LayerNormGemmSm100, // gemm_sm100.cu (bf16, 2-SM; variance cascade + GEMM)
+  RowStats,           // rowstats.cu (variance / sum_sum / moments: HBM streaming)
 };
+
+// Row-statistics cascades (rowstats.cu): a = x | x1 | mass, b = - | x2 | pos.
+struct RowStatsArgs {
+  int pattern;  // RF_PATTERN_VARIANCE / SUM_SUM / MOMENTS
+  const float* a;
+  const float* b;
+  int64_t rows, len, free_len;
+  float* d1;
+  float* d2;
+  float* d3;
+  double c, eps;  // sum_sum: sqrt(max(d1 - c, eps))
+};
+cudaError_t launch_rowstats(const RowStatsArgs& r, cudaStream_t st);
 
 // ---- kernel launchers (stream-ordered; return cudaGetLastError()) ----------
 

@@ -91,6 +91,7 @@ class Desc:
     fmax: float = 448.0
     eps: float = 1e-6
     softmax_scale: float = 1.0
+    offset: float = 0.0
     device: int = 0
 
     def to_c(self) -> N.rf_desc:
@@ -100,6 +101,7 @@ class Desc:
         d.batch, d.heads, d.rows = self.batch, self.heads, self.rows
         d.len, d.free_len, d.segments = self.len, self.free_len, self.segments
         d.fmax, d.eps, d.softmax_scale = self.fmax, self.eps, self.softmax_scale
+        d.offset = self.offset
         d.tile_rows = d.tile_stream = 0
         d.device = self.device
         return d
@@ -319,3 +321,57 @@ def moe_routing(logits, k: int, stream=None):
     rec = torch.empty(rows, k, 2, dtype=torch.int32, device=logits.device)
     p.run([logits.contiguous()], [d1, d2, rec], stream)
     return d1, d2, rec[..., 0].view(torch.float32), rec[..., 1]
+
+
+def _rows_f32(name, *ts):
+    import torch
+
+    for t in ts:
+        _require(t.dtype == torch.float32 and t.is_cuda, f"{name}: float32 cuda tensors")
+    return [t.contiguous() for t in ts]
+
+
+def variance(x, segments: int = 1, stream=None):
+    """make_variance per row: d1 = sum x, d2 = sum x^2. x: [rows, n] float32."""
+    import torch
+
+    _require(x.dim() == 2, "x must be [rows, n]")
+    (x,) = _rows_f32("variance", x)
+    p = plan(Desc(N.RF_PATTERN_VARIANCE, "f32", rows=x.shape[0], len=x.shape[1],
+                  segments=segments, device=x.device.index or 0))
+    d1 = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
+    d2 = torch.empty_like(d1)
+    p.run([x], [d1, d2], stream)
+    return d1, d2
+
+
+def sum_sum(x1, x2, offset: float = 10.0, eps: float = 1e-12, segments: int = 1, stream=None):
+    """make_sum_sum per row: d1 = sum x1^2, d2 = sum x1 x2 / sqrt(max(d1 - offset, eps))."""
+    import torch
+
+    _require(x1.dim() == 2 and x1.shape == x2.shape, "x1, x2 must be [rows, n]")
+    x1, x2 = _rows_f32("sum_sum", x1, x2)
+    p = plan(Desc(N.RF_PATTERN_SUM_SUM, "f32", rows=x1.shape[0], len=x1.shape[1], eps=eps,
+                  offset=offset, segments=segments, device=x1.device.index or 0))
+    d1 = torch.empty(x1.shape[0], dtype=torch.float32, device=x1.device)
+    d2 = torch.empty_like(d1)
+    p.run([x1, x2], [d1, d2], stream)
+    return d1, d2
+
+
+def moments(mass, pos, segments: int = 1, stream=None):
+    """moment_of_inertia per row: d1 = sum m, d2[f] = sum m p_f, d3[f] = sum m p_f^2.
+    mass: [rows, n], pos: [rows, n, F] (F <= 8) float32."""
+    import torch
+
+    _require(mass.dim() == 2 and pos.dim() == 3 and pos.shape[:2] == mass.shape,
+             "mass [rows, n], pos [rows, n, F]")
+    mass, pos = _rows_f32("moments", mass, pos)
+    rows, n, F = pos.shape
+    p = plan(Desc(N.RF_PATTERN_MOMENTS, "f32", rows=rows, len=n, free_len=F, segments=segments,
+                  device=mass.device.index or 0))
+    d1 = torch.empty(rows, dtype=torch.float32, device=mass.device)
+    d2 = torch.empty(rows, F, dtype=torch.float32, device=mass.device)
+    d3 = torch.empty_like(d2)
+    p.run([mass, pos], [d1, d2, d3], stream)
+    return d1, d2, d3

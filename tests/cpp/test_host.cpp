@@ -115,11 +115,29 @@ TEST(moe_routing_matches) {  // proj/data/moe_routing.cascade
   CHECK(p.pattern == RF_PATTERN_MOE_ROUTING && p.free_len == 8 && p.x == "s");
 }
 
+TEST(row_statistics_builtins_match) {  // proj/data/{variance,sum_sum,moment_of_inertia}.cascade
+  Program v = plan("cascade variance\ninput x len 8192\nreduce 1 op sum\n    x[l]\n"
+                   "reduce 2 op sum\n    x[l] * x[l]\n");
+  CHECK(v.pattern == RF_PATTERN_VARIANCE && v.x == "x");
+  Program s = plan("cascade sum_sum\ninput x1 len 1024\ninput x2 len 1024\nconst EPS = 1e-12\n"
+                   "reduce 1 op sum\n    x1[l] * x1[l]\nreduce 2 op sum\n"
+                   "    x1[l] * x2[l] / sqrt(max(d1 - 10, EPS))\n");
+  CHECK(s.pattern == RF_PATTERN_SUM_SUM && s.x == "x1" && s.v == "x2" && s.offset == 10.0 &&
+        s.eps == 1e-12);
+  Program m = plan("cascade moment_of_inertia\ninput mass len 1024\ninput pos len 1024 free 3\n"
+                   "reduce 1 op sum\n    mass[l]\nreduce 2 op sum free 3\n    mass[l] * pos[l, f]\n"
+                   "reduce 3 op sum free 3\n    mass[l] * pos[l, f] * pos[l, f]\n");
+  CHECK(m.pattern == RF_PATTERN_MOMENTS && m.x == "mass" && m.v == "pos" && m.free_len == 3);
+}
+
 TEST(unsupported_cascades_are_not_fusable) {
-  // variance / moe_routing / moment_of_inertia have no kernel: NotFusable, no CPU fallback
-  CHECK_THROWS_AS(plan("cascade variance\ninput x len 8\nreduce 1 op sum\n    x[l]\n"
-                       "reduce 2 op sum\n    x[l] * x[l]\n"),
+  // cascades without a kernel: NotFusable, no CPU fallback
+  CHECK_THROWS_AS(plan("cascade prod_chain\ninput x len 64\nreduce 1 op prod\n    x[l]\n"
+                       "reduce 2 op sum\n    x[l] / d1\n"),
                   NotFusable);
+  CHECK_THROWS_AS(plan("cascade v\ninput x len 8\ninput y len 8\nreduce 1 op sum\n    x[l]\n"
+                       "reduce 2 op sum\n    x[l] * y[l]\n"),
+                  NotFusable);  // not the variance shape
   CHECK_THROWS_AS(plan("cascade moe\ninput s len 8\nreduce 1 op max\n    s[l]\nreduce 2 op sum\n"
                        "    exp(s[l] - d1)\nreduce 3 op topk 9\n    s[l]\n"),
                   NotFusable);  // top-k > 8: no kernel
@@ -327,6 +345,7 @@ int main(int argc, char** argv) {
   RUN(dsl_files_parse_and_match_kernels);
   RUN(moe_routing_matches);
   RUN(layernorm_gemm_matches);
+  RUN(row_statistics_builtins_match);
   RUN(unsupported_cascades_are_not_fusable);
   RUN(syntax_errors);
   RUN(compare_reports_flags_corruption_with_a_location);

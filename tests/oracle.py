@@ -42,6 +42,9 @@ def lib():
             "rfo_rmsnorm_gemm_incremental": (None, [D, D, D, I, I, ctypes.c_double, D, D]),
             "rfo_layernorm_gemm": (None, [D, D, D, I, I, I, ctypes.c_double, D, D, D, D,
                                           ctypes.c_int]),
+            "rfo_variance": (None, [D, I, I, D, D]),
+            "rfo_sum_sum": (None, [D, D, I, I, ctypes.c_double, ctypes.c_double, D, D]),
+            "rfo_moments": (None, [D, D, I, I, I, D, D, D]),
             "rfo_layernorm_gemm_incremental": (None, [D, D, D, I, I, ctypes.c_double, D, D, D, D]),
             "rfo_moe_routing": (None, [D, I, I, I, D, D, D, ctypes.POINTER(ctypes.c_int64)]),
             "rfo_scaled_max_err": (ctypes.c_double, [D, D, I, ctypes.POINTER(ctypes.c_int64)]),
@@ -178,6 +181,30 @@ def layernorm_gemm_incremental(x, g, w, eps=1e-5):
     lib().rfo_layernorm_gemm_incremental(_p(x), _p(g), _p(w), K, Nn, eps, _p(d1), _p(d2),
                                          _p(d3), _p(d4))
     return d1[0], d2[0], d3, d4
+
+
+def variance(x):
+    x = _f64(x)
+    rows, n = x.shape
+    d1, d2 = np.empty(rows), np.empty(rows)
+    lib().rfo_variance(_p(x), rows, n, _p(d1), _p(d2))
+    return d1, d2
+
+
+def sum_sum(x1, x2, c=10.0, eps=1e-12):
+    x1, x2 = _f64(x1), _f64(x2)
+    rows, n = x1.shape
+    d1, d2 = np.empty(rows), np.empty(rows)
+    lib().rfo_sum_sum(_p(x1), _p(x2), rows, n, c, eps, _p(d1), _p(d2))
+    return d1, d2
+
+
+def moments(mass, pos):
+    mass, pos = _f64(mass), _f64(pos)
+    rows, n, F = pos.shape
+    d1, d2, d3 = np.empty(rows), np.empty((rows, F)), np.empty((rows, F))
+    lib().rfo_moments(_p(mass), _p(pos), rows, n, F, _p(d1), _p(d2), _p(d3))
+    return d1, d2, d3
 
 
 def moe_routing(s, k):

@@ -175,3 +175,30 @@ def test_quant_e4m3_restatement_close_to_real_oracle():
 def test_quant_zero_row_is_domain_nan():
     d1, c = O.quant_gemm_e4m3(np.zeros((1, 128)), np.ones((128, 4)))
     assert d1[0] == 0 and np.isnan(c).all()
+
+
+@pytest.mark.parametrize("name", O.golden_names("variance_"))
+def test_variance_oracle_matches_reference(name):
+    g = O.load_golden(name)
+    d1, d2 = O.variance(g["in.x"].reshape(1, -1))
+    for tag in ["oracle", "incremental", "multi2", "multi8"]:
+        assert _err(d1, g[f"{tag}.d1"]) < TOL, tag
+        assert _err(d2, g[f"{tag}.d2"]) < TOL, tag
+
+
+@pytest.mark.parametrize("name", O.golden_names("sum_sum_"))
+def test_sum_sum_oracle_matches_reference(name):
+    g = O.load_golden(name)
+    d1, d2 = O.sum_sum(g["in.x1"].reshape(1, -1), g["in.x2"].reshape(1, -1), 10.0, 1e-12)
+    for tag in ["oracle", "incremental", "multi2", "multi8"]:
+        assert _err(d1, g[f"{tag}.d1"]) < TOL, tag
+        assert _err(d2, g[f"{tag}.d2"]) < TOL, tag
+
+
+def test_moments_oracle_matches_reference():
+    g = O.load_golden("moment_of_inertia_1024_s100")
+    d1, d2, d3 = O.moments(g["in.mass"].reshape(1, -1), g["in.pos"].reshape(1, 1024, 3))
+    for tag in ["oracle", "incremental", "multi2", "multi8"]:
+        assert _err(d1, g[f"{tag}.d1"]) < TOL, tag
+        assert _err(d2.ravel(), g[f"{tag}.d2"]) < TOL, tag
+        assert _err(d3.ravel(), g[f"{tag}.d3"]) < TOL, tag
