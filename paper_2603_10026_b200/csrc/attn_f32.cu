@@ -8,15 +8,28 @@
 // reference's own tile plan for this loop). The output accumulator is kept
 // normalised every tile (paper form, not deferred), so each slice's state
 // (m, l, O) is exactly the reference's exposed partial and slices merge with
-// incr_push_child semantics (merge.cu).
+// incr_push_child semantics.
 //
 // This path serves BASELINE config 1 (fp32, Sq=Skv=1024, D=64): small and
-// latency-bound, so it is a SIMT kernel with split-KV (segments) for
-// occupancy rather than a tensor-core kernel (fp32 parity at 1e-5 rules out
-// single-pass TF32). Register tiling: a CTA owns 64 query rows x 64-key tiles;
-// each thread computes a 4-row x 4-key block of S and a 4-row x D/16 block of
-// O (0.5 shared loads per FMA); a row's 16 threads are one half-warp, so the
-// row statistics reduce with shuffles. Row = one reference cascade instance.
+// latency-bound, so it is a SIMT kernel with split-KV for occupancy rather
+// than a tensor-core kernel (fp32 parity at 1e-5 rules out single-pass TF32).
+// Register tiling: a CTA owns 64 query rows x 64-key tiles; each thread
+// computes a 4-row x 4-key block of S (float4 shared loads along D) and a
+// 4-row x D/16 block of O whose columns are contiguous float4s, so the P V
+// phase reads P and V as float4 too (3 shared wavefronts per 64 FMA). A row's
+// 16 threads are one half-warp, so row statistics reduce with shuffles.
+//
+// Split-KV (run_multisegment, simulator.cpp:660-687): slice states go to the
+// partial buffers and are folded in slice order by merge.cu (or across GPUs).
+// The plan may cut each reference slice into c sub-slices to fill the GPU
+// (cfg1: 8 slices x 2 -> 256 CTAs, 2 per SM); the fold's closed form
+// (tests/acceptance.cpp:162-178) is the same sum over the finer slices.
+// Two one-launch variants were measured slower on cfg1: the
+// slices of a row tile as one thread-block cluster folding through DSMEM
+// (only 15 8-CTA clusters are co-resident, 16 needed -> two waves; 25-31 us),
+// and a last-arriving-CTA fold (threadfence + arrival counter; 22 us kernel
+// vs 13 + a ~5 us merge launch).
+#include <atomic>
 #include <cuda_bf16.h>
 
 #include "rf_internal.h"
@@ -45,11 +58,23 @@ __device__ __forceinline__ float hw_sum(float v) {
   for (int o = 1; o < 16; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+__device__ __forceinline__ float f4_at(const float4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+template <int D>
+constexpr size_t smem_floats() {
+  return static_cast<size_t>(BM + 2 * BN) * (D + 4) + BM * (BN + 4);
+}
 
 template <int D, typename T>
-__global__ void __launch_bounds__(NT) attn_f32_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(NT, D <= 64 ? 2 : 1) attn_f32_kernel(AttnArgs a) {
   constexpr int DP = D + 4;  // padded rows (float4-aligned, conflict-free column reads)
   constexpr int TD = D / 16;  // O columns per thread
+  // D >= 64: TD/4 float4s at columns c4*64 + 4*tx (P V reads P and V as
+  // float4); D = 16/32: scalar columns tx + 16*c.
+  constexpr bool VEC = D >= 64;
+  constexpr int TD4 = VEC ? TD / 4 : 1;
   extern __shared__ __align__(16) float smem_f32[];
   float* sQ = smem_f32;              // [BM][DP]   (pre-scaled)
   float* sK = sQ + BM * DP;          // [BN][DP]
@@ -84,24 +109,6 @@ __global__ void __launch_bounds__(NT) attn_f32_kernel(AttnArgs a) {
       return make_float4(load_f(p), load_f(p + 1), load_f(p + 2), load_f(p + 3));
     }
   };
-  {
-    float4 qv[NQ];
-#pragma unroll
-    for (int u = 0; u < NQ; ++u) {
-      const int idx = tid + u * NT;
-      qv[u] = idx < BM * CH ? ld4(Q + bh * a.sq * D, row0 + idx / CH, a.sq, idx % CH)
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int u = 0; u < NQ; ++u) {
-      const int idx = tid + u * NT;
-      if (idx < BM * CH) {
-        float4 v = qv[u];
-        v.x *= a.scale; v.y *= a.scale; v.z *= a.scale; v.w *= a.scale;
-        *reinterpret_cast<float4*>(sQ + (idx / CH) * DP + 4 * (idx % CH)) = v;
-      }
-    }
-  }
   float4 kr[NKV], vr[NKV];
   auto fetch = [&](int64_t t0) {
 #pragma unroll
@@ -113,8 +120,28 @@ __global__ void __launch_bounds__(NT) attn_f32_kernel(AttnArgs a) {
       vr[u] = ok ? ld4(V + bh * a.skv * D, key, kv1, idx % CH) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
-  fetch(kv0);
+  {
+    float4 qv[NQ];
+#pragma unroll
+    for (int u = 0; u < NQ; ++u) {
+      const int idx = tid + u * NT;
+      qv[u] = idx < BM * CH ? ld4(Q + bh * a.sq * D, row0 + idx / CH, a.sq, idx % CH)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    fetch(kv0);  // first K/V tile in flight with Q
+#pragma unroll
+    for (int u = 0; u < NQ; ++u) {
+      const int idx = tid + u * NT;
+      if (idx < BM * CH) {
+        float4 v = qv[u];
+        v.x *= a.scale; v.y *= a.scale; v.z *= a.scale; v.w *= a.scale;
+        *reinterpret_cast<float4*>(sQ + (idx / CH) * DP + 4 * (idx % CH)) = v;
+      }
+    }
+  }
 
+  // O column of this thread's c-th accumulator
+  auto col_of = [&](int c) { return VEC ? (c >> 2) * 64 + 4 * tx + (c & 3) : tx + 16 * c; };
   float m[TR], l[TR], o[TR][TD];
   bool touched = false;
 #pragma unroll
@@ -198,17 +225,44 @@ __global__ void __launch_bounds__(NT) attn_f32_kernel(AttnArgs a) {
     for (int r = 0; r < TR; ++r)
 #pragma unroll
       for (int c = 0; c < TD; ++c) acc[r][c] = 0.f;
+if constexpr (VEC) {
+#pragma unroll 2
+    for (int kk = 0; kk < BN; kk += 4) {
+      float4 pv[TR];
+#pragma unroll
+      for (int r = 0; r < TR; ++r) pv[r] = *reinterpret_cast<const float4*>(sP + (ty + 16 * r) * PP + kk);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float4 vv[TD4];
+#pragma unroll
+        for (int c4 = 0; c4 < TD4; ++c4)
+          vv[c4] = *reinterpret_cast<const float4*>(sV + (kk + u) * DP + c4 * 64 + 4 * tx);
+#pragma unroll
+        for (int r = 0; r < TR; ++r) {
+          const float pr = f4_at(pv[r], u);
+#pragma unroll
+          for (int c4 = 0; c4 < TD4; ++c4) {
+            acc[r][4 * c4 + 0] = fmaf(pr, vv[c4].x, acc[r][4 * c4 + 0]);
+            acc[r][4 * c4 + 1] = fmaf(pr, vv[c4].y, acc[r][4 * c4 + 1]);
+            acc[r][4 * c4 + 2] = fmaf(pr, vv[c4].z, acc[r][4 * c4 + 2]);
+            acc[r][4 * c4 + 3] = fmaf(pr, vv[c4].w, acc[r][4 * c4 + 3]);
+          }
+        }
+      }
+    }
+    } else {
 #pragma unroll 4
-    for (int kk = 0; kk < BN; ++kk) {
-      float pv[TR], vv[TD];
+      for (int kk = 0; kk < BN; ++kk) {
+        float pv[TR], vv[TD];
 #pragma unroll
-      for (int r = 0; r < TR; ++r) pv[r] = sP[(ty + 16 * r) * PP + kk];
+        for (int r = 0; r < TR; ++r) pv[r] = sP[(ty + 16 * r) * PP + kk];
 #pragma unroll
-      for (int c = 0; c < TD; ++c) vv[c] = sV[kk * DP + tx + 16 * c];
+        for (int c = 0; c < TD; ++c) vv[c] = sV[kk * DP + tx + 16 * c];
 #pragma unroll
-      for (int r = 0; r < TR; ++r)
+        for (int r = 0; r < TR; ++r)
 #pragma unroll
-        for (int c = 0; c < TD; ++c) acc[r][c] = fmaf(pv[r], vv[c], acc[r][c]);
+          for (int c = 0; c < TD; ++c) acc[r][c] = fmaf(pv[r], vv[c], acc[r][c]);
+      }
     }
 #pragma unroll
     for (int r = 0; r < TR; ++r)
@@ -216,47 +270,58 @@ __global__ void __launch_bounds__(NT) attn_f32_kernel(AttnArgs a) {
       for (int c = 0; c < TD; ++c) o[r][c] = fmaf(o[r][c], corr[r], acc[r][c] * inv_l[r]);
   }
 
+  // the slice merge (a programmatic dependent launch) may be scheduled now
+  asm volatile("griddepcontrol.launch_dependents;");
+  {
 #pragma unroll
-  for (int r = 0; r < TR; ++r) {
-    const int64_t gr = row0 + ty + 16 * r;
-    if (gr >= a.sq) continue;
-    const int64_t row = bh * a.sq + gr;
-    if (a.part_m == nullptr) {
-      T* O = static_cast<T*>(a.o);
+    for (int r = 0; r < TR; ++r) {
+      const int64_t gr = row0 + ty + 16 * r;
+      if (gr >= a.sq) continue;
+      const int64_t row = bh * a.sq + gr;
+      if (a.part_m == nullptr) {
+        T* O = static_cast<T*>(a.o);
 #pragma unroll
-      for (int c = 0; c < TD; ++c) store_f(O + row * D + tx + 16 * c, o[r][c]);
-      if (tx == 0) {
-        a.m[row] = m[r];
-        a.l[row] = l[r];
-      }
-    } else {
-      const int64_t ps = slice - a.part_base;
-      float* po = a.part_o + (ps * a.rows_total + row) * D;
+        for (int c = 0; c < TD; ++c) store_f(O + row * D + col_of(c), o[r][c]);
+        if (tx == 0) {
+          a.m[row] = m[r];
+          a.l[row] = l[r];
+        }
+      } else {
+        const int64_t ps = slice - a.part_base;
+        float* po = a.part_o + (ps * a.rows_total + row) * D;
 #pragma unroll
-      for (int c = 0; c < TD; ++c) po[tx + 16 * c] = o[r][c];
-      if (tx == 0) {
-        a.part_m[ps * a.rows_total + row] = m[r];
-        a.part_l[ps * a.rows_total + row] = l[r];
+        for (int c = 0; c < TD; ++c) po[col_of(c)] = o[r][c];
+        if (tx == 0) {
+          a.part_m[ps * a.rows_total + row] = m[r];
+          a.part_l[ps * a.rows_total + row] = l[r];
+        }
       }
     }
   }
 }
 
-template <int D>
-cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
+template <int D, typename T>
+cudaError_t launch_t(const AttnArgs& a, cudaStream_t st) {
+  auto k = attn_f32_kernel<D, T>;
+  const size_t smem = sizeof(float) * smem_floats<D>();
+  static std::atomic<uint64_t> attr_set{0};  // per device, per template instance
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (!(attr_set.load(std::memory_order_relaxed) & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set.fetch_or(bit);
+  }
   dim3 grid(static_cast<unsigned>((a.sq + BM - 1) / BM), static_cast<unsigned>(a.bh),
             static_cast<unsigned>(a.nslices));
-  const size_t smem = sizeof(float) * ((BM + 2 * BN) * (D + 4) + BM * (BN + 4));
-  if (a.dtype == RF_BF16) {
-    auto k = attn_f32_kernel<D, __nv_bfloat16>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, NT, smem, st>>>(a);
-  } else {
-    auto k = attn_f32_kernel<D, float>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, NT, smem, st>>>(a);
-  }
+  k<<<grid, NT, smem, st>>>(a);
   return cudaGetLastError();
+}
+
+template <int D>
+cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
+  return a.dtype == RF_BF16 ? launch_t<D, __nv_bfloat16>(a, st) : launch_t<D, float>(a, st);
 }
 
 }  // namespace

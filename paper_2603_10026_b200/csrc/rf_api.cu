@@ -342,6 +342,15 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
       p->nsplit = d.segments;
       if (d.dtype == RF_F32) {
         p->kernel = rf::Kernel::AttentionF32;
+        // A grid too small to fill the GPU (cfg1: 16 row tiles x 8 slices):
+        // cut every reference slice into c sub-slices of >= 64 keys, up to
+        // two CTAs per SM. The slice-ordered fold's closed form is the same
+        // sum over the finer slices (merge.cu); rf_run_partials keeps the
+        // reference's slices.
+        const int64_t tiles = d.batch * d.heads * ((d.rows + 63) / 64);
+        const int64_t slice = d.len / d.segments;
+        for (int64_t c = 2; c <= 16 && tiles * p->nsplit < 2 * 148; c *= 2)
+          if (slice % c == 0 && slice / c >= 64) p->nsplit = d.segments * c;
       } else if (d.rows == 1) {
         p->kernel = rf::Kernel::AttentionDecode;
         p->nsplit = pick_decode_splits(d.batch * d.heads, d.len, d.segments);

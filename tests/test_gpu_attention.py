@@ -60,6 +60,28 @@ def test_fp32_ragged_shapes(shape):
     _check(q, k, v, m, l, o, 1e-5)
 
 
+@pytest.mark.parametrize("shape,segments", [((2, 3, 100, 512, 128), 4), ((1, 2, 64, 96, 64), 2),
+                                            ((1, 1, 200, 1024, 64), 8), ((3, 1, 17, 64, 128), 1),
+                                            ((1, 1, 64, 1024, 16), 32)])
+def test_fp32_sub_slices(shape, segments):
+    """Reference slices cut into sub-slices by the plan to fill the GPU, folded
+    by the merge kernel: ragged rows, slices shorter than a KV tile, D = 64 /
+    128, and run_incremental (segments = 1) on a small grid."""
+    import torch
+    from paper_2603_10026_b200 import Desc, Plan
+    from paper_2603_10026_b200 import _native as N
+
+    B, H, Sq, Skv, D = shape
+    q, k, v = _inputs(B, H, Sq, Skv, D, 11, torch.float32)
+    plan = Plan(Desc(N.RF_PATTERN_ATTENTION, "f32", rows=Sq, len=Skv, free_len=D, batch=B,
+                     heads=H, segments=segments))
+    m = torch.empty(B, H, Sq, device="cuda")
+    l, o = torch.empty_like(m), torch.empty(B, H, Sq, D, device="cuda")
+    plan.run([q.cuda(), k.cuda(), v.cuda()], [m, l, o])
+    torch.cuda.synchronize()
+    _check(q, k, v, m, l, o, 1e-5)
+
+
 @pytest.mark.parametrize("name", O.golden_names("attention_"))
 def test_fp32_against_reference_goldens(name):
     """The reference's own fixtures (its generator, oracle and executors)."""
