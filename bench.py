@@ -47,6 +47,10 @@ CONFIGS = {
     # not a BASELINE.json config: the north_star's LayerNorm variant of cfg5
     5: dict(name="cfg6: LayerNorm stats + GEMM T16384 K4096 N11008 (extra, north_star)",
             pattern="ln", M=16384, K=4096, N=11008, dtype="bf16"),
+    # not a BASELINE.json config: SURVEY §8 f1, the paper's MoE routing R8
+    # (PAPER.md:1583-1590): router GEMM 2048 x 4096 -> 128 experts + top-8
+    6: dict(name="cfg7: MoE router R8 s2048 hd4096 en128 top8 (extra, SURVEY f1)",
+            pattern="router", M=2048, K=4096, N=128, topk=8, dtype="bf16"),
 }
 
 
@@ -85,6 +89,8 @@ def work_of(cfg):
         return flops, bytes_
     M, K, N = cfg["M"], cfg["K"], cfg["N"]
     flops = 2.0 * M * N * K
+    if cfg["pattern"] == "router":  # X once, packed W once, d1/d2 + top-k records
+        return flops, 2 * M * K + 2 * N * K + 8 * M + 8 * M * cfg["topk"]
     if cfg["pattern"] == "quant":
         bytes_ = 2 * M * K + N * K + 4 * M * N + 4 * M
     elif cfg["pattern"] == "ln":  # d3 and d4 both written (bf16), d1/d2 f32
@@ -96,6 +102,8 @@ def work_of(cfg):
 
 def bound_of(cfg):
     if cfg["pattern"] == "attention" and cfg["Sq"] == 1:
+        return "hbm"
+    if cfg["pattern"] == "router":  # 2 * en FLOP per byte of X: far below the ridge
         return "hbm"
     return "tensor"
 
@@ -157,6 +165,10 @@ def cpu_reference(cfg, budget_s=12.0, threads=None):
         segs = cfg.get("segments", 1) if cfg["Sq"] == 1 else 1
         args = ["attention", str(cfg["Skv"]), str(cfg["D"]), "100000000", str(threads), str(segs)]
         sample = f"rows = (b,h,query) cascades of kv={cfg['Skv']}, hd={cfg['D']}"
+    elif cfg["pattern"] == "router":
+        args = ["router", str(cfg["K"]), str(cfg["N"]), "100000000", str(threads), str(cfg["topk"])]
+        sample = (f"rows = tokens: router GEMM hd={cfg['K']} -> en={cfg['N']} (fp64) + the "
+                  f"moe_routing cascade (top-{cfg['topk']})")
     elif cfg["pattern"] == "quant":
         args = ["quant", str(cfg["K"]), str(cfg["N"]), str(threads), str(threads), "1"]
         sample = f"rows = tokens of K={cfg['K']}, N={cfg['N']}"
@@ -233,7 +245,17 @@ class Workload:
             self.segments_global = cfg.get("segments", 1) * world
         else:
             M, K, Nn = cfg["M"], cfg["K"], cfg["N"]
-            if pat == "quant":
+            if pat == "router":
+                a = (rnd(M, K) * 2 - 1).bfloat16()
+                self.plan = Plan(Desc(N.RF_PATTERN_MOE_ROUTER, "bf16", rows=M, len=Nn,
+                                      free_len=cfg["topk"], producer_len=K, device=dev.index))
+                w = (rnd(K, Nn) * 2 - 1) / K ** 0.5
+                wp = self.plan.pack_weight(w)
+                del w
+                self.outputs = [torch.empty(M, device=dev), torch.empty(M, device=dev),
+                                torch.empty(M, cfg["topk"], 2, dtype=torch.int32, device=dev)]
+                self.data = "synthetic (x ~ U(-1,1) bf16, router w ~ U(-1,1)/sqrt(hd) packed bf16)"
+            elif pat == "quant":
                 a = (rnd(M, K) * 4 - 2).bfloat16()  # make_quant_gemm: a ~ U(-2, 2)
                 self.plan = Plan(Desc(N.RF_PATTERN_QUANT_GEMM_E4M3, "bf16", rows=M, len=K,
                                       free_len=Nn, device=dev.index))
@@ -424,7 +446,7 @@ def run_ours(args, cfg):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": {"quant": "e4m3 (bf16 in)", "rms": "bf16", "ln": "bf16"}.get(cfg["pattern"], cfg["dtype"]),
+        "dtype": {"quant": "e4m3 (bf16 in)", "rms": "bf16", "ln": "bf16", "router": "bf16"}.get(cfg["pattern"], cfg["dtype"]),
         "data": wl.data,
         "config": conf,
         "roofline": {"bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 1),
@@ -476,7 +498,13 @@ def run_reference(args, cfg):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (the reference's own make_attention generator)",
+        "data": "synthetic (" + {
+            "attention": "the reference's own make_attention generator",
+            "quant": "the reference's own make_quant_gemm generator",
+            "rms": "the reference's DSL input generator for the RMSNorm->GEMM cascade",
+            "ln": "the reference's DSL input generator for the LayerNorm->GEMM cascade",
+            "router": "x, w ~ U(-1,1); scores through make_moe_routing's cascade",
+        }[cfg["pattern"]] + ")",
         "config": {"workload": cfg["name"]},
         "cpu_baseline": cb,
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

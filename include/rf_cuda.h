@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define RF_CUDA_ABI_VERSION 2
+#define RF_CUDA_ABI_VERSION 3
 
 typedef enum rf_status {
   RF_OK = 0,
@@ -87,7 +87,12 @@ typedef enum rf_pattern {
   RF_PATTERN_SUM_SUM = 8,
   /* d1 = sum m, d2[f] = sum m p[l,f], d3[f] = sum m p[l,f]^2, free_len <= 8
    *                                               (data/moment_of_inertia.cascade)        */
-  RF_PATTERN_MOMENTS = 9
+  RF_PATTERN_MOMENTS = 9,
+  /* MoE router: scores s = X W (the router GEMM; a producer of the
+   * cascade input) feeding the MOE_ROUTING cascade: d1 = max s, d2 = sum exp(s - d1),
+   * d3 = top-K' of s, ties to the lowest index. len = experts (32/64/128/256),
+   * free_len = K' <= 8, producer_len = hd (the GEMM's reduce axis, % 64)      */
+  RF_PATTERN_MOE_ROUTER = 10
 } rf_pattern;
 
 typedef enum rf_dtype { RF_F32 = 0, RF_BF16 = 1, RF_E4M3 = 2 } rf_dtype;
@@ -111,7 +116,8 @@ typedef struct rf_desc {
   int32_t tile_rows;    /* 0 = kernel default (reference pick_tile: 128) */
   int32_t tile_stream;  /* 0 = kernel default */
   int32_t device;       /* CUDA ordinal the plan is bound to */
-  int32_t reserved;
+  int32_t producer_len; /* MOE_ROUTER: hd, the reduce axis of the producer GEMM (ABI v3;
+                           was `reserved` in v2, same offset) */
 } rf_desc;
 
 /* Device buffers for one rf_run. Inputs by pattern:
@@ -129,6 +135,9 @@ typedef struct rf_desc {
  *   MOE_ROUTING    in[0] = logits [rows, experts] f32 (len = experts, free_len = K' <= 8);
  *                  d1, d2 [rows] f32; d3 = [rows, K'] records {f32 value, i32 index}
  *                  (1-based expert index like OutputVal.topk; 0 = empty slot)
+ *   MOE_ROUTER     in[0] = X [rows, hd] bf16, in[1] = packed W (rf_pack_weight: w [hd, en]
+ *                  f32 -> bf16 [en, hd]); d1, d2, d3 as MOE_ROUTING; d4 = the scores s
+ *                  [rows, en] f32 (optional: may be null)
  *   VARIANCE       in[0] = x [rows, len] f32; d1, d2 [rows] f32
  *   SUM_SUM        in[0] = x1, in[1] = x2 [rows, len] f32; d1, d2 [rows] f32
  *   MOMENTS        in[0] = mass [rows, len] f32, in[1] = pos [rows, len, free_len] f32;
@@ -175,6 +184,7 @@ int64_t rf_plan_launches_per_run(const rf_plan* plan);
  *   RMSNORM_GEMM: w [K,N] f32, g [K] f32 -> packed bf16 [N,K] of g[l]*w[l,f]
  *   LAYERNORM_GEMM: as RMSNORM_GEMM, followed by N f32 column sums of the packed
  *                 (bf16-rounded) g*w, at byte offset 2*N*K
+ *   MOE_ROUTER:   w [hd, en] f32 -> packed bf16 [en, hd] (g unused)
  * `packed` must hold rf_packed_bytes(plan) bytes. Stream-ordered. */
 rf_status rf_pack_weight(const rf_plan* plan, const void* w, const void* g, void* packed,
                          void* stream);

@@ -12,6 +12,7 @@
 //       pinned against these.
 //
 //   ref_driver bench <pattern> <L0> <free> <rows> <threads> [segments] [budget_s]
+//   ref_driver bench router <hd> <experts> <rows> <threads> <K'> [budget_s]
 //       Times the reference's CPU fused loop (run_incremental, or
 //       run_multisegment when segments > 1; proj/src/simulator.cpp:631-687) on
 //       a bounded sample of rows of a BASELINE.json configuration, one row per
@@ -377,9 +378,48 @@ struct SoftmaxJob : RowJob {
   double flops_per_row() const override { return 3.0 * n; }
 };
 
+// MoE router: the producer GEMM s = x W (hd -> en, the paper's routing
+// module) recomputed per token inside the timed body like the
+// attention P row, then the make_moe_routing cascade (workloads.cpp:124-169)
+// through run_incremental.
+struct RouterJob : RowJob {
+  long long hd, en, k;
+  Workload w;
+  FusedProgram prog;
+  std::vector<double> wt;  // [hd, en], shared by every token
+  RouterJob(long long hd_, long long en_, long long k_)
+      : hd(hd_), en(en_), k(k_), w(make_moe_routing(en_, k_)), prog(derive_fused(w.spec)) {
+    std::mt19937_64 rng(7);
+    std::uniform_real_distribution<double> u(-1.0, 1.0);
+    wt.resize(static_cast<std::size_t>(hd * en));
+    for (double& x : wt) x = u(rng) / std::sqrt(static_cast<double>(hd));
+  }
+  TensorStore make(std::uint64_t seed) const override {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> u(-1.0, 1.0);
+    std::vector<double> x(static_cast<std::size_t>(hd));
+    for (double& v : x) v = u(rng);
+    TensorStore st;
+    st.define("x", hd, 0, std::move(x));
+    return st;
+  }
+  void run(TensorStore& st) const override {
+    const auto& x = st.array("x").data;
+    std::vector<double> sc(static_cast<std::size_t>(en), 0.0);
+    for (long long l = 0; l < hd; ++l)
+      for (long long e = 0; e < en; ++e) sc[e] += x[l] * wt[l * en + e];
+    TensorStore row;
+    row.define("s", en, 0, std::move(sc));
+    ExecReport r = run_incremental(prog, TreeConfig{{en, 1}}, row);
+    if (r.outputs.size() != 3) std::abort();
+  }
+  double flops_per_row() const override { return 2.0 * hd * en; }
+};
+
 int cmd_bench(int argc, char** argv) {
   if (argc < 7) {
-    std::fprintf(stderr, "bench <attention|quant|rms|ln|softmax> <L0> <free> <rows> <threads> [segments]\n");
+    std::fprintf(stderr, "bench <attention|quant|rms|ln|softmax> <L0> <free> <rows> <threads> [segments]\n"
+                         "bench router <hd> <experts> <rows> <threads> <K'>\n");
     return 2;
   }
   std::string pat = argv[2];
@@ -394,6 +434,7 @@ int cmd_bench(int argc, char** argv) {
   else if (pat == "rms") job = std::make_unique<RmsJob>(l0, fr);
   else if (pat == "ln") job = std::make_unique<LnJob>(l0, fr);
   else if (pat == "softmax") job = std::make_unique<SoftmaxJob>(l0);
+  else if (pat == "router") job = std::make_unique<RouterJob>(l0, fr, segs);  // hd, en, K'
   else return 2;
   if (threads < 1) threads = 1;
   if (rows < threads) rows = threads;

@@ -17,6 +17,8 @@ from .executors import (  # noqa: F401
     attention,
     layernorm_gemm,
     layernorm_gemm_plan,
+    moe_router,
+    moe_router_plan,
     moe_routing,
     moments,
     plan,
@@ -36,6 +38,7 @@ __all__ = [
     "rmsnorm_gemm",
     "layernorm_gemm",
     "moe_routing",
+    "moe_router",
     "variance",
     "sum_sum",
     "moments",

@@ -33,8 +33,9 @@ RF_PATTERN_LAYERNORM_GEMM = 6
 RF_PATTERN_VARIANCE = 7
 RF_PATTERN_SUM_SUM = 8
 RF_PATTERN_MOMENTS = 9
+RF_PATTERN_MOE_ROUTER = 10
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # rf_dtype
 RF_F32 = 0
@@ -59,7 +60,7 @@ class rf_desc(ctypes.Structure):
         ("tile_rows", ctypes.c_int32),
         ("tile_stream", ctypes.c_int32),
         ("device", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("producer_len", ctypes.c_int32),
     ]
 
 

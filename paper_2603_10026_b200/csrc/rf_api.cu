@@ -56,9 +56,22 @@ rf_status fail(rf_status s, const std::string& msg) {
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+// Patterns with a plan-time packed weight in in[1] (tcgen05 GEMM tiles of 128 rows).
 bool is_gemm(int pattern) {
   return pattern == RF_PATTERN_QUANT_GEMM_E4M3 || pattern == RF_PATTERN_RMSNORM_GEMM ||
-         pattern == RF_PATTERN_LAYERNORM_GEMM;
+         pattern == RF_PATTERN_LAYERNORM_GEMM || pattern == RF_PATTERN_MOE_ROUTER;
+}
+
+// The packed weight's source w [k, n] (reduce-axis major): GEMM patterns
+// w [K, N]; the MoE router's w [hd, experts].
+void pack_dims(const rf_desc& d, int64_t& k, int64_t& n) {
+  if (d.pattern == RF_PATTERN_MOE_ROUTER) {
+    k = d.producer_len;
+    n = d.len;
+  } else {
+    k = d.len;
+    n = d.free_len;
+  }
 }
 
 // Input/output byte sizes per pattern, for the host path and shape checks.
@@ -100,6 +113,12 @@ void io_sizes(const rf_plan* p, size_t in[4], size_t out[4]) {
       out[0] = out[1] = sizeof(float) * d.rows;
       out[2] = 8 * d.rows * d.free_len;
       break;
+    case RF_PATTERN_MOE_ROUTER:
+      in[0] = 2 * d.rows * d.producer_len;
+      out[0] = out[1] = sizeof(float) * d.rows;
+      out[2] = 8 * d.rows * d.free_len;
+      out[3] = sizeof(float) * d.rows * d.len;
+      break;
     case RF_PATTERN_VARIANCE:
       in[0] = sizeof(float) * d.rows * d.len;
       out[0] = out[1] = sizeof(float) * d.rows;
@@ -129,6 +148,7 @@ const char* kernel_name(rf::Kernel k) {
     case rf::Kernel::MoeRouting: return "moe_routing (SIMT, warp per token, bit-exact top-k)";
     case rf::Kernel::LayerNormGemmSm100: return "layernorm_gemm_sm100 (bf16 tcgen05 cta_group::2)";
     case rf::Kernel::RowStats: return "rowstats (SIMT HBM streaming, fp64 accumulation)";
+    case rf::Kernel::MoeRouter: return "moe_router (tcgen05 split-K router GEMM + routing cascade)";
   }
   return "?";
 }
@@ -235,6 +255,26 @@ rf_status run_range(const rf_plan* p, const rf_io* io, int64_t u0, int64_t nu, c
           static_cast<int>(p->d.free_len), static_cast<float*>(io->d[0]) + u0,
           static_cast<float*>(io->d[1]) + u0, static_cast<char*>(io->d[2]) + 8 * u0 * p->d.free_len, st);
       if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("moe launch: ") + cudaGetErrorString(e));
+      return RF_OK;
+    }
+    case RF_PATTERN_MOE_ROUTER: {
+      const rf_desc& d = p->d;
+      rf::RouterArgs r{};
+      r.x = static_cast<const char*>(io->in[0]) + 2 * u0 * d.producer_len;
+      r.w = io->in[1];
+      r.part = p->ws_m + u0 * d.len;
+      r.rows = nu;
+      r.hd = d.producer_len;
+      r.experts = d.len;
+      r.splits = p->nsplit;
+      r.part_stride = d.rows;
+      r.k = static_cast<int>(d.free_len);
+      r.d1 = static_cast<float*>(io->d[0]) + u0;
+      r.d2 = static_cast<float*>(io->d[1]) + u0;
+      r.topk = static_cast<char*>(io->d[2]) + 8 * u0 * d.free_len;
+      r.scores = io->d[3] ? static_cast<float*>(io->d[3]) + u0 * d.len : nullptr;
+      cudaError_t e = rf::launch_router(r, st);
+      if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("router launch: ") + cudaGetErrorString(e));
       return RF_OK;
     }
     case RF_PATTERN_VARIANCE:
@@ -390,6 +430,16 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
       p->kernel = rf::Kernel::MoeRouting;
       p->rows_total = d.rows;
       break;
+    case RF_PATTERN_MOE_ROUTER:
+      if (d.dtype != RF_BF16) return bail(RF_ERR_UNSUPPORTED, "moe_router: bf16 activations");
+      if (!rf::router_supports(d.rows, d.producer_len, d.len, d.free_len))
+        return bail(RF_ERR_UNSUPPORTED,
+                    "moe_router: experts (len) must be 32/64/128/256, hd (producer_len) % 64, "
+                    "1 <= K' (free_len) <= min(8, experts)");
+      p->kernel = rf::Kernel::MoeRouter;
+      p->rows_total = d.rows;
+      p->nsplit = rf::router_pick_splits(d.rows, d.producer_len);
+      break;
     case RF_PATTERN_VARIANCE:
     case RF_PATTERN_SUM_SUM:
     case RF_PATTERN_MOMENTS:
@@ -404,7 +454,8 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
     default:
       return bail(RF_ERR_UNSUPPORTED, "unknown pattern");
   }
-  p->launches = (p->d.pattern == RF_PATTERN_ATTENTION && p->nsplit > 1) ? 2 : 1;
+  p->launches = ((p->d.pattern == RF_PATTERN_ATTENTION && p->nsplit > 1) ||
+                 p->d.pattern == RF_PATTERN_MOE_ROUTER) ? 2 : 1;
 
   // ---- persistent workspace ----
   if (cudaMalloc(&p->domain_flag, sizeof(int)) != cudaSuccess ||
@@ -416,6 +467,11 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
         cudaMalloc(&p->ws_l, n * sizeof(float)) != cudaSuccess ||
         cudaMalloc(&p->ws_o, n * d.free_len * sizeof(float)) != cudaSuccess)
       return bail(RF_ERR_CUDA, "segment workspace allocation failed");
+  }
+  if (p->d.pattern == RF_PATTERN_MOE_ROUTER) {  // split-K partial scores (L2-resident)
+    const size_t n = static_cast<size_t>(p->nsplit) * p->d.rows * p->d.len;
+    if (n && cudaMalloc(&p->ws_m, n * sizeof(float)) != cudaSuccess)
+      return bail(RF_ERR_CUDA, "router workspace allocation failed");
   }
   char buf[512];
   std::snprintf(buf, sizeof buf,
@@ -468,6 +524,9 @@ rf_status rf_pack_weight(const rf_plan* p, const void* w, const void* g, void* p
                             reinterpret_cast<float*>(static_cast<char*>(packed) +
                                                      2 * p->d.free_len * p->d.len),
                             as_stream(stream));
+  } else if (p->d.pattern == RF_PATTERN_MOE_ROUTER) {
+    e = rf::launch_pack_rms(static_cast<const float*>(w), nullptr, p->d.producer_len, p->d.len, packed,
+                            as_stream(stream));
   } else {
     return fail(RF_ERR_UNSUPPORTED, "pattern has no packed weight");
   }
@@ -482,6 +541,7 @@ size_t rf_packed_bytes(const rf_plan* p) {
     case RF_PATTERN_QUANT_GEMM_E4M3: return nk;
     case RF_PATTERN_RMSNORM_GEMM: return 2 * nk;
     case RF_PATTERN_LAYERNORM_GEMM: return 2 * nk + 4 * static_cast<size_t>(p->d.free_len);
+    case RF_PATTERN_MOE_ROUTER: return 2 * static_cast<size_t>(p->d.producer_len) * p->d.len;
     default: return 0;
   }
 }
@@ -489,21 +549,23 @@ size_t rf_packed_bytes(const rf_plan* p) {
 rf_status rf_pack_weight_host(const rf_plan* p, const float* w, const float* g, void** packed) {
   if (!p || !w || !packed) return fail(RF_ERR_ARG, "null plan/w/packed");
   *packed = nullptr;
-  const bool quant = p->d.pattern == RF_PATTERN_QUANT_GEMM_E4M3;
+  const bool needs_g = p->d.pattern == RF_PATTERN_RMSNORM_GEMM || p->d.pattern == RF_PATTERN_LAYERNORM_GEMM;
   if (rf_packed_bytes(p) == 0) return fail(RF_ERR_UNSUPPORTED, "pattern has no packed weight");
-  if (!quant && !g) return fail(RF_ERR_ARG, "rmsnorm pack needs g");
+  if (needs_g && !g) return fail(RF_ERR_ARG, "rmsnorm/layernorm pack needs g");
+  int64_t wk = 0, wn = 0;
+  pack_dims(p->d, wk, wn);
   int prev = 0;
   cudaGetDevice(&prev);
   RF_CUDA_TRY(cudaSetDevice(p->d.device));
-  const size_t kn = static_cast<size_t>(p->d.len) * p->d.free_len;
+  const size_t kn = static_cast<size_t>(wk) * wn;
   float *dw = nullptr, *dg = nullptr;
   void* out = nullptr;
   RF_CUDA_TRY(cudaMalloc(&dw, kn * sizeof(float)));
   RF_CUDA_TRY(cudaMalloc(&out, rf_packed_bytes(p)));
   RF_CUDA_TRY(cudaMemcpy(dw, w, kn * sizeof(float), cudaMemcpyHostToDevice));
-  if (g) {
-    RF_CUDA_TRY(cudaMalloc(&dg, p->d.len * sizeof(float)));
-    RF_CUDA_TRY(cudaMemcpy(dg, g, p->d.len * sizeof(float), cudaMemcpyHostToDevice));
+  if (g && needs_g) {
+    RF_CUDA_TRY(cudaMalloc(&dg, wk * sizeof(float)));
+    RF_CUDA_TRY(cudaMemcpy(dg, g, wk * sizeof(float), cudaMemcpyHostToDevice));
   }
   rf_status st = rf_pack_weight(p, dw, dg, out, nullptr);
   RF_CUDA_TRY(cudaDeviceSynchronize());
@@ -526,7 +588,7 @@ rf_status rf_run(const rf_plan* p, const rf_io* io, void* stream) {
   io_sizes(p, in, out);
   for (int i = 0; i < 4; ++i)
     if (in[i] && !io->in[i]) return fail(RF_ERR_SHAPE, "missing input " + std::to_string(i));
-  for (int i = 0; i < 3; ++i)  // d4 (layernorm) is optional
+  for (int i = 0; i < 3; ++i)  // d4 (layernorm; router scores) is optional
     if (out[i] && !io->d[i]) return fail(RF_ERR_SHAPE, "missing output d" + std::to_string(i + 1));
   if (is_gemm(p->d.pattern) && !io->in[1])
     return fail(RF_ERR_SHAPE, "missing packed weight in[1]");

@@ -34,7 +34,24 @@ enum class Kernel {
   MoeRouting,         // moe.cu (softmax stats + top-k, bit-exact indices)
   LayerNormGemmSm100, // gemm_sm100.cu (bf16, 2-SM; variance cascade + GEMM)
   RowStats,           // rowstats.cu (variance / sum_sum / moments: HBM streaming)
+  MoeRouter,          // router.cu (tcgen05 split-K router GEMM + routing cascade)
 };
+
+// MoE router (router.cu): scores = X W^T-packed, then the routing cascade.
+struct RouterArgs {
+  const void* x;        // [rows, hd] bf16
+  const void* w;        // packed [experts, hd] bf16
+  float* part;          // split partials [splits, part_stride, experts] (+ row offset)
+  int64_t rows, hd, experts, splits, part_stride;
+  int k;                // K' (top-k size)
+  float* d1;
+  float* d2;
+  void* topk;           // [rows, K'] {f32 value, i32 1-based index}
+  float* scores;        // [rows, experts] f32 or null
+};
+cudaError_t launch_router(const RouterArgs& a, cudaStream_t st);
+bool router_supports(int64_t rows, int64_t hd, int64_t experts, int64_t k);
+int64_t router_pick_splits(int64_t rows, int64_t hd);
 
 // Row-statistics cascades (rowstats.cu): a = x | x1 | mass, b = - | x2 | pos.
 struct RowStatsArgs {

@@ -93,6 +93,7 @@ class Desc:
     softmax_scale: float = 1.0
     offset: float = 0.0
     device: int = 0
+    producer_len: int = 0  # MOE_ROUTER: hd (the router GEMM's reduce axis)
 
     def to_c(self) -> N.rf_desc:
         d = N.rf_desc()
@@ -104,6 +105,7 @@ class Desc:
         d.offset = self.offset
         d.tile_rows = d.tile_stream = 0
         d.device = self.device
+        d.producer_len = self.producer_len
         return d
 
 
@@ -165,6 +167,8 @@ class Plan:
         import torch
 
         k, n = self.desc.len, self.desc.free_len
+        if self.desc.pattern == N.RF_PATTERN_MOE_ROUTER:
+            k, n = self.desc.producer_len, self.desc.len  # w [hd, experts]
         if tuple(w.shape) != (k, n) or w.dtype != torch.float32:
             raise ShapeMismatch(f"w must be float32 [{k}, {n}] (reduce-axis major)")
         nbytes = int(N.lib().rf_packed_bytes(self._h))
@@ -175,7 +179,7 @@ class Plan:
                                      _stream_ptr(stream)))
         if self.desc.pattern == N.RF_PATTERN_QUANT_GEMM_E4M3:
             return raw.view(n, k)
-        if self.desc.pattern == N.RF_PATTERN_RMSNORM_GEMM:
+        if self.desc.pattern in (N.RF_PATTERN_RMSNORM_GEMM, N.RF_PATTERN_MOE_ROUTER):
             return raw.view(torch.bfloat16).view(n, k)
         # layernorm: bf16 [N, K] (g folded) followed by N f32 column sums; the
         # returned tensor is the whole buffer (rf_run reads both parts)
@@ -321,6 +325,31 @@ def moe_routing(logits, k: int, stream=None):
     rec = torch.empty(rows, k, 2, dtype=torch.int32, device=logits.device)
     p.run([logits.contiguous()], [d1, d2, rec], stream)
     return d1, d2, rec[..., 0].view(torch.float32), rec[..., 1]
+
+
+def moe_router_plan(tokens: int, hd: int, experts: int, k: int, device: int = 0) -> Plan:
+    return plan(Desc(N.RF_PATTERN_MOE_ROUTER, "bf16", rows=tokens, len=experts, free_len=k,
+                     producer_len=hd, device=device))
+
+
+def moe_router(x, w_packed, k: int, with_scores: bool = False, stream=None):
+    """MoE router: scores s = x W (router GEMM on tcgen05) and the routing
+    cascade over them (d1 = max s, d2 = sum exp(s - d1), top-k experts, ties to
+    the lowest index). x: [tokens, hd] bf16; w_packed: Plan.pack_weight of
+    w [hd, experts] float32. Returns (d1, d2, values, indices[, scores])."""
+    import torch
+
+    _require(x.dim() == 2 and x.dtype == torch.bfloat16, "x must be bfloat16 [tokens, hd]")
+    tokens, hd = x.shape
+    experts = w_packed.shape[0]
+    p = moe_router_plan(tokens, hd, experts, k, x.device.index or 0)
+    d1 = torch.empty(tokens, dtype=torch.float32, device=x.device)
+    d2 = torch.empty_like(d1)
+    rec = torch.empty(tokens, k, 2, dtype=torch.int32, device=x.device)
+    sc = torch.empty(tokens, experts, dtype=torch.float32, device=x.device) if with_scores else None
+    p.run([x.contiguous(), w_packed], [d1, d2, rec, sc], stream)
+    out = (d1, d2, rec[..., 0].view(torch.float32), rec[..., 1])
+    return out + (sc,) if with_scores else out
 
 
 def _rows_f32(name, *ts):

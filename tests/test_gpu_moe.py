@@ -11,7 +11,7 @@ from tests import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("experts,k", [(128, 1), (64, 6), (64, 8), (128, 8), (100, 3), (7, 4)])
+@pytest.mark.parametrize("experts,k", [(128, 1), (64, 6), (64, 8), (128, 8), (100, 3), (7, 4), (300, 5), (256, 8)])
 def test_moe_routing_vs_oracle(experts, k):
     import torch
     from paper_2603_10026_b200 import moe_routing
