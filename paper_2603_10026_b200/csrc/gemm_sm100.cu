@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(NT, 1)
 namespace rms2 {
 
 constexpr int BK = 64;
-constexpr int STAGES = 6;
+constexpr int STAGES = 3;  // two CTA pairs per SM pair: one pair's epilogue overlaps the other's mainloop
 constexpr int NT = 192;  // warps 0-3 stats + epilogue, 4 TMA, 5 MMA (leader) / relay (peer)
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB: this CTA's 128 rows
 constexpr int B_BYTES = 128 * BK * 2; // 16 KB: this CTA's half of the 256 N-rows
@@ -240,7 +240,7 @@ struct Smem {
 // d1 = sum x, d2 = sum x^2 from the same tiles; d3 = acc / sigma and
 // d4 = (d1/K) / sigma * colsum in the epilogue — both corrections telescope).
 template <bool LN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 2)
     rms_gemm_2sm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                         const __grid_constant__ CUtensorMap ty, const __grid_constant__ CUtensorMap ty4,
                         const rms::Params p) {
