@@ -51,6 +51,10 @@ CONFIGS = {
     # (PAPER.md:1583-1590): router GEMM 2048 x 4096 -> 128 experts + top-8
     6: dict(name="cfg7: MoE router R8 s2048 hd4096 en128 top8 (extra, SURVEY f1)",
             pattern="router", M=2048, K=4096, N=128, topk=8, dtype="bf16"),
+    # not a BASELINE.json config: SURVEY §8 f4, the paper's MLA decode L3
+    # (PAPER.md:1559-1567): bs 32, 128 heads, kv 4096, latent 512 + rope 64
+    7: dict(name="cfg8: MLA decode L3 bs32 hn128 kv4096 hd512+64 (extra, SURVEY f4)",
+            pattern="mla", B=32, Skv=4096, dtype="bf16", segments=1),
 }
 
 
@@ -81,6 +85,9 @@ def fp8_peak():
 
 def work_of(cfg):
     """Algorithmic FLOPs and bytes per step."""
+    if cfg["pattern"] == "mla":  # S = q K^T (576) + P V (512) per head; cache read once
+        B, S = cfg["B"], cfg["Skv"]
+        return 2.0 * B * 128 * S * (576 + 512), 2 * B * S * 576 + 2 * B * 128 * (576 + 512) + 8 * B * 128
     if cfg["pattern"] == "attention":
         B, H, Sq, Skv, D = cfg["B"], cfg["H"], cfg["Sq"], cfg["Skv"], cfg["D"]
         es = 4 if cfg["dtype"] == "f32" else 2
@@ -104,6 +111,8 @@ def bound_of(cfg):
     if cfg["pattern"] == "attention" and cfg["Sq"] == 1:
         return "hbm"
     if cfg["pattern"] == "router":  # 2 * en FLOP per byte of X: far below the ridge
+        return "hbm"
+    if cfg["pattern"] == "mla":  # ~240 FLOP/B: at the ridge; the cache stream bounds it
         return "hbm"
     return "tensor"
 
@@ -161,7 +170,11 @@ def cpu_reference(cfg, budget_s=12.0, threads=None):
     if not os.path.exists(REF_DRIVER):
         return None
     threads = threads or os.cpu_count() or 1
-    if cfg["pattern"] == "attention":
+    if cfg["pattern"] == "mla":
+        args = ["attention", str(cfg["Skv"]), "512", "100000000", str(threads), "1"]
+        sample = (f"rows = (b, head) cascades of kv={cfg['Skv']}, V width 512 (the reference's "
+                  f"attention cascade; its P row is a 512-wide dot, the 64 rope columns not counted)")
+    elif cfg["pattern"] == "attention":
         segs = cfg.get("segments", 1) if cfg["Sq"] == 1 else 1
         args = ["attention", str(cfg["Skv"]), str(cfg["D"]), "100000000", str(threads), str(segs)]
         sample = f"rows = (b,h,query) cascades of kv={cfg['Skv']}, hd={cfg['D']}"
@@ -224,7 +237,19 @@ class Workload:
         rnd = lambda *shape: torch.rand(*shape, device=dev, generator=g)  # noqa: E731
         self.cfg = cfg
         pat = cfg["pattern"]
-        if pat == "attention":
+        if pat == "mla":
+            B, S = cfg["B"], cfg["Skv"]
+            q = (rnd(B, 128, 576) * 2 - 1).bfloat16()
+            kv = (rnd(B, S, 576) * 2 - 1).bfloat16()
+            self.plan = Plan(Desc(N.RF_PATTERN_MLA_DECODE, "bf16", rows=1, len=S, free_len=512, batch=B,
+                                  heads=128, segments=cfg.get("segments", 1), softmax_scale=576 ** -0.5,
+                                  producer_len=576, device=dev.index))
+            self.inputs = [q, kv]
+            m = torch.empty(B, 128, device=dev)
+            self.outputs = [m, torch.empty_like(m), torch.empty(B, 128, 512, dtype=torch.bfloat16, device=dev)]
+            self.step_inputs = [0, 1]
+            self.data = "synthetic (q, cache ~ U(-1,1) bf16; cache rows [c_kv 512 | k_rope 64])"
+        elif pat == "attention":
             dt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
             B, H, Sq, Skv, D = cfg["B"], cfg["H"], cfg["Sq"], cfg["Skv"], cfg["D"]
             q = ((rnd(B, H, Sq, D) * 2 - 1) / D ** 0.5).to(dt)
@@ -446,7 +471,7 @@ def run_ours(args, cfg):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": {"quant": "e4m3 (bf16 in)", "rms": "bf16", "ln": "bf16", "router": "bf16"}.get(cfg["pattern"], cfg["dtype"]),
+        "dtype": {"quant": "e4m3 (bf16 in)", "rms": "bf16", "ln": "bf16", "router": "bf16", "mla": "bf16"}.get(cfg["pattern"], cfg["dtype"]),
         "data": wl.data,
         "config": conf,
         "roofline": {"bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 1),
@@ -504,6 +529,7 @@ def run_reference(args, cfg):
             "rms": "the reference's DSL input generator for the RMSNorm->GEMM cascade",
             "ln": "the reference's DSL input generator for the LayerNorm->GEMM cascade",
             "router": "x, w ~ U(-1,1); scores through make_moe_routing's cascade",
+            "mla": "the reference's own make_attention generator at hd 512",
         }[cfg["pattern"]] + ")",
         "config": {"workload": cfg["name"]},
         "cpu_baseline": cb,

@@ -92,7 +92,12 @@ typedef enum rf_pattern {
    * cascade input) feeding the MOE_ROUTING cascade: d1 = max s, d2 = sum exp(s - d1),
    * d3 = top-K' of s, ties to the lowest index. len = experts (32/64/128/256),
    * free_len = K' <= 8, producer_len = hd (the GEMM's reduce axis, % 64)      */
-  RF_PATTERN_MOE_ROUTER = 10
+  RF_PATTERN_MOE_ROUTER = 10,
+  /* MLA decode (absorbed multi-latent attention, the paper's L1-L9):
+   * the ATTENTION cascade with P = scale q K^T over cache rows K = [c_kv | k_rope]
+   * (producer_len = 576 wide) and V = c_kv (their first free_len = 512 columns);
+   * heads = 128 queries per batch share the cache, rows = 1, len = Skv      */
+  RF_PATTERN_MLA_DECODE = 11
 } rf_pattern;
 
 typedef enum rf_dtype { RF_F32 = 0, RF_BF16 = 1, RF_E4M3 = 2 } rf_dtype;
@@ -116,7 +121,8 @@ typedef struct rf_desc {
   int32_t tile_rows;    /* 0 = kernel default (reference pick_tile: 128) */
   int32_t tile_stream;  /* 0 = kernel default */
   int32_t device;       /* CUDA ordinal the plan is bound to */
-  int32_t producer_len; /* MOE_ROUTER: hd, the reduce axis of the producer GEMM (ABI v3;
+  int32_t producer_len; /* MOE_ROUTER: hd, the reduce axis of the producer GEMM;
+                           MLA_DECODE: the q / cache row width (576) (ABI v3;
                            was `reserved` in v2, same offset) */
 } rf_desc;
 
@@ -138,6 +144,8 @@ typedef struct rf_desc {
  *   MOE_ROUTER     in[0] = X [rows, hd] bf16, in[1] = packed W (rf_pack_weight: w [hd, en]
  *                  f32 -> bf16 [en, hd]); d1, d2, d3 as MOE_ROUTING; d4 = the scores s
  *                  [rows, en] f32 (optional: may be null)
+ *   MLA_DECODE     in[0] = q [B, 128, 576] bf16, in[1] = cache [B, Skv, 576] bf16;
+ *                  d1 = m [B, 128] f32, d2 = l f32, d3 = O [B, 128, 512] bf16
  *   VARIANCE       in[0] = x [rows, len] f32; d1, d2 [rows] f32
  *   SUM_SUM        in[0] = x1, in[1] = x2 [rows, len] f32; d1, d2 [rows] f32
  *   MOMENTS        in[0] = mass [rows, len] f32, in[1] = pos [rows, len, free_len] f32;

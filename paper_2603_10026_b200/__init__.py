@@ -17,6 +17,7 @@ from .executors import (  # noqa: F401
     attention,
     layernorm_gemm,
     layernorm_gemm_plan,
+    mla_decode,
     moe_router,
     moe_router_plan,
     moe_routing,
@@ -39,6 +40,7 @@ __all__ = [
     "layernorm_gemm",
     "moe_routing",
     "moe_router",
+    "mla_decode",
     "variance",
     "sum_sum",
     "moments",

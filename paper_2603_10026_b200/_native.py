@@ -34,6 +34,7 @@ RF_PATTERN_VARIANCE = 7
 RF_PATTERN_SUM_SUM = 8
 RF_PATTERN_MOMENTS = 9
 RF_PATTERN_MOE_ROUTER = 10
+RF_PATTERN_MLA_DECODE = 11
 
 ABI_VERSION = 3
 

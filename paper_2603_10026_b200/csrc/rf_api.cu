@@ -113,6 +113,12 @@ void io_sizes(const rf_plan* p, size_t in[4], size_t out[4]) {
       out[0] = out[1] = sizeof(float) * d.rows;
       out[2] = 8 * d.rows * d.free_len;
       break;
+    case RF_PATTERN_MLA_DECODE:
+      in[0] = 2 * d.batch * d.heads * d.producer_len;
+      in[1] = 2 * d.batch * d.len * d.producer_len;
+      out[0] = out[1] = sizeof(float) * d.batch * d.heads;
+      out[2] = 2 * d.batch * d.heads * d.free_len;
+      break;
     case RF_PATTERN_MOE_ROUTER:
       in[0] = 2 * d.rows * d.producer_len;
       out[0] = out[1] = sizeof(float) * d.rows;
@@ -149,6 +155,7 @@ const char* kernel_name(rf::Kernel k) {
     case rf::Kernel::LayerNormGemmSm100: return "layernorm_gemm_sm100 (bf16 tcgen05 cta_group::2)";
     case rf::Kernel::RowStats: return "rowstats (SIMT HBM streaming, fp64 accumulation)";
     case rf::Kernel::MoeRouter: return "moe_router (tcgen05 split-K router GEMM + routing cascade)";
+    case rf::Kernel::MlaDecode: return "mla_decode (tcgen05, 128 heads x latent cache, split-KV)";
   }
   return "?";
 }
@@ -257,6 +264,34 @@ rf_status run_range(const rf_plan* p, const rf_io* io, int64_t u0, int64_t nu, c
       if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("moe launch: ") + cudaGetErrorString(e));
       return RF_OK;
     }
+    case RF_PATTERN_MLA_DECODE: {
+      const rf_desc& d = p->d;
+      const int64_t hn = d.heads;
+      rf::MlaArgs a{};
+      a.q = static_cast<const char*>(io->in[0]) + 2 * u0 * hn * d.producer_len;
+      a.kv = static_cast<const char*>(io->in[1]) + 2 * u0 * d.len * d.producer_len;
+      a.o = static_cast<char*>(io->d[2]) + 2 * u0 * hn * d.free_len;
+      a.m = static_cast<float*>(io->d[0]) + u0 * hn;
+      a.l = static_cast<float*>(io->d[1]) + u0 * hn;
+      a.bs = nu;
+      a.skv = d.len;
+      a.nslices = p->nsplit;
+      a.rows_total = p->rows_total;
+      a.scale = static_cast<float>(d.softmax_scale);
+      if (p->nsplit > 1) {
+        a.part_m = p->ws_m + u0 * hn;
+        a.part_l = p->ws_l + u0 * hn;
+        a.part_o = p->ws_o + u0 * hn * d.free_len;
+      }
+      cudaError_t e = rf::launch_mla_decode(a, st);
+      if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("mla launch: ") + cudaGetErrorString(e));
+      if (p->nsplit > 1) {
+        e = rf::launch_attention_merge(a.part_m, a.part_l, a.part_o, p->nsplit, nu * hn, p->rows_total,
+                                       d.free_len, a.m, a.l, a.o, RF_BF16, st);
+        if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("merge launch: ") + cudaGetErrorString(e));
+      }
+      return RF_OK;
+    }
     case RF_PATTERN_MOE_ROUTER: {
       const rf_desc& d = p->d;
       rf::RouterArgs r{};
@@ -305,6 +340,7 @@ rf_status run_range(const rf_plan* p, const rf_io* io, int64_t u0, int64_t nu, c
 
 // Independent units for chunking: (b,h) pairs for attention, rows otherwise.
 int64_t units_of(const rf_plan* p) {
+  if (p->d.pattern == RF_PATTERN_MLA_DECODE) return p->d.batch;  // heads share the batch's cache
   return p->d.pattern == RF_PATTERN_ATTENTION ? p->d.batch * p->d.heads : p->d.rows;
 }
 
@@ -430,6 +466,16 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
       p->kernel = rf::Kernel::MoeRouting;
       p->rows_total = d.rows;
       break;
+    case RF_PATTERN_MLA_DECODE:
+      if (d.dtype != RF_BF16) return bail(RF_ERR_UNSUPPORTED, "mla_decode: bf16 q / cache");
+      if (d.rows != 1) return bail(RF_ERR_SHAPE, "mla_decode: one query per head (rows = 1)");
+      if (!rf::mla_supports(d.heads, d.len, d.free_len, d.producer_len, d.segments))
+        return bail(RF_ERR_UNSUPPORTED,
+                    "mla_decode: heads 128, free_len 512, producer_len 576, (Skv / segments) % 32 == 0");
+      p->kernel = rf::Kernel::MlaDecode;
+      p->rows_total = d.batch * d.heads;
+      p->nsplit = rf::mla_pick_splits(d.batch, d.len, d.segments);
+      break;
     case RF_PATTERN_MOE_ROUTER:
       if (d.dtype != RF_BF16) return bail(RF_ERR_UNSUPPORTED, "moe_router: bf16 activations");
       if (!rf::router_supports(d.rows, d.producer_len, d.len, d.free_len))
@@ -454,14 +500,15 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
     default:
       return bail(RF_ERR_UNSUPPORTED, "unknown pattern");
   }
-  p->launches = ((p->d.pattern == RF_PATTERN_ATTENTION && p->nsplit > 1) ||
+  p->launches = (((p->d.pattern == RF_PATTERN_ATTENTION || p->d.pattern == RF_PATTERN_MLA_DECODE) &&
+                  p->nsplit > 1) ||
                  p->d.pattern == RF_PATTERN_MOE_ROUTER) ? 2 : 1;
 
   // ---- persistent workspace ----
   if (cudaMalloc(&p->domain_flag, sizeof(int)) != cudaSuccess ||
       cudaMemset(p->domain_flag, 0, sizeof(int)) != cudaSuccess)
     return bail(RF_ERR_CUDA, "workspace allocation failed");
-  if (p->d.pattern == RF_PATTERN_ATTENTION && p->nsplit > 1) {
+  if ((p->d.pattern == RF_PATTERN_ATTENTION || p->d.pattern == RF_PATTERN_MLA_DECODE) && p->nsplit > 1) {
     const size_t n = static_cast<size_t>(p->nsplit) * p->rows_total;
     if (cudaMalloc(&p->ws_m, n * sizeof(float)) != cudaSuccess ||
         cudaMalloc(&p->ws_l, n * sizeof(float)) != cudaSuccess ||

@@ -35,6 +35,7 @@ enum class Kernel {
   LayerNormGemmSm100, // gemm_sm100.cu (bf16, 2-SM; variance cascade + GEMM)
   RowStats,           // rowstats.cu (variance / sum_sum / moments: HBM streaming)
   MoeRouter,          // router.cu (tcgen05 split-K router GEMM + routing cascade)
+  MlaDecode,          // mla.cu (tcgen05 MLA decode, 128 heads share the latent cache)
 };
 
 // MoE router (router.cu): scores = X W^T-packed, then the routing cascade.
@@ -50,6 +51,23 @@ struct RouterArgs {
   float* scores;        // [rows, experts] f32 or null
 };
 cudaError_t launch_router(const RouterArgs& a, cudaStream_t st);
+
+// MLA decode (mla.cu): 128 heads, cache rows [c_kv 512 | k_rope 64].
+struct MlaArgs {
+  const void* q;    // [bs, 128, 576] bf16
+  const void* kv;   // [bs, skv, 576] bf16 (K = whole row, V = first 512)
+  void* o;          // [bs, 128, 512] bf16 (nslices == 1)
+  float* m;
+  float* l;
+  float* part_m;    // [nslices, rows_total] (nslices > 1)
+  float* part_l;
+  float* part_o;    // [nslices, rows_total, 512]
+  int64_t bs, skv, nslices, rows_total;
+  float scale;
+};
+cudaError_t launch_mla_decode(const MlaArgs& a, cudaStream_t st);
+bool mla_supports(int64_t heads, int64_t skv, int64_t dv, int64_t dqk, int64_t segments);
+int64_t mla_pick_splits(int64_t bs, int64_t skv, int64_t segments);
 bool router_supports(int64_t rows, int64_t hd, int64_t experts, int64_t k);
 int64_t router_pick_splits(int64_t rows, int64_t hd);
 

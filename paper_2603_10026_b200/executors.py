@@ -352,6 +352,28 @@ def moe_router(x, w_packed, k: int, with_scores: bool = False, stream=None):
     return out + (sc,) if with_scores else out
 
 
+def mla_decode(q, cache, segments: int = 1, softmax_scale: float = 1.0, stream=None):
+    """MLA decode (absorbed multi-latent attention): the attention cascade with
+    P = scale * q . cache^T over the 576-wide cache rows [c_kv | k_rope] and
+    V = c_kv (their first 512 columns). q: [B, 128, 576] bf16, cache:
+    [B, Skv, 576] bf16. Returns (m [B,128], l [B,128], O [B,128,512] bf16)."""
+    import torch
+
+    _require(q.dim() == 3 and cache.dim() == 3 and q.dtype == cache.dtype == torch.bfloat16,
+             "q [B,128,576] and cache [B,Skv,576] must be bfloat16")
+    B, hn, dqk = q.shape
+    _require(cache.shape[0] == B and cache.shape[2] == dqk, "cache must be [B, Skv, q.shape[2]]")
+    skv = cache.shape[1]
+    p = plan(Desc(N.RF_PATTERN_MLA_DECODE, "bf16", rows=1, len=skv, free_len=512, batch=B, heads=hn,
+                  segments=segments, softmax_scale=softmax_scale, producer_len=dqk,
+                  device=q.device.index or 0))
+    m = torch.empty(B, hn, dtype=torch.float32, device=q.device)
+    l = torch.empty_like(m)
+    o = torch.empty(B, hn, 512, dtype=torch.bfloat16, device=q.device)
+    p.run([q.contiguous(), cache.contiguous()], [m, l, o], stream)
+    return m, l, o
+
+
 def _rows_f32(name, *ts):
     import torch
 

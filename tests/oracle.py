@@ -100,6 +100,20 @@ def attention(q, k, v, scale=1.0):
     return m, l, o
 
 
+def attention_closed_form(p, v):
+    """The attention cascade's oracle lambda (make_attention, workloads.cpp:101-118)
+    on precomputed scores: p [rows, kv], v [rows or 1, kv, Dv] -> m, l [rows],
+    o [rows, Dv]: m = max p, l = sum e^(p-m), o = sum e^(p-m)/l v. numpy fp64;
+    pinned against the C oracle by tests/test_oracle_golden.py. Lets K and V
+    differ in width (MLA: K = [c_kv | k_rope] 576 wide, V = c_kv 512 wide)."""
+    p = np.asarray(p, dtype=np.float64)
+    m = p.max(axis=1)
+    e = np.exp(p - m[:, None])
+    l = e.sum(axis=1)
+    o = np.einsum("rk,rkd->rd", e, np.broadcast_to(v, (p.shape[0],) + v.shape[1:])) / l[:, None]
+    return m, l, o
+
+
 def attention_incremental(p, v, segments=1):
     """p [rows, kv], v [rows, kv, D] -> m, l, o (run_incremental/multisegment semantics)."""
     p, v = _f64(p), _f64(v)

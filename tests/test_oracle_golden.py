@@ -35,6 +35,18 @@ def test_attention_oracle_and_streaming_match_reference(name):
             assert _err(os_.ravel(), g[f"multi{s}.d3"]) < TOL
 
 
+@pytest.mark.parametrize("name", O.golden_names("attention_"))
+def test_attention_closed_form_matches_reference(name):
+    """The numpy closed form used for MLA (K and V of different widths)."""
+    g = O.load_golden(name)
+    p, v = g["in.P"], g["in.V"]
+    kv, hd = v.shape
+    m, l, o = O.attention_closed_form(p.reshape(1, kv), v.reshape(1, kv, hd))
+    assert _err(m, g["oracle.d1"]) < TOL
+    assert _err(l, g["oracle.d2"]) < TOL
+    assert _err(o.ravel(), g["oracle.d3"]) < TOL
+
+
 def test_attention_incremental_rejects_bad_segmentation():
     p = np.zeros((1, 6))
     v = np.zeros((1, 6, 2))
