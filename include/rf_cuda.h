@@ -22,8 +22,10 @@
  *  - Plain C types only; device pointers are `void*`, streams are the CUDA
  *    runtime handle passed as `void*` (cudaStream_t), 0 = legacy default.
  *  - Every call is stream-ordered and non-blocking unless it says otherwise.
- *    Plans are immutable after creation and safe to use from several host
- *    threads on different streams (one plan per device).
+ *    Plans are immutable after creation (one plan per device). A plan owns its
+ *    split workspace and host-path staging, so rf_run / rf_run_host calls on
+ *    ONE plan must be ordered (same stream or events); use one plan per
+ *    stream for concurrent execution.
  *  - No exceptions cross the boundary. Errors are rf_status codes that the
  *    host layer maps back onto the reference's exception types:
  *      RF_ERR_SHAPE        -> redfuse::ShapeMismatch          (simulator.hpp:17-19)
