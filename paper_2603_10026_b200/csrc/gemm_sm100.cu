@@ -782,9 +782,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
         }
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(&s.abf_empty[sa]);
-      uint32_t mx = qnt::absmax_bf16x2(x[0], x[1]);
+      // tile absmax: 8 independent chains, then a 3-level tree (the quantiser
+      // is on the MMA's critical path: a 63-long dependent chain costs ~300 cycles)
+      uint32_t mc[8];
 #pragma unroll
-      for (int i = 2; i < 64; ++i) mx = qnt::absmax_bf16x2(mx, x[i]);
+      for (int i = 0; i < 8; ++i) mc[i] = qnt::absmax_bf16x2(x[i], x[i + 8]);
+#pragma unroll
+      for (int i = 16; i < 64; ++i) mc[i & 7] = qnt::absmax_bf16x2(mc[i & 7], x[i]);
+#pragma unroll
+      for (int w = 4; w > 0; w >>= 1)
+#pragma unroll
+        for (int i = 0; i < w; ++i) mc[i] = qnt::absmax_bf16x2(mc[i], mc[i + w]);
+      const uint32_t mx = mc[0];
       const float tile_max = fmaxf(__uint_as_float((mx << 16) & 0x7fffffffu),
                                    __uint_as_float(mx & 0x7fff0000u));
       amax = fmaxf(amax, tile_max);
