@@ -226,19 +226,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_wait(&s.s_full[k], i & 1);
       tc_fence_after();
       if ((threadIdx.x & 127) == 0) RF_TRACE(512 * k + 4 * i + 0);
-      uint32_t sr[4][32];
+      float tmax;
+      {
+        // pass 1 (reduction 1): d1 = max(d1, max_tile) over the 4 chunks in flight
+        uint32_t sr[4][32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(tSk + c * 32, sr[c]);
-      tmem_ld_wait();
-#define SV(j) __uint_as_float(sr[(j) >> 5][(j) & 31])
-      // reduction 1: d1 = max(d1, max_tile)   (8 independent chains)
-      float mx[8];
+        for (int c = 0; c < 4; ++c) tmem_ld32(tSk + c * 32, sr[c]);
+        tmem_ld_wait();
+        float mx[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) mx[j] = SV(j);
+        for (int j = 0; j < 8; ++j) mx[j] = __uint_as_float(sr[0][j]);
 #pragma unroll
-      for (int j = 8; j < BN; ++j) mx[j & 7] = fmaxf(mx[j & 7], SV(j));
-      const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        for (int j = 8; j < BN; ++j) mx[j & 7] = fmaxf(mx[j & 7], __uint_as_float(sr[j >> 5][j & 31]));
+        tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                     fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      }
       if ((threadIdx.x & 127) == 0) RF_TRACE(512 * k + 4 * i + 3);
       m_true = fmaxf(m_true, tmax * p.scale);
       // correction exp(d1' - d1): lazily re-base the accumulators
@@ -249,17 +251,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         l *= alpha;
         m_ref = m_true;
       }
-      // reductions 2 and 3: P = exp(S - d1) in bf16 into TMEM, row sum in fp32.
-      // Pairs in packed f32x2; one pair in four on the FMA pipe (MUFU offload).
+      // pass 2 (reductions 2 and 3): S re-read from TMEM one 32-column chunk
+      // at a time (chunk c + 1 in flight while c is exponentiated; P chunk c
+      // lands in columns [16c, 16c + 16), never ahead of an unread S chunk),
+      // so only 64 S registers are live. P = exp(S - d1) in bf16 into TMEM,
+      // row sum in fp32; pairs packed f32x2, one pair in four on the FMA pipe.
       const uint64_t c12 = f2(c1, c1), nmb2 = f2(-m_ref * kLog2e, -m_ref * kLog2e);
       uint64_t acc2[4] = {0, 0, 0, 0};
+      uint32_t sr[2][32];
+      tmem_ld32(tSk, sr[0]);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {  // per 32-column chunk: its S registers die here
+      for (int c = 0; c < 4; ++c) {
+        tmem_ld_wait();
+        if (c + 1 < 4) tmem_ld32(tSk + (c + 1) * 32, sr[(c + 1) & 1]);
         uint32_t pk[16];
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
-          const int c0 = 32 * c + 2 * jj;
-          const uint64_t x2 = ffma2(f2(SV(c0), SV(c0 + 1)), c12, nmb2);
+          const uint64_t x2 = ffma2(f2(__uint_as_float(sr[c & 1][2 * jj]), __uint_as_float(sr[c & 1][2 * jj + 1])),
+                                    c12, nmb2);
           uint64_t p2;
           if (kPolyPairs(jj)) {
             p2 = ex2_poly2(x2);
@@ -279,7 +288,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       float rs0, rs1;
       f2split(s01, rs0, rs1);
       const float rs = rs0 + rs1;
-#undef SV
       l += rs;
       if (i > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll
