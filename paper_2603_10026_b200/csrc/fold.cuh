@@ -6,10 +6,10 @@
 // Partials are normalised by their own l (paper form). Like the reference's
 // tile combine (proj/src/tile_ir.cpp:706-712) the raw partial l_s is read
 // before any rescale (no in-place double count, PAPER.md:1953-1958 caveat).
-// Untouched (empty) slices have l_s = 0 and drop out. Sums run in slice order,
-// with up to 8 slices' loads in flight per round. Partials are read with
-// ld.global.cg (L2), so a CTA may fold slices other CTAs of the same launch
-// just wrote (attn_f32.cu's last-CTA fold).
+// Untouched (empty) slices have l_s = 0 and drop out. Sums run in slice order;
+// up to 16 slices fold in two dependent rounds of loads (all (m, l), then all
+// O rows); more slices fold 16 at a time, re-basing the running sums.
+// Partials are read with ld.global.cg (L2).
 #pragma once
 
 #include <cuda_bf16.h>
@@ -21,27 +21,41 @@ template <typename TO>
 __device__ __forceinline__ void fold_chunk(const float* pm, const float* pl, const float* po,
                                            int64_t nslices, int64_t stride, int64_t d, int64_t row,
                                            int64_t c4, float* m_out, float* l_out, TO* o_out) {
-  constexpr int R = 8;  // slices in flight per round
-  float m = -INFINITY;
-  for (int64_t s0 = 0; s0 < nslices; s0 += R) {
-    float ms[R];
-#pragma unroll
-    for (int j = 0; j < R; ++j) ms[j] = s0 + j < nslices ? __ldcg(pm + (s0 + j) * stride + row) : -INFINITY;
-#pragma unroll
-    for (int j = 0; j < R; ++j) m = fmaxf(m, ms[j]);
-  }
+  constexpr int R = 16;  // slices per round: <= 16 slices fold in 2 dependent round trips
   float l = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float m = -INFINITY;
   for (int64_t s0 = 0; s0 < nslices; s0 += R) {
+    // round 1: every slice's (m, l) of this round; the running max is
+    // re-based like a two-level fold when there is more than one round
     float ms[R], ls[R];
-    float4 os[R];
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       const bool ok = s0 + j < nslices;
       const int64_t ix = (s0 + j) * stride + row;
-      ms[j] = ok ? __ldcg(pm + ix) : 0.f;
+      ms[j] = ok ? __ldcg(pm + ix) : -INFINITY;
       ls[j] = ok ? __ldcg(pl + ix) : 0.f;
-      os[j] = ok ? __ldcg(reinterpret_cast<const float4*>(po + ix * d) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float mr = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < R; ++j) mr = fmaxf(mr, ms[j]);
+    const float mn = fmaxf(m, mr);
+    if (s0 > 0 && mn != m) {  // later rounds: re-base what is accumulated (exp(m - mn) <= 1)
+      const float f = l != 0.f ? __expf(m - mn) : 0.f;
+      l *= f;
+      acc.x *= f;
+      acc.y *= f;
+      acc.z *= f;
+      acc.w *= f;
+    }
+    m = mn;
+    // round 2: the O rows of this round, all in flight
+    float4 os[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const bool ok = s0 + j < nslices && ls[j] != 0.f;
+      os[j] = ok ? __ldcg(reinterpret_cast<const float4*>(po + ((s0 + j) * stride + row) * d) + c4)
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int j = 0; j < R; ++j) {

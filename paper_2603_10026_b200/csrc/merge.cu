@@ -13,7 +13,7 @@ namespace rf {
 namespace {
 
 template <typename TO>
-__global__ void __launch_bounds__(256) merge_kernel(const float* __restrict__ pm, const float* __restrict__ pl,
+__global__ void __launch_bounds__(128) merge_kernel(const float* __restrict__ pm, const float* __restrict__ pl,
                                                     const float* __restrict__ po, int64_t nslices, int64_t rows,
                                                     int64_t stride, int64_t d, float* __restrict__ m_out,
                                                     float* __restrict__ l_out, TO* __restrict__ o_out) {
@@ -39,8 +39,8 @@ cudaError_t launch_attention_merge(const float* pm, const float* pl, const float
   // kernel drains (its launch latency overlaps that kernel's tail);
   // griddepcontrol.wait in the kernel orders the partial reads.
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>((threads + 255) / 256));
-  cfg.blockDim = dim3(256);
+  cfg.gridDim = dim3(static_cast<unsigned>((threads + 127) / 128));
+  cfg.blockDim = dim3(128);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
