@@ -16,7 +16,8 @@
 //     applied once at finalize (finalize_root, simulator.cpp:611-621,
 //     retargets the root's scaling the same way).
 //
-// CTA = 2 Q tiles x 128 rows (ping-pong), KV tiles of 128 keys.
+// CTA = 2 Q tiles x 128 rows (ping-pong), KV tiles of 128 keys; persistent
+// (one CTA per SM walks the work units, see attn_sm100_kernel).
 // Warp roles (320 threads, ~200 registers per thread):
 //   warps 0-3  softmax + correction + epilogue for Q tile 0 (thread = row)
 //   warps 4-7  the same for Q tile 1
@@ -66,9 +67,9 @@ struct Smem {
   static constexpr int kChunks = D / 64;    // 128 B swizzle chunks along D
   uint8_t q[2][kTile];
   uint8_t kv[NSLOT][kTile];
-  uint64_t bar_q;
+  uint64_t q_full, q_empty;
   uint64_t kv_full[NSLOT], kv_empty[NSLOT];
-  uint64_t s_full[2], p_full[2], pv_done[2];
+  uint64_t s_full[2], p_full[2], pv_done[2], o_empty[2];
   uint32_t tmem_base;
 };
 
@@ -82,8 +83,15 @@ struct Params {
   float* part_m;
   float* part_l;
   float* part_o;
+  int units_x, units_bh, units;  // work units: (Q tile pair, b*h, slice)
 };
 
+// Persistent: one CTA per SM walks the work units u = blockIdx.x,
+// blockIdx.x + gridDim.x, ... (unit = 2 Q tiles of one (b,h) and one KV
+// slice). Barrier phases run on across units; the Q of unit u+1 is loaded as
+// soon as the last S MMA of unit u has retired, and the epilogue of unit u
+// (TMEM O -> global) overlaps the first S MMAs of unit u+1 (O_k is only
+// overwritten by P V_k of the next unit after the epilogue released it).
 template <int D>
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_sm100_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -92,22 +100,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   Smem<D>& s = *reinterpret_cast<Smem<D>*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = warp_id();
-  const int bh = blockIdx.y;
-  const int64_t q_row0 = static_cast<int64_t>(blockIdx.x) * 2 * BM;  // within (b,h)
-  const int64_t slice = p.slice_begin + blockIdx.z;
-  const int64_t kv0 = slice * p.slice_len;
   const int n_tiles = static_cast<int>(p.slice_len / BN);
+  auto unit_of = [&](int u, int& bh, int64_t& q_row0, int64_t& slice) {
+    const int x = u % p.units_x;
+    const int r = u / p.units_x;
+    bh = r % p.units_bh;
+    slice = p.slice_begin + r / p.units_bh;
+    q_row0 = static_cast<int64_t>(x) * 2 * BM;
+  };
 
   if (threadIdx.x == 0) {
-    mbar_init(&s.bar_q, 1);
+    mbar_init(&s.q_full, 1);
+    mbar_init(&s.q_empty, 1);
     for (int i = 0; i < NSLOT; ++i) {
       mbar_init(&s.kv_full[i], 1);
       mbar_init(&s.kv_empty[i], 1);
     }
     for (int k = 0; k < 2; ++k) {
       mbar_init(&s.s_full[k], 1);
-      mbar_init(&s.p_full[k], 4);  // one arrival per softmax warp
+      mbar_init(&s.p_full[k], 4);   // one arrival per softmax warp
       mbar_init(&s.pv_done[k], 1);
+      mbar_init(&s.o_empty[k], 4);  // the tile's softmax warps have read O_k
     }
     fence_barrier_init();
   }
@@ -123,22 +136,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       prefetch_tmap(&tq);
       prefetch_tmap(&tk);
       prefetch_tmap(&tv);
-      const int32_t qy = static_cast<int32_t>(bh * p.sq + q_row0);
-      mbar_arrive_expect_tx(&s.bar_q, 2 * Smem<D>::kTile);
-      for (int k = 0; k < 2; ++k)
-        for (int c = 0; c < Smem<D>::kChunks; ++c)
-          tma_load_2d(s.q[k] + c * BM * 128, &tq, &s.bar_q, c * 64, qy + k * BM, kEvictFirst);
-      const int32_t ky = static_cast<int32_t>(bh * p.skv + kv0);
-      for (int t = 0; t < 2 * n_tiles; ++t) {
-        const int slot = t % NSLOT;
-        const uint32_t ph = (t / NSLOT) & 1;
-        mbar_wait(&s.kv_empty[slot], ph ^ 1);
-        RF_TRACE(1536 + t);
-        mbar_arrive_expect_tx(&s.kv_full[slot], Smem<D>::kTile);
-        const CUtensorMap* m = (t & 1) ? &tv : &tk;
-        const int32_t y = ky + (t >> 1) * BN;
-        for (int c = 0; c < Smem<D>::kChunks; ++c)
-          tma_load_2d(s.kv[slot] + c * BN * 128, m, &s.kv_full[slot], c * 64, y, kEvictLast);
+      int t = 0;  // K/V item counter across units
+      int uc = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++uc) {
+        int bh;
+        int64_t q_row0, slice;
+        unit_of(u, bh, q_row0, slice);
+        mbar_wait(&s.q_empty, (uc & 1) ^ 1);
+        const int32_t qy = static_cast<int32_t>(bh * p.sq + q_row0);
+        mbar_arrive_expect_tx(&s.q_full, 2 * Smem<D>::kTile);
+        for (int k = 0; k < 2; ++k)
+          for (int c = 0; c < Smem<D>::kChunks; ++c)
+            tma_load_2d(s.q[k] + c * BM * 128, &tq, &s.q_full, c * 64, qy + k * BM, kEvictFirst);
+        const int32_t ky = static_cast<int32_t>(bh * p.skv + slice * p.slice_len);
+        for (int j = 0; j < 2 * n_tiles; ++j, ++t) {
+          const int slot = t % NSLOT;
+          mbar_wait(&s.kv_empty[slot], ((t / NSLOT) & 1) ^ 1);
+          RF_TRACE(1536 + (t & 511));
+          mbar_arrive_expect_tx(&s.kv_full[slot], Smem<D>::kTile);
+          const CUtensorMap* m = (j & 1) ? &tv : &tk;
+          const int32_t y = ky + (j >> 1) * BN;
+          for (int c = 0; c < Smem<D>::kChunks; ++c)
+            tma_load_2d(s.kv[slot] + c * BN * 128, m, &s.kv_full[slot], c * 64, y, kEvictLast);
+        }
       }
     }
   } else if (warp == 9) {
@@ -172,43 +192,47 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       __syncwarp();
     };
-    auto release = [&](int slot) {
-      if (leader) mma_commit(&s.kv_empty[slot]);
+    auto commit_to = [&](uint64_t* bar) {
+      if (leader) mma_commit(bar);
       __syncwarp();
     };
-    mbar_wait(&s.bar_q, 0);
-    mbar_wait(&s.kv_full[0], 0);
-    tc_fence_after();
-    issue_s(0, 0);
-    issue_s(1, 0);
-    release(0);
-    for (int i = 0; i < n_tiles; ++i) {
-      const int tV = 2 * i + 1, tK = 2 * i + 2;
-      const int sV = tV % NSLOT, sK = tK % NSLOT;
-      const uint32_t phV = (tV / NSLOT) & 1, phK = (tK / NSLOT) & 1;
-      const uint32_t ph = i & 1;
-      const bool last = i + 1 == n_tiles;
-      mbar_wait(&s.kv_full[sV], phV);
-      // tile 0: PV0_i then S0_{i+1}
-      mbar_wait(&s.p_full[0], ph);
+    auto wait_kv = [&](int t) {
+      mbar_wait(&s.kv_full[t % NSLOT], (t / NSLOT) & 1);
       tc_fence_after();
-      if (leader) RF_TRACE(1024 + 4 * i + 0);
-      issue_pv(0, sV, i > 0, last);
-      if (!last) {
-        mbar_wait(&s.kv_full[sK], phK);
-        tc_fence_after();
-        if (leader) RF_TRACE(1024 + 4 * i + 1);
-        issue_s(0, sK);
-      }
-      // tile 1: PV1_i then S1_{i+1}
-      mbar_wait(&s.p_full[1], ph);
+    };
+    int t = 0;   // K/V item counter across units
+    int g = 0;   // tile counter across units (s_full / p_full phases)
+    int uc = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++uc) {
+      mbar_wait(&s.q_full, uc & 1);
+      wait_kv(t);
       tc_fence_after();
-      if (leader) RF_TRACE(1024 + 4 * i + 2);
-      issue_pv(1, sV, i > 0, last);
-      release(sV);
-      if (!last) {
-        issue_s(1, sK);
-        release(sK);
+      if (leader && uc == 0) RF_TRACE(1024 + 0);
+      issue_s(0, t % NSLOT);
+      issue_s(1, t % NSLOT);
+      if (n_tiles == 1) commit_to(&s.q_empty);  // last S of the unit
+      commit_to(&s.kv_empty[t % NSLOT]);
+      ++t;
+      for (int i = 0; i < n_tiles; ++i, ++g) {
+        const int tV = t, tK = t + 1;
+        const uint32_t ph = g & 1;
+        const bool last = i + 1 == n_tiles;
+        wait_kv(tV);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          mbar_wait(&s.p_full[k], ph);
+          if (i == 0 && uc > 0) mbar_wait(&s.o_empty[k], (uc - 1) & 1);  // previous unit's O_k read
+          tc_fence_after();
+          issue_pv(k, tV % NSLOT, i > 0, last);
+          if (!last) {
+            if (k == 0) wait_kv(tK);
+            issue_s(k, tK % NSLOT);
+            if (k == 1 && i + 2 == n_tiles) commit_to(&s.q_empty);  // last S of the unit
+          }
+        }
+        commit_to(&s.kv_empty[tV % NSLOT]);
+        if (!last) commit_to(&s.kv_empty[tK % NSLOT]);
+        t += last ? 1 : 2;
       }
     }
   } else {
@@ -219,130 +243,142 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t tSk = tmem + k * 128 + lane_off;
     const uint32_t tOk = tmem + 256 + k * 128 + lane_off;
     const float c1 = p.scale_log2;
-    float m_true = -INFINITY;  // d1: exact running max
-    float m_ref = -INFINITY;   // reference max of the accumulators
-    float l = 0.f;             // d2 relative to m_ref
-    for (int i = 0; i < n_tiles; ++i) {
-      mbar_wait(&s.s_full[k], i & 1);
-      tc_fence_after();
-      if ((threadIdx.x & 127) == 0) RF_TRACE(512 * k + 4 * i + 0);
-      float tmax;
-      {
-        // pass 1 (reduction 1): d1 = max(d1, max_tile) over the 4 chunks in flight
-        uint32_t sr[4][32];
+    int g = 0;  // tile counter across units
+    int uc = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++uc) {
+      int bh;
+      int64_t q_row0, slice;
+      unit_of(u, bh, q_row0, slice);
+      float m_true = -INFINITY;  // d1: exact running max
+      float m_ref = -INFINITY;   // reference max of the accumulators
+      float l = 0.f;             // d2 relative to m_ref
+      for (int i = 0; i < n_tiles; ++i, ++g) {
+        mbar_wait(&s.s_full[k], g & 1);
+        tc_fence_after();
+        if ((threadIdx.x & 127) == 0 && uc == 0) RF_TRACE(512 * k + 4 * i + 0);
+        float tmax;
+        {
+          // pass 1 (reduction 1): d1 = max(d1, max_tile) over the 4 chunks in flight
+          uint32_t sr[4][32];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32(tSk + c * 32, sr[c]);
-        tmem_ld_wait();
-        float mx[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) mx[j] = __uint_as_float(sr[0][j]);
-#pragma unroll
-        for (int j = 8; j < BN; ++j) mx[j & 7] = fmaxf(mx[j & 7], __uint_as_float(sr[j >> 5][j & 31]));
-        tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                     fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-      }
-      if ((threadIdx.x & 127) == 0) RF_TRACE(512 * k + 4 * i + 3);
-      m_true = fmaxf(m_true, tmax * p.scale);
-      // correction exp(d1' - d1): lazily re-base the accumulators
-      const bool need = (m_true - m_ref) * kLog2e > kRescaleThreshold;
-      float alpha = 1.f;
-      if (need) {
-        alpha = ex2_mufu((m_ref - m_true) * kLog2e);  // 0 on the first tile
-        l *= alpha;
-        m_ref = m_true;
-      }
-      // pass 2 (reductions 2 and 3): S re-read from TMEM one 32-column chunk
-      // at a time (chunk c + 1 in flight while c is exponentiated; P chunk c
-      // lands in columns [16c, 16c + 16), never ahead of an unread S chunk),
-      // so only 64 S registers are live. P = exp(S - d1) in bf16 into TMEM,
-      // row sum in fp32; pairs packed f32x2, one pair in four on the FMA pipe.
-      const uint64_t c12 = f2(c1, c1), nmb2 = f2(-m_ref * kLog2e, -m_ref * kLog2e);
-      uint64_t acc2[4] = {0, 0, 0, 0};
-      uint32_t sr[2][32];
-      tmem_ld32(tSk, sr[0]);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        tmem_ld_wait();
-        if (c + 1 < 4) tmem_ld32(tSk + (c + 1) * 32, sr[(c + 1) & 1]);
-        uint32_t pk[16];
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const uint64_t x2 = ffma2(f2(__uint_as_float(sr[c & 1][2 * jj]), __uint_as_float(sr[c & 1][2 * jj + 1])),
-                                    c12, nmb2);
-          uint64_t p2;
-          if (kPolyPairs(jj)) {
-            p2 = ex2_poly2(x2);
-          } else {
-            float x0, x1;
-            f2split(x2, x0, x1);
-            p2 = f2(ex2_mufu(x0), ex2_mufu(x1));
-          }
-          acc2[jj & 3] = fadd2(acc2[jj & 3], p2);
-          float p0, p1;
-          f2split(p2, p0, p1);
-          pk[jj] = pack_bf16x2(p0, p1);
-        }
-        tmem_st16(tSk + 16 * c, pk);
-      }
-      const uint64_t s01 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
-      float rs0, rs1;
-      f2split(s01, rs0, rs1);
-      const float rs = rs0 + rs1;
-      l += rs;
-      if (i > 0 && __any_sync(0xffffffffu, need)) {
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(tOk + c * 32, r);
+          for (int c = 0; c < 4; ++c) tmem_ld32(tSk + c * 32, sr[c]);
           tmem_ld_wait();
+          float mx[8];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * alpha);
-          tmem_st32(tOk + c * 32, r);
+          for (int j = 0; j < 8; ++j) mx[j] = __uint_as_float(sr[0][j]);
+#pragma unroll
+          for (int j = 8; j < BN; ++j) mx[j & 7] = fmaxf(mx[j & 7], __uint_as_float(sr[j >> 5][j & 31]));
+          tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                       fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         }
+        if ((threadIdx.x & 127) == 0 && uc == 0) RF_TRACE(512 * k + 4 * i + 3);
+        m_true = fmaxf(m_true, tmax * p.scale);
+        // correction exp(d1' - d1): lazily re-base the accumulators
+        const bool need = (m_true - m_ref) * kLog2e > kRescaleThreshold;
+        float alpha = 1.f;
+        if (need) {
+          alpha = ex2_mufu((m_ref - m_true) * kLog2e);  // 0 on the first tile
+          l *= alpha;
+          m_ref = m_true;
+        }
+        // pass 2 (reductions 2 and 3): S re-read from TMEM one 32-column chunk
+        // at a time (chunk c + 1 in flight while c is exponentiated; P chunk c
+        // lands in columns [16c, 16c + 16), never ahead of an unread S chunk).
+        // P = exp(S - d1) in bf16 into TMEM, row sum in fp32; pairs packed
+        // f32x2, one pair in four on the FMA pipe.
+        const uint64_t c12 = f2(c1, c1), nmb2 = f2(-m_ref * kLog2e, -m_ref * kLog2e);
+        uint64_t acc2[4] = {0, 0, 0, 0};
+        uint32_t sr[2][32];
+        tmem_ld32(tSk, sr[0]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          tmem_ld_wait();
+          if (c + 1 < 4) tmem_ld32(tSk + (c + 1) * 32, sr[(c + 1) & 1]);
+          uint32_t pk[16];
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const uint64_t x2 = ffma2(f2(__uint_as_float(sr[c & 1][2 * jj]), __uint_as_float(sr[c & 1][2 * jj + 1])),
+                                      c12, nmb2);
+            uint64_t p2;
+            if (kPolyPairs(jj)) {
+              p2 = ex2_poly2(x2);
+            } else {
+              float x0, x1;
+              f2split(x2, x0, x1);
+              p2 = f2(ex2_mufu(x0), ex2_mufu(x1));
+            }
+            acc2[jj & 3] = fadd2(acc2[jj & 3], p2);
+            float p0, p1;
+            f2split(p2, p0, p1);
+            pk[jj] = pack_bf16x2(p0, p1);
+          }
+          tmem_st16(tSk + 16 * c, pk);
+        }
+        const uint64_t s01 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
+        float rs0, rs1;
+        f2split(s01, rs0, rs1);
+        l += rs0 + rs1;
+        // O *= exp(d1' - d1): P V_k,i-1 has retired (S_k,i, issued after it, is complete)
+        if (i > 0 && __any_sync(0xffffffffu, need)) {
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(tOk + c * 32, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * alpha);
+            tmem_st32(tOk + c * 32, r);
+          }
+        }
+        if ((threadIdx.x & 127) == 0 && uc == 0) RF_TRACE(512 * k + 4 * i + 1);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if ((threadIdx.x & 127) == 0 && uc == 0) RF_TRACE(512 * k + 4 * i + 2);
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&s.p_full[k]);
       }
-      if ((threadIdx.x & 127) == 0) RF_TRACE(512 * k + 4 * i + 1);
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if ((threadIdx.x & 127) == 0) RF_TRACE(512 * k + 4 * i + 2);
-      if ((threadIdx.x & 31) == 0) mbar_arrive(&s.p_full[k]);
-    }
-    // ---- finalize (finalize_root): d2 re-based to the true d1, d3 = O / d2 ----
-    const float l_true = l * ex2_mufu((m_ref - m_true) * kLog2e);
-    const int64_t grow = static_cast<int64_t>(bh) * p.sq + q_row0 + k * BM + row;
-    const int64_t ps = slice - p.part_base;
-    if (p.part_m == nullptr) {
-      p.m[grow] = m_true;
-      p.l[grow] = l_true;
-    } else {
-      p.part_m[ps * p.rows_total + grow] = m_true;
-      p.part_l[ps * p.rows_total + grow] = l_true;
-    }
-    mbar_wait(&s.pv_done[k], 0);
-    tc_fence_after();
-    const float inv_l = 1.f / l;
-#pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t r[32];
-      tmem_ld32(tOk + c * 32, r);
-      tmem_ld_wait();
-      if (p.part_o == nullptr) {
-        uint4* dst = reinterpret_cast<uint4*>(p.o + grow * D + c * 32);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          uint4 w;
-          w.x = pack_bf16x2(__uint_as_float(r[8 * v + 0]) * inv_l, __uint_as_float(r[8 * v + 1]) * inv_l);
-          w.y = pack_bf16x2(__uint_as_float(r[8 * v + 2]) * inv_l, __uint_as_float(r[8 * v + 3]) * inv_l);
-          w.z = pack_bf16x2(__uint_as_float(r[8 * v + 4]) * inv_l, __uint_as_float(r[8 * v + 5]) * inv_l);
-          w.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]) * inv_l, __uint_as_float(r[8 * v + 7]) * inv_l);
-          dst[v] = w;
-        }
+      // ---- finalize (finalize_root): d2 re-based to the true d1, d3 = O / d2 ----
+      const float l_true = l * ex2_mufu((m_ref - m_true) * kLog2e);
+      const int64_t grow = static_cast<int64_t>(bh) * p.sq + q_row0 + k * BM + row;
+      const int64_t ps = slice - p.part_base;
+      if (p.part_m == nullptr) {
+        p.m[grow] = m_true;
+        p.l[grow] = l_true;
       } else {
-        float4* dst = reinterpret_cast<float4*>(p.part_o + (ps * p.rows_total + grow) * D + c * 32);
+        p.part_m[ps * p.rows_total + grow] = m_true;
+        p.part_l[ps * p.rows_total + grow] = l_true;
+      }
+      mbar_wait(&s.pv_done[k], uc & 1);
+      tc_fence_after();
+      const float inv_l = 1.f / l;
 #pragma unroll
-        for (int v = 0; v < 8; ++v)
-          dst[v] = make_float4(__uint_as_float(r[4 * v]) * inv_l, __uint_as_float(r[4 * v + 1]) * inv_l,
-                               __uint_as_float(r[4 * v + 2]) * inv_l, __uint_as_float(r[4 * v + 3]) * inv_l);
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tOk + c * 32, r);
+        tmem_ld_wait();
+        if (c + 1 == D / 32) {  // O_k fully read: the next unit's P V_k may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if ((threadIdx.x & 31) == 0) mbar_arrive(&s.o_empty[k]);
+        }
+        if (p.part_o == nullptr) {
+          uint4* dst = reinterpret_cast<uint4*>(p.o + grow * D + c * 32);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            uint4 w;
+            w.x = pack_bf16x2(__uint_as_float(r[8 * v + 0]) * inv_l, __uint_as_float(r[8 * v + 1]) * inv_l);
+            w.y = pack_bf16x2(__uint_as_float(r[8 * v + 2]) * inv_l, __uint_as_float(r[8 * v + 3]) * inv_l);
+            w.z = pack_bf16x2(__uint_as_float(r[8 * v + 4]) * inv_l, __uint_as_float(r[8 * v + 5]) * inv_l);
+            w.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]) * inv_l, __uint_as_float(r[8 * v + 7]) * inv_l);
+            dst[v] = w;
+          }
+        } else {
+          float4* dst = reinterpret_cast<float4*>(p.part_o + (ps * p.rows_total + grow) * D + c * 32);
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            dst[v] = make_float4(__uint_as_float(r[4 * v]) * inv_l, __uint_as_float(r[4 * v + 1]) * inv_l,
+                                 __uint_as_float(r[4 * v + 2]) * inv_l, __uint_as_float(r[4 * v + 3]) * inv_l);
+        }
       }
     }
   }
@@ -377,13 +413,18 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   p.part_m = a.part_m;
   p.part_l = a.part_l;
   p.part_o = a.part_o;
+  p.units_x = static_cast<int>(a.sq / (2 * BM));
+  p.units_bh = static_cast<int>(a.bh);
+  p.units = p.units_x * p.units_bh * static_cast<int>(a.nslices);
   const size_t smem = sizeof(Smem<D>) + 1024;
   auto kern = attn_sm100_kernel<D>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  dim3 grid(static_cast<unsigned>(a.sq / (2 * BM)), static_cast<unsigned>(a.bh),
-            static_cast<unsigned>(a.nslices));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  dim3 grid(static_cast<unsigned>(p.units < sms ? p.units : sms));  // persistent: one CTA per SM
   kern<<<grid, NTHREADS, smem, st>>>(tq, tk, tv, p);
   return cudaGetLastError();
 }
