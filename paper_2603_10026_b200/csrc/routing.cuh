@@ -4,10 +4,10 @@
 //   index), ties to the LOWEST index (topk_merge, proj/src/simulator.cpp:80-88;
 //   tests/test_workloads.cpp:210-224).
 // Lane l holds experts e = l + 32 j (j < PER). The top-K' is K' rounds of a
-// warp argmax under the total order (value desc, index asc): every round is a
-// 5-step butterfly over (value, index) pairs, so the winner is unique and the
-// indices are bit-exact regardless of the reduction tree; the owning lane then
-// retires the winner. Round 1's winner is d1 (exact max), after which d2 is a
+// warp argmax under the total order (value desc, index asc), encoded as one
+// 64-bit key per candidate: every round is a 5-step butterfly of branch-free
+// 64-bit maxima, so the winner is unique and the indices are bit-exact
+// regardless of the reduction tree; the owning lane then retires the winner. Round 1's winner is d1 (exact max), after which d2 is a
 // warp sum of exp(s - d1) — the incremental Eq.17 rescaling collapses because
 // the whole row is already in registers (one pass over memory).
 #pragma once
@@ -16,11 +16,23 @@
 
 namespace rf {
 
-// a ranks before b: larger value, then lower index; index 0 = no candidate
-__device__ __forceinline__ bool route_before(float av, int ai, float bv, int bi) {
-  if (ai == 0) return false;
-  if (bi == 0) return true;
-  return av > bv || (av == bv && ai < bi);
+// Candidates as 64-bit keys ordered like (value desc, index asc): the value's
+// bits mapped to an order-preserving unsigned (-0 canonicalised to +0, so
+// equal values tie and fall to the index), then ~index. Key 0 = no candidate.
+// The argmax is then one branch-free 64-bit max per butterfly step.
+__device__ __forceinline__ uint64_t route_key(float v, int idx1) {
+  if (idx1 == 0) return 0ull;
+  uint32_t u = __float_as_uint(v == 0.f ? 0.f : v);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return (static_cast<uint64_t>(u) << 32) | static_cast<uint32_t>(~idx1);
+}
+__device__ __forceinline__ float route_value(uint64_t key) {
+  uint32_t u = static_cast<uint32_t>(key >> 32);
+  u = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+  return __uint_as_float(u);
+}
+__device__ __forceinline__ int route_index(uint64_t key) {
+  return static_cast<int>(~static_cast<uint32_t>(key));
 }
 
 // x[j] = score of expert lane + 32 j (only e < experts are valid). Writes the
@@ -28,34 +40,30 @@ __device__ __forceinline__ bool route_before(float av, int ai, float bv, int bi)
 template <int PER, int K>
 __device__ __forceinline__ void warp_route(const float (&x)[PER], int experts, int lane, float* d1,
                                            float* d2, int2* topk) {
-  uint32_t taken = 0;
+  uint64_t key[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int e = lane + 32 * j;
+    key[j] = route_key(x[j], e < experts ? e + 1 : 0);
+  }
   float m = -INFINITY;
   int2 rec = make_int2(0, 0);
 #pragma unroll
   for (int r = 0; r < K; ++r) {
-    float bv = 0.f;
-    int bi = 0;
+    uint64_t best = key[0];
 #pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const int e = lane + 32 * j;
-      const int ei = (e < experts && !((taken >> j) & 1)) ? e + 1 : 0;
-      if (route_before(x[j], ei, bv, bi)) {
-        bv = x[j];
-        bi = ei;
-      }
-    }
+    for (int j = 1; j < PER; ++j) best = key[j] > best ? key[j] : best;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (route_before(ov, oi, bv, bi)) {
-        bv = ov;
-        bi = oi;
-      }
+      const uint64_t o = __shfl_xor_sync(0xffffffffu, best, off);
+      best = o > best ? o : best;
     }
-    if (bi != 0 && ((bi - 1) & 31) == lane) taken |= 1u << ((bi - 1) >> 5);
-    if (r == 0) m = bi != 0 ? bv : -INFINITY;
-    if (lane == r) rec = bi != 0 ? make_int2(__float_as_int(bv), bi) : make_int2(0, 0);
+    // the owning lane retires the winner
+#pragma unroll
+    for (int j = 0; j < PER; ++j) key[j] = key[j] == best ? 0ull : key[j];
+    const bool found = best != 0ull;
+    if (r == 0) m = found ? route_value(best) : -INFINITY;
+    if (lane == r && found) rec = make_int2(__float_as_int(route_value(best)), route_index(best));
   }
   float t = 0.f;
 #pragma unroll
