@@ -88,6 +88,17 @@ def test_tcgen05_prefill_multisegment(segments):
     assert max(errs) < TOL
 
 
+@pytest.mark.parametrize("B,H,Sq,Skv,segments,D", [(2, 64, 512, 256, 1, 128), (1, 100, 512, 512, 2, 128),
+                                                   (3, 50, 256, 384, 1, 64), (1, 160, 256, 128, 1, 128)])
+def test_tcgen05_persistent_multi_unit(B, H, Sq, Skv, segments, D):
+    """More work units than SMs: each persistent CTA walks several units, so
+    barrier phases, the Q reload after the last S, and the o_empty hand-off of
+    the epilogue to the next unit are all exercised (and so are units whose
+    KV slice has 2-4 tiles)."""
+    errs, _ = _run(B, H, Sq, Skv, D, segments=segments, seed=B + H, expect="tcgen05")
+    assert max(errs) < TOL
+
+
 def test_tcgen05_stats_are_tight():
     """d1 is an exact max of fp32 logits; d2 accumulates fp32 exps: both far
     tighter than the bf16 tolerance."""
