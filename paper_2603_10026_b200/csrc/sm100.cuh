@@ -461,8 +461,10 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
 
 // 2^x for a pair on the FMA/ALU pipes only: n = rint(x) via the 1.5*2^23
 // magic-number add (no F2I/FRND, which would issue on the XU pipe like
-// MUFU), f = x - n in [-0.5, 0.5], p = degree-3 fit of 2^f (max rel err
-// 7.7e-5 < bf16's 3.9e-3), 2^x = p * 2^n by an integer add to the exponent.
+// MUFU), f = x - n in [-0.5, 0.5], p = degree-2 relative-minimax fit of 2^f
+// (max rel err 1.7e-3, below bf16's 3.9e-3 ulp: the P this feeds is rounded
+// to bf16; one FFMA2 less than degree 3 measured +4 % on cfg2), 2^x = p * 2^n
+// by an integer add to the exponent.
 // Inputs are clamped at -127 (result ~1e-38); valid for x <= 127.
 __device__ __forceinline__ uint64_t ex2_poly2(uint64_t x2) {
   float x0, x1;
@@ -472,10 +474,8 @@ __device__ __forceinline__ uint64_t ex2_poly2(uint64_t x2) {
   const uint64_t t = fadd2(x2, magic);
   const uint64_t r = fadd2(t, nmagic);
   const uint64_t f = ffma2(r, f2(-1.f, -1.f), x2);
-  uint64_t p = ffma2(f, f2(0.05508868396282196f, 0.05508868396282196f),
-                     f2(0.24260404706001282f, 0.24260404706001282f));
-  p = ffma2(p, f, f2(0.6932762265205383f, 0.6932762265205383f));
-  p = ffma2(p, f, f2(0.9999289512634277f, 0.9999289512634277f));
+  uint64_t p = ffma2(f, f2(0.2384257f, 0.2384257f), f2(0.70344281f, 0.70344281f));
+  p = ffma2(p, f, f2(1.00044296f, 1.00044296f));
   float p0, p1, t0, t1;
   f2split(p, p0, p1);
   f2split(t, t0, t1);
