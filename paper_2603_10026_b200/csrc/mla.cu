@@ -7,74 +7,65 @@
 // All 128 heads of a batch share the cache, so a decode step is GEMM-shaped:
 // S = Q (128 x 576) K^T, O += P V (N = 512).
 //
-// TMEM holds 512 fp32 columns and O alone is 128 x 512, so a (batch, KV
-// slice) runs on a CTA PAIR (thread-block cluster of 2) that splits both
-// reductions by the cache's 64-column chunks: CTA h owns chunks
-// {4h .. 4h+3} (+ the rope chunk 8 for h = 0):
-//   * its Q chunks stay resident in shared memory (80 / 64 KB) and it streams
-//     only its own chunks of each 64-key cache tile (40 / 32 KB per tile,
-//     2-slot TMA ring, SWIZZLE_128B) — the pair reads every cache byte once;
-//   * tcgen05.mma kind::f16 computes its PARTIAL S_h = Q_h K_h^T
-//     (M = 128, N = 64 keys, 20 / 16 K-steps) into a double-buffered S in TMEM;
-//   * the softmax warps (thread = head row) swap partial S tiles with the
-//     peer through distributed shared memory: each stages its 64 fp32
-//     partials in its own shared memory, one thread bulk-copies the 32 KB
-//     tile into the peer's receive buffer (cp.async.bulk shared::cta ->
-//     shared::cluster, completing on the peer's mbarrier: no release fence;
-//     per-thread st.async was measured ~10x slower); S = S_0 + S_1 is then
-//     bit-identical in both CTAs (operands added in the same order), and so
-//     are d1, d2 and P;
-//   * P (bf16) overwrites the S buffer and is the TMEM A operand of
-//     O_h += P V_h (M = 128, N = 256, K = 64), V_h = the CTA's own 4 chunks
-//     of the same smem tile as an MN-major B;
-//   * the d3 correction exp(d1' - d1) is applied to the TMEM accumulator
-//     lazily (only when the running max passes the reference by 2^8, after
-//     P V_{i-1} has retired); d2'/d2 telescopes to 1/d2 at finalize
-//     (finalize_root, proj/src/simulator.cpp:611-621) — as attn_sm100.cu;
-//   * Multi-Segment: each KV slice writes its (m, l, O/l) partial state,
-//     merged in slice order by merge.cu (run_multisegment semantics).
-// MMA order: S_{i+1} and P V_i as their inputs arrive (S_{i+1} under softmax i).
-// Warps: 0-3 softmax + exchange + epilogue, 4 TMA, 5 MMA (192 threads).
+// A (batch, KV slice) runs on a CTA PAIR issuing 2-SM MMAs
+// (tcgen05.mma.cta_group::2, M = 128): CTA h owns heads [64h, 64h + 64) —
+// its 64 Q rows stay in shared memory (9 x 8 KB, SWIZZLE_128B) — and, per
+// 128-key cache tile,
+//   * S = Q K^T (N = 128 keys, K = 576): CTA h stages keys [64h, 64h + 64)
+//     of the tile (9 chunks of 64 columns), so the pair reads every cache
+//     byte from HBM once;
+//   * the 2-SM accumulator layout puts row r's keys [0, 64) in TMEM lane r
+//     and keys [64, 128) in lane r + 64: the softmax thread of each lane owns
+//     half a row; the two halves exchange their row max through shared
+//     memory (no cross-CTA traffic in the loop);
+//   * P (bf16) goes to shared memory (the MMA's A operand, 16 KB);
+//   * O += P V as two N = 256 MMAs (V columns [0, 256) and [256, 512));
+//     CTA h supplies V columns 256j + [128h, 128h + 128) of all 128 keys —
+//     re-read from L2 (the pair's K stages just brought them in);
+//     O is 64 rows x 512 per CTA = 256 TMEM columns (lane r: columns
+//     256j + [0, 128), lane r + 64: 256j + [128, 256)).
+// One 17-stage ring of 8 KB (9 K + 8 V stages = exactly one tile): tile
+// i + 1's K stages load as soon as S_i has consumed tile i's, its V stages
+// once P V_i has. The MMA warp issues S_{i+1} and P V_i as their inputs arrive
+// (S_{i+1} runs under softmax i; S is double-buffered in TMEM).
+// The d3 correction exp(d1' - d1) is lazy (only when the running max passes
+// the reference by 2^8, after P V_{i-1} has retired); d2'/d2 telescopes to
+// 1/d2 at finalize (finalize_root, proj/src/simulator.cpp:611-621), as in
+// attn_sm100.cu. Multi-Segment: each KV slice writes its (m, l, O/l)
+// partial state, merged in slice order by merge.cu (run_multisegment).
+// Warps: 0-3 softmax + correction + epilogue, 4 TMA, 5 MMA (leader) / relay
+// of the peer's TMA completions to the leader (192 threads).
 #include <cuda_bf16.h>
 
 #include "rf_internal.h"
 #include "sm100.cuh"
-
-#ifdef RF_MLA_TRACE
-__device__ unsigned long long g_mla_trace[2][64][8];
-#define MT_STAMP(t, i) do { if ((blockIdx.y | blockIdx.z) == 0 && (t) < 64) { unsigned long long v_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v_)); g_mla_trace[blockIdx.x][(t)][(i)] = v_; } } while (0)
-#else
-#define MT_STAMP(t, i) do {} while (0)
-#endif
 
 namespace rf {
 namespace {
 
 using namespace sm100;
 
-constexpr int HN = 128;        // heads (rows, UMMA M)
+constexpr int HN = 128;        // heads per batch (2-SM UMMA M)
+constexpr int HC = HN / 2;     // heads per CTA
 constexpr int DQK = 576;       // cache row / query width
 constexpr int DV = 512;        // value width (latent)
-constexpr int DH = DV / 2;     // value columns per CTA
-constexpr int TK = 64;         // keys per tile
-constexpr int MAXC = 5;        // chunks per CTA (h = 0: 0-3 + rope 8; h = 1: 4-7)
-constexpr int NSLOT = 2;
+constexpr int NCH = DQK / 64;  // 64-column chunks per cache row
+constexpr int TK = 128;        // keys per tile
+constexpr int NKS = NCH;       // K stages per tile (this CTA's 64 keys x 64 columns)
+constexpr int NVS = 8;         // V stages per tile (2 halves x 4 x 32 keys x 128 columns)
+constexpr int NST = NKS + NVS; // ring stages = one tile
+constexpr int STB = 8192;      // stage bytes
 constexpr int NT = 192;
-constexpr int XB = HN * TK * 4; // exchange buffer bytes (one partial S tile, fp32)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 struct Smem {
-  uint8_t q[MAXC][HN * 128];          // 5 x 16 KB
-  uint8_t kv[NSLOT][MAXC][TK * 128];  // 2 x 5 x 8 KB
-  float xsend[HN * TK];               // this CTA's partial S, staged for the bulk copy
-  float xrecv[HN * TK];               // the peer's partial S of the current tile
-  uint64_t q_full;
-  uint64_t kv_full[NSLOT], kv_empty[NSLOT];
-  uint64_t s_full[2], p_full[2];
-  uint64_t pv_done, o_full;
-  uint64_t x_full;   // peer's partial landed (complete_tx)
-  uint64_t x_empty;  // peer has consumed the partial we sent (remote arrivals)
+  uint8_t q[NCH][HC * 128];  // 9 x 8 KB
+  uint8_t ring[NST][STB];    // 17 x 8 KB
+  uint8_t p[2][HC * 128];    // P: keys [0, 64) and [64, 128), K-major SWIZZLE_128B
+  float xm[2][HN];           // row-half exchange (max per tile, then l)
+  uint64_t q_full, full[NST], empty[NST];
+  uint64_t s_full[2], p_full, pv_done, o_full;
   uint32_t tmem_base;
 };
 
@@ -89,253 +80,225 @@ struct Params {
   float* part_o;
 };
 
-__device__ __forceinline__ int chunk_of(int h, int j) { return h == 0 ? (j < 4 ? j : 8) : 4 + j; }
-
-// Bulk copy (TMA engine) from this CTA's shared memory into the peer's,
-// completing `bytes` on the peer's mbarrier.
-__device__ __forceinline__ void bulk_copy_to_peer(uint32_t dst_cluster, uint32_t src, uint32_t bytes,
-                                                  uint32_t bar_cluster) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          dst_cluster),
-      "r"(src), "r"(bytes), "r"(bar_cluster)
-      : "memory");
-}
-
-// float4 chunk q of row r at chunk q ^ (r & 15): conflict-free row-per-thread access
-__device__ __forceinline__ int xoff(int r, int q) { return r * TK + 4 * (q ^ (r & 15)); }
-
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
-    mla_decode_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv,
-                      const Params p) {
+    mla_decode_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                      const __grid_constant__ CUtensorMap tv, const Params p) {
   extern __shared__ uint8_t smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = warp_id();
-  const int h = static_cast<int>(cluster_ctarank());  // = blockIdx.x: V columns [256 h, +256)
-  const int nc = h == 0 ? 5 : 4;
+  const int h = static_cast<int>(cluster_ctarank());
+  const bool leader = h == 0;
   const int b = blockIdx.y;      // batch
   const int slice = blockIdx.z;  // KV slice
   const int64_t kv0 = static_cast<int64_t>(slice) * p.slice_len;
   const int n_tiles = static_cast<int>(p.slice_len / TK);
 
   if (threadIdx.x == 0) {
-    mbar_init(&s.q_full, 1);
-    for (int i = 0; i < NSLOT; ++i) {
-      mbar_init(&s.kv_full[i], 1);
-      mbar_init(&s.kv_empty[i], 1);
+    mbar_init(&s.q_full, leader ? 2 : 1);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&s.full[i], leader ? 2 : 1);  // leader: own TMA + the peer's relay
+      mbar_init(&s.empty[i], 1);
     }
-    for (int k = 0; k < 2; ++k) {
-      mbar_init(&s.s_full[k], 1);
-      mbar_init(&s.p_full[k], 4);  // one arrival per softmax warp
-    }
+    for (int k = 0; k < 2; ++k) mbar_init(&s.s_full[k], 1);
+    mbar_init(&s.p_full, 8);  // 4 softmax warps of each CTA (leader's copy is the one used)
     mbar_init(&s.pv_done, 1);
     mbar_init(&s.o_full, 1);
-    mbar_init(&s.x_full, 1);   // armed with expect_tx by this CTA each tile
-    mbar_init(&s.x_empty, 4);  // the peer's 4 softmax warps
     fence_barrier_init();
-    mbar_arrive_expect_tx(&s.x_full, XB);  // tile 0's incoming partial
   }
-  if (warp == 5) tmem_alloc<512>(&s.tmem_base);
+  if (warp == 5) tmem_alloc_2sm<512>(&s.tmem_base);
   tc_fence_before();
-  cluster_sync();  // barriers of both CTAs initialised before any remote traffic
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem = s.tmem_base;
-  const uint32_t tS[2] = {tmem + 0, tmem + TK};
-  const uint32_t tO = tmem + 256;
+  const uint32_t tS[2] = {tmem + 0, tmem + 64};
+  const uint32_t tO = tmem + 256;  // + 128 j: V columns 256 j + ...
 
   if (warp == 4) {
     // ------------------------------------------------------------ TMA ----
     if (elect_one()) {
       prefetch_tmap(&tq);
-      prefetch_tmap(&tkv);
-      mbar_arrive_expect_tx(&s.q_full, nc * HN * 128);
-      for (int j = 0; j < nc; ++j)
-        tma_load_2d(s.q[j], &tq, &s.q_full, chunk_of(h, j) * 64, b * HN, kEvictFirst);
+      prefetch_tmap(&tk);
+      prefetch_tmap(&tv);
+      mbar_arrive_expect_tx(&s.q_full, NCH * HC * 128);
+      for (int c = 0; c < NCH; ++c) tma_load_2d(s.q[c], &tq, &s.q_full, c * 64, b * HN + h * HC, kEvictFirst);
       const int32_t y0 = static_cast<int32_t>(static_cast<int64_t>(b) * p.skv + kv0);
       for (int t = 0; t < n_tiles; ++t) {
-        const int slot = t % NSLOT;
-        mbar_wait(&s.kv_empty[slot], ((t / NSLOT) & 1) ^ 1);
-        MT_STAMP(t, 0);
-        mbar_arrive_expect_tx(&s.kv_full[slot], nc * TK * 128);
-        for (int j = 0; j < nc; ++j)
-          tma_load_2d(s.kv[slot][j], &tkv, &s.kv_full[slot], chunk_of(h, j) * 64, y0 + t * TK, kEvictFirst);
+        const uint32_t ph = (t & 1) ^ 1;
+        const int32_t key0 = y0 + t * TK;
+        for (int c = 0; c < NKS; ++c) {  // this CTA's 64 keys, all 576 columns (HBM)
+          mbar_wait(&s.empty[c], ph);
+          mbar_arrive_expect_tx(&s.full[c], STB);
+          tma_load_2d(s.ring[c], &tk, &s.full[c], c * 64, key0 + h * 64, kEvictNormal);
+        }
+        for (int v = 0; v < NVS; ++v) {  // all 128 keys, V columns 256 j + [128 h, +128) (L2)
+          const int st = NKS + v, j = v >> 2, kk = v & 3;
+          mbar_wait(&s.empty[st], ph);
+          mbar_arrive_expect_tx(&s.full[st], STB);
+          const int c0 = 4 * j + 2 * h;
+          tma_load_2d(s.ring[st], &tv, &s.full[st], c0 * 64, key0 + 32 * kk, kEvictFirst);
+          tma_load_2d(s.ring[st] + STB / 2, &tv, &s.full[st], (c0 + 1) * 64, key0 + 32 * kk, kEvictFirst);
+        }
       }
     }
   } else if (warp == 5) {
-    // ------------------------------------------------------------ MMA ----
-    const uint32_t id_s = idesc_f16(HN, TK, kFmtBF16, false, false);
-    const uint32_t id_o = idesc_f16(HN, DH, kFmtBF16, false, true);
-    const bool leader = elect_one();
-    auto issue_s = [&](int i) {  // partial S_i = Q_h K_h,i^T into S buffer i & 1
-      const int slot = i % NSLOT;
-      mbar_wait(&s.kv_full[slot], (i / NSLOT) & 1);
-      tc_fence_after();
-      if (leader) {
-        const uint32_t qa = smem_u32(s.q[0]), kb = smem_u32(s.kv[slot][0]);
-        for (int j = 0; j < nc; ++j)
+    if (leader) {
+      // ---------------------------------------------------------- MMA ----
+      const uint32_t id_s = idesc_f16(HN, TK, kFmtBF16, false, false);
+      const uint32_t id_o = idesc_f16(HN, 256, kFmtBF16, false, true);
+      const bool el = elect_one();
+      auto issue_s = [&](int i) {  // S_i = Q K_i^T into S buffer i & 1
+        for (int c = 0; c < NKS; ++c) {
+          mbar_wait(&s.full[c], i & 1);
+          tc_fence_after();
+          if (el) {
+            const uint32_t qa = smem_u32(s.q[c]), kb = smem_u32(s.ring[c]);
 #pragma unroll
-          for (int k4 = 0; k4 < 4; ++k4)
-            mma_f16_ss(tS[i & 1], sdesc_kmajor_sw128(qa + j * HN * 128 + k4 * 32),
-                       sdesc_kmajor_sw128(kb + j * TK * 128 + k4 * 32), id_s, (j | k4) != 0);
-        mma_commit(&s.s_full[i & 1]);
-        MT_STAMP(i, 1);
-      }
-      __syncwarp();
-    };
-    auto issue_pv = [&](int i) {  // O_h += P_i V_h,i  (V_h = this CTA's chunks 0-3 of tile i)
-      const int slot = i % NSLOT;
-      mbar_wait(&s.p_full[i & 1], (i >> 1) & 1);
-      tc_fence_after();
-      if (leader) {
-        const uint32_t vb = smem_u32(s.kv[slot][0]);
+            for (int k4 = 0; k4 < 4; ++k4)
+              mma_f16_ss_2sm(tS[i & 1], sdesc_kmajor_sw128(qa + k4 * 32), sdesc_kmajor_sw128(kb + k4 * 32), id_s,
+                             (c | k4) != 0);
+            mma_commit_2sm(&s.empty[c]);
+            if (c + 1 == NKS) mma_commit_2sm(&s.s_full[i & 1]);
+          }
+          __syncwarp();
+        }
+      };
+      auto issue_pv = [&](int i) {  // O += P_i V_i
+        mbar_wait(&s.p_full, i & 1);
+        tc_fence_after();
+        const uint32_t pa = smem_u32(s.p[0]);
+        for (int v = 0; v < NVS; ++v) {
+          const int st = NKS + v, j = v >> 2, kk = v & 3;
+          mbar_wait(&s.full[st], i & 1);
+          tc_fence_after();
+          if (el) {
+            const uint32_t vb = smem_u32(s.ring[st]);
 #pragma unroll
-        for (int ks = 0; ks < TK / 16; ++ks)
-          mma_f16_ts(tO, tS[i & 1] + ks * 8, sdesc_mnmajor_sw128(vb + ks * 2048, TK * 128), id_o,
-                     (i | ks) != 0);
-        mma_commit(&s.kv_empty[slot]);
-        mma_commit(&s.pv_done);
-        if (i + 1 == n_tiles) mma_commit(&s.o_full);
-        MT_STAMP(i, 2);
-      }
-      __syncwarp();
-    };
-    mbar_wait(&s.q_full, 0);
-    if (n_tiles > 0) issue_s(0);
-    // S_{i+1} (other S buffer, runs under softmax i) and P V_i in whichever
-    // order their inputs arrive: the tensor pipe executes in issue order and
-    // issue blocks at its rate, so a fixed S-first order would hold P V_i —
-    // and with it the release of cache slot i, which gates the load of tile
-    // i + 2 — behind tile i + 1's arrival.
-    for (int i = 0; i < n_tiles; ++i) {
-      bool s_next = i + 1 >= n_tiles;  // S_{i+1} issued (or none)
-      for (;;) {
-        int pick = 0;  // 1: S_{i+1}, 2: P V_i (lane 0 decides for the warp)
-        if (lane_id() == 0) {
-          if (!s_next && mbar_try_wait(&s.kv_full[(i + 1) % NSLOT], ((i + 1) / NSLOT) & 1)) pick = 1;
-          else if (mbar_try_wait(&s.p_full[i & 1], (i >> 1) & 1)) pick = 2;
+            for (int ks = 0; ks < 2; ++ks)
+              mma_f16_ss_2sm(tO + 128 * j, sdesc_kmajor_sw128(pa + (kk >> 1) * (HC * 128) + (kk & 1) * 64 + ks * 32),
+                             sdesc_mnmajor_sw128(vb + ks * 2048, STB / 2), id_o, (i | kk | ks) != 0);
+            mma_commit_2sm(&s.empty[st]);
+            if (v + 1 == NVS) {
+              mma_commit_2sm(&s.pv_done);
+              if (i + 1 == n_tiles) mma_commit_2sm(&s.o_full);
+            }
+          }
+          __syncwarp();
         }
-        pick = __shfl_sync(0xffffffffu, pick, 0);
-        if (pick == 1) {
-          issue_s(i + 1);
-          s_next = true;
-        } else if (pick == 2) {
-          issue_pv(i);
-          break;
+      };
+      mbar_wait(&s.q_full, 0);
+      if (n_tiles > 0) issue_s(0);
+      // S_{i+1} (other S buffer, runs under softmax i) and P V_i in whichever
+      // order their inputs arrive: the tensor pipe executes in issue order,
+      // so a fixed S-first order would hold P V_i — and the V loads of tile
+      // i + 1 behind it — until tile i + 1's first K stage has landed.
+      for (int i = 0; i < n_tiles; ++i) {
+        bool s_next = i + 1 >= n_tiles;
+        for (;;) {
+          int pick = 0;
+          if (lane_id() == 0) {
+            if (!s_next && mbar_try_wait(&s.full[0], (i + 1) & 1)) pick = 1;
+            else if (mbar_try_wait(&s.p_full, i & 1)) pick = 2;
+          }
+          pick = __shfl_sync(0xffffffffu, pick, 0);
+          if (pick == 1) {
+            issue_s(i + 1);
+            s_next = true;
+          } else if (pick == 2) {
+            issue_pv(i);
+            break;
+          }
         }
+        if (!s_next) issue_s(i + 1);
       }
-      if (!s_next) issue_s(i + 1);
+    } else if (elect_one()) {
+      // relay: this CTA's TMA stages have landed -> the leader's barriers
+      mbar_wait(&s.q_full, 0);
+      mbar_arrive_cluster(mapa_shared(smem_u32(&s.q_full), 0));
+      for (int t = 0; t < n_tiles; ++t)
+        for (int st = 0; st < NST; ++st) {
+          mbar_wait(&s.full[st], t & 1);
+          mbar_arrive_cluster(mapa_shared(smem_u32(&s.full[st]), 0));
+        }
     }
   } else {
-    // ------------------- partial-S exchange / softmax / correction / epilogue --
-    const int row = threadIdx.x;  // head
+    // -------------------------- softmax / correction / epilogue (lane = thread) --
+    const int lane = threadIdx.x;  // TMEM lane: row lane % 64, keys / V columns half lane / 64
+    const int row = lane & (HC - 1), half = lane >> 6;
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
     const float c1 = p.scale * kLog2e;
-    const uint32_t peer = static_cast<uint32_t>(h ^ 1);
-    const uint32_t xrecv_peer = mapa_shared(smem_u32(s.xrecv), peer);
-    const uint32_t xfull_peer = mapa_shared(smem_u32(&s.x_full), peer);
-    const uint32_t xempty_peer = mapa_shared(smem_u32(&s.x_empty), peer);
+    const uint32_t p_row = smem_u32(s.p[half]) + (row >> 3) * 1024 + (row & 7) * 128;
+    const uint32_t pfull_leader = mapa_shared(smem_u32(&s.p_full), 0);
     float m_true = -INFINITY, m_ref = -INFINITY, l = 0.f;
     for (int i = 0; i < n_tiles; ++i) {
       const int bb = i & 1;
       mbar_wait(&s.s_full[bb], (i >> 1) & 1);
       tc_fence_after();
-      if (threadIdx.x == 0) MT_STAMP(i, 3);
       uint32_t sv[2][32];
       tmem_ld32(tS[bb] + lane_off, sv[0]);
       tmem_ld32(tS[bb] + lane_off + 32, sv[1]);
       tmem_ld_wait();
-      // stage this CTA's partial row; one thread bulk-copies the tile into the
-      // peer once the peer has consumed the previous one
-      if (i > 0) {
-        if (threadIdx.x == 0) bulk_wait_read0();  // previous copy has read xsend
-        named_bar_sync(1, 128);
-      }
+      float mx = __uint_as_float(sv[0][0]);
 #pragma unroll
-      for (int q = 0; q < TK / 4; ++q)
-        *reinterpret_cast<uint4*>(s.xsend + xoff(row, q)) =
-            make_uint4(sv[q >> 3][(4 * q) & 31], sv[q >> 3][(4 * q + 1) & 31], sv[q >> 3][(4 * q + 2) & 31],
-                       sv[q >> 3][(4 * q + 3) & 31]);
-      fence_proxy_async_smem();
+      for (int j = 1; j < 64; ++j) mx = fmaxf(mx, __uint_as_float(sv[j >> 5][j & 31]));
+      s.xm[bb][lane] = mx;
       named_bar_sync(1, 128);
-      if (threadIdx.x == 0) {
-        if (i > 0) mbar_wait(&s.x_empty, (i - 1) & 1);
-        MT_STAMP(i, 4);
-        bulk_copy_to_peer(xrecv_peer, smem_u32(s.xsend), XB, xfull_peer);
-        bulk_commit();
-      }
-      // receive the peer's partial row: S = S_0 + S_1 (operands in chunk order,
-      // so both CTAs round identically)
-      mbar_wait(&s.x_full, i & 1);
-      if (threadIdx.x == 0) MT_STAMP(i, 5);
-      float sx[TK];
-#pragma unroll
-      for (int q = 0; q < TK / 4; ++q) {
-        const float4 v = *reinterpret_cast<const float4*>(s.xrecv + xoff(row, q));
-        const float pv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float own = __uint_as_float(sv[q >> 3][(4 * q + e) & 31]);
-          sx[4 * q + e] = h == 0 ? own + pv[e] : pv[e] + own;
-        }
-      }
-      // the receive buffer is free again: re-arm it for the next tile, then
-      // tell the peer (its next copy may land after this point)
-      __syncwarp();
-      if (threadIdx.x == 0 && i + 1 < n_tiles) mbar_arrive_expect_tx(&s.x_full, XB);
-      if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(xempty_peer);
-      float mx = sx[0];
-#pragma unroll
-      for (int j = 1; j < TK; ++j) mx = fmaxf(mx, sx[j]);
+      mx = fmaxf(mx, s.xm[bb][lane ^ 64]);
       m_true = fmaxf(m_true, mx * p.scale);
-      const bool need = (m_true - m_ref) * kLog2e > kRescaleThreshold;
+      const bool need = (m_true - m_ref) * kLog2e > kRescaleThreshold;  // same in both halves
       float alpha = 1.f;
       if (need) {
         alpha = ex2_mufu((m_ref - m_true) * kLog2e);  // 0 on the first tile
         l *= alpha;
         m_ref = m_true;
       }
-      if (i > 0 && __any_sync(0xffffffffu, need)) {
-        // O *= exp(d1' - d1) once P V_{i-1} has retired (pv_done completions so
-        // far are i - 1 or i: P V_i needs this tile's P)
-        mbar_wait(&s.pv_done, (i - 1) & 1);
-        tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < DH / 16; ++c) {
-          uint32_t r[16];
-          tmem_ld16(tO + lane_off + c * 16, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * alpha);
-          tmem_st16(tO + lane_off + c * 16, r);
-        }
-        tmem_st_wait();
-      }
       const float nmb = -m_ref * kLog2e;
+      uint32_t pk[32];
       float rs = 0.f;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float p0 = ex2_mufu(fmaf(sx[32 * c + 2 * j], c1, nmb));
-          const float p1 = ex2_mufu(fmaf(sx[32 * c + 2 * j + 1], c1, nmb));
-          rs += p0 + p1;
-          pk[j] = pack_bf16x2(p0, p1);
-        }
-        tmem_st16(tS[bb] + lane_off + 16 * c, pk);
+      for (int j = 0; j < 32; ++j) {
+        const float p0 = ex2_mufu(fmaf(__uint_as_float(sv[j >> 4][(2 * j) & 31]), c1, nmb));
+        const float p1 = ex2_mufu(fmaf(__uint_as_float(sv[j >> 4][(2 * j + 1) & 31]), c1, nmb));
+        rs += p0 + p1;
+        pk[j] = pack_bf16x2(p0, p1);
       }
       l += rs;
-      tmem_st_wait();
+      // P V_{i-1} has retired: the P buffer is free and O may be rescaled
+      if (i > 0) {
+        mbar_wait(&s.pv_done, (i - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, need)) {
+#pragma unroll 1
+          for (int c = 0; c < 256 / 16; ++c) {
+            uint32_t r[16];
+            tmem_ld16(tO + lane_off + c * 16, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * alpha);
+            tmem_st16(tO + lane_off + c * 16, r);
+          }
+          tmem_st_wait();
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        sts128(p_row + ((u ^ (row & 7)) << 4), make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
+      fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
-      if ((threadIdx.x & 31) == 0) mbar_arrive(&s.p_full[bb]);
-      if (threadIdx.x == 0) MT_STAMP(i, 6);
+      if ((threadIdx.x & 31) == 0) {
+        if (leader) mbar_arrive(&s.p_full);
+        else mbar_arrive_cluster(pfull_leader);
+      }
     }
-    if (threadIdx.x == 0) bulk_wait0();  // the last copy has left this CTA
-    // ---- finalize (finalize_root): d2 re-based to the true d1, d3 = O / d2 ----
-    const float l_true = l * ex2_mufu((m_ref - m_true) * kLog2e);
-    const int64_t grow = static_cast<int64_t>(b) * HN + row;
-    if (h == 0) {
+    // ---- finalize (finalize_root): d2 = the two halves' sums re-based to d1 ----
+    named_bar_sync(1, 128);  // every half has read the last max exchange
+    s.xm[0][lane] = l;
+    named_bar_sync(1, 128);
+    const float lo = s.xm[0][lane & 63], hi = s.xm[0][(lane & 63) + 64];
+    const float l_ref = lo + hi;  // same operand order in both halves
+    const float l_true = l_ref * ex2_mufu((m_ref - m_true) * kLog2e);
+    const int64_t grow = static_cast<int64_t>(b) * HN + h * HC + row;
+    if (half == 0) {
       if (p.part_m == nullptr) {
         p.m[grow] = m_true;
         p.l[grow] = l_true;
@@ -348,13 +311,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       mbar_wait(&s.o_full, 0);
       tc_fence_after();
     }
-    const float inv_l = 1.f / l;
+    const float inv_l = 1.f / l_ref;
 #pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
+    for (int c = 0; c < 256 / 32; ++c) {
       uint32_t r[32];
       tmem_ld32(tO + lane_off + c * 32, r);
       tmem_ld_wait();
-      const int col = h * DH + c * 32;
+      const int col = 256 * (c >> 2) + 128 * half + 32 * (c & 3);
       if (p.part_o == nullptr) {
         uint4* dst = reinterpret_cast<uint4*>(p.o + grow * DV + col);
 #pragma unroll
@@ -377,7 +340,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   }
   tc_fence_before();
   cluster_sync();  // no remote traffic into a CTA that has exited
-  if (warp == 5) tmem_dealloc<512>(tmem);
+  if (warp == 5) tmem_dealloc_2sm<512>(tmem);
 }
 
 }  // namespace
@@ -399,12 +362,13 @@ int64_t mla_pick_splits(int64_t bs, int64_t skv, int64_t segments) {
 
 cudaError_t launch_mla_decode(const MlaArgs& a, cudaStream_t st) {
   if (!mla_supports(HN, a.skv, DV, DQK, a.nslices)) return cudaErrorNotSupported;
-  CUtensorMap tq, tkv;
+  CUtensorMap tq, tk, tv;
   const uint64_t qdims[2] = {DQK, static_cast<uint64_t>(a.bs * HN)};
   const uint64_t kdims[2] = {DQK, static_cast<uint64_t>(a.bs * a.skv)};
   const uint64_t strides[1] = {DQK * 2};
-  const uint32_t qbox[2] = {64, HN}, kbox[2] = {64, TK};
-  if (!make_tmap(&tq, a.q, 2, qdims, strides, qbox, 2) || !make_tmap(&tkv, a.kv, 2, kdims, strides, kbox, 2))
+  const uint32_t qbox[2] = {64, HC}, kbox[2] = {64, TK / 2}, vbox[2] = {64, 32};
+  if (!make_tmap(&tq, a.q, 2, qdims, strides, qbox, 2) || !make_tmap(&tk, a.kv, 2, kdims, strides, kbox, 2) ||
+      !make_tmap(&tv, a.kv, 2, kdims, strides, vbox, 2))
     return cudaErrorInvalidValue;
   Params p{};
   p.skv = a.skv;
@@ -422,7 +386,7 @@ cudaError_t launch_mla_decode(const MlaArgs& a, cudaStream_t st) {
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   dim3 grid(2, static_cast<unsigned>(a.bs), static_cast<unsigned>(a.nslices));
-  mla_decode_kernel<<<grid, NT, smem, st>>>(tq, tkv, p);
+  mla_decode_kernel<<<grid, NT, smem, st>>>(tq, tk, tv, p);
   return cudaGetLastError();
 }
 

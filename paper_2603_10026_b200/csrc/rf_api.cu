@@ -479,7 +479,7 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
       if (d.rows != 1) return bail(RF_ERR_SHAPE, "mla_decode: one query per head (rows = 1)");
       if (!rf::mla_supports(d.heads, d.len, d.free_len, d.producer_len, d.segments))
         return bail(RF_ERR_UNSUPPORTED,
-                    "mla_decode: heads 128, free_len 512, producer_len 576, (Skv / segments) % 32 == 0");
+                    "mla_decode: heads 128, free_len 512, producer_len 576, (Skv / segments) % 128 == 0");
       p->kernel = rf::Kernel::MlaDecode;
       p->rows_total = d.batch * d.heads;
       p->nsplit = rf::mla_pick_splits(d.batch, d.len, d.segments);
