@@ -17,11 +17,13 @@
 
 namespace rf {
 
-template <typename TO>
+// R = slices per round (<= R slices fold in 2 dependent round trips); the
+// caller picks the smallest R >= the slice count up to 16, which keeps the
+// register footprint (and with it the occupancy) proportional to the work.
+template <typename TO, int R = 16>
 __device__ __forceinline__ void fold_chunk(const float* pm, const float* pl, const float* po,
                                            int64_t nslices, int64_t stride, int64_t d, int64_t row,
                                            int64_t c4, float* m_out, float* l_out, TO* o_out) {
-  constexpr int R = 16;  // slices per round: <= 16 slices fold in 2 dependent round trips
   float l = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   float m = -INFINITY;

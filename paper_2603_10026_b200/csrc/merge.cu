@@ -12,7 +12,7 @@
 namespace rf {
 namespace {
 
-template <typename TO>
+template <typename TO, int R>
 __global__ void __launch_bounds__(128) merge_kernel(const float* __restrict__ pm, const float* __restrict__ pl,
                                                     const float* __restrict__ po, int64_t nslices, int64_t rows,
                                                     int64_t stride, int64_t d, float* __restrict__ m_out,
@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(128) merge_kernel(const float* __restrict__ pm
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t row = t / cpr;
   if (row >= rows) return;
-  fold_chunk(pm, pl, po, nslices, stride, d, row, t - row * cpr, m_out, l_out, o_out);
+  fold_chunk<TO, R>(pm, pl, po, nslices, stride, d, row, t - row * cpr, m_out, l_out, o_out);
 }
 
 }  // namespace
@@ -47,11 +47,21 @@ cudaError_t launch_attention_merge(const float* pm, const float* pl, const float
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (out_dtype == RF_BF16)
-    return cudaLaunchKernelEx(&cfg, merge_kernel<__nv_bfloat16>, pm, pl, po, nslices, rows, stride, d, m, l,
-                              static_cast<__nv_bfloat16*>(o));
-  return cudaLaunchKernelEx(&cfg, merge_kernel<float>, pm, pl, po, nslices, rows, stride, d, m, l,
-                            static_cast<float*>(o));
+  auto go = [&](auto kernel, auto* out) {
+    return cudaLaunchKernelEx(&cfg, kernel, pm, pl, po, nslices, rows, stride, d, m, l, out);
+  };
+  if (out_dtype == RF_BF16) {
+    auto* ob = static_cast<__nv_bfloat16*>(o);
+    if (nslices <= 2) return go(merge_kernel<__nv_bfloat16, 2>, ob);
+    if (nslices <= 4) return go(merge_kernel<__nv_bfloat16, 4>, ob);
+    if (nslices <= 8) return go(merge_kernel<__nv_bfloat16, 8>, ob);
+    return go(merge_kernel<__nv_bfloat16, 16>, ob);
+  }
+  auto* of = static_cast<float*>(o);
+  if (nslices <= 2) return go(merge_kernel<float, 2>, of);
+  if (nslices <= 4) return go(merge_kernel<float, 4>, of);
+  if (nslices <= 8) return go(merge_kernel<float, 8>, of);
+  return go(merge_kernel<float, 16>, of);
 }
 
 }  // namespace rf

@@ -37,8 +37,31 @@
 // of the peer's TMA completions to the leader (192 threads).
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "rf_internal.h"
 #include "sm100.cuh"
+
+// Timeline hooks (tools/trace_mla.py, built with -DRF_MLA_TRACE): globaltimer
+// stamps of the first and the last cluster of the grid.
+#ifdef RF_MLA_TRACE
+__device__ unsigned long long g_mla_trace[2][2][64][8];
+#define MT_STAMP(t, i)                                                                              \
+  do {                                                                                              \
+    const int c_ = (blockIdx.y | blockIdx.z) == 0 ? 0                                               \
+                   : (blockIdx.y == gridDim.y - 1 && blockIdx.z == gridDim.z - 1) ? 1 : -1;         \
+    if (c_ >= 0 && (t) < 64) {                                                                      \
+      unsigned long long v_;                                                                        \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v_));                                       \
+      g_mla_trace[c_][blockIdx.x][(t)][(i)] = v_;                                                   \
+    }                                                                                               \
+  } while (0)
+extern "C" int rf_mla_trace_read(unsigned long long* out) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, g_mla_trace, sizeof(g_mla_trace)));
+}
+#else
+#define MT_STAMP(t, i) do {} while (0)
+#endif
 
 namespace rf {
 namespace {
@@ -53,24 +76,34 @@ constexpr int NCH = DQK / 64;  // 64-column chunks per cache row
 constexpr int TK = 128;        // keys per tile
 constexpr int NKS = NCH;       // K stages per tile (this CTA's 64 keys x 64 columns)
 constexpr int NVS = 8;         // V stages per tile (2 halves x 4 x 32 keys x 128 columns)
-constexpr int NST = NKS + NVS; // ring stages = one tile
+#ifndef MLA_NKR
+#define MLA_NKR 9
+#define MLA_NVR 6
+#endif
+constexpr int NKR = MLA_NKR;   // K ring slots (1.4 tiles of K in flight)
+constexpr int NVR = MLA_NVR;   // V ring slots
 constexpr int STB = 8192;      // stage bytes
-constexpr int NT = 192;
+constexpr int NT = 256;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 struct Smem {
   uint8_t q[NCH][HC * 128];  // 9 x 8 KB
-  uint8_t ring[NST][STB];    // 17 x 8 KB
-  uint8_t p[2][HC * 128];    // P: keys [0, 64) and [64, 128), K-major SWIZZLE_128B
+  uint8_t kr[NKR][STB];      // K ring
+  uint8_t vr[NVR][STB];      // V ring
+  uint8_t p[2][2][HC * 128]; // P (double-buffered): keys [0, 64) and [64, 128), K-major SW128
   float xm[2][HN];           // row-half exchange (max per tile, then l)
-  uint64_t q_full, full[NST], empty[NST];
-  uint64_t s_full[2], p_full, pv_done, o_full;
+  uint64_t q_full, kfull[NKR], kempty[NKR], vfull[NVR], vempty[NVR];
+  uint64_t q_empty, s_full[2], p_full[2], pv_done[2], o_full, o_empty;
   uint32_t tmem_base;
 };
 
 struct Params {
-  int64_t skv, slice_len, rows_total;
+  int64_t skv, rows_total;
+  int tpb;        // 128-key tiles per batch
+  int64_t total;  // tiles of the whole grid (bs x tpb)
+  int clusters;   // CTA pairs (= gridDim.y)
+  int nslots;     // partial slots per batch (1: direct output)
   float scale;
   __nv_bfloat16* o;
   float* m;
@@ -80,6 +113,42 @@ struct Params {
   float* part_o;
 };
 
+// Range scheduling: the flattened (batch, tile) sequence is cut into
+// `clusters` contiguous ranges, one per CTA pair; a range covers one or more
+// batch segments, each of which writes a partial (m, l, O/l) state to slot
+// (cluster - first cluster of that batch).
+__host__ __device__ __forceinline__ int64_t range_start(int64_t k, int64_t clusters, int64_t total) {
+  return k * total / clusters;
+}
+__host__ __device__ __forceinline__ int64_t cluster_of(int64_t x, int64_t clusters, int64_t total) {
+  return ((x + 1) * clusters - 1) / total;
+}
+
+struct Segment {
+  int b, t0, t1, slot;
+  bool last_of_batch;
+};
+// Segment `i` of cluster k's range; false when the range is exhausted.
+__device__ __forceinline__ bool segment(const Params& p, int k, int i, Segment& sg) {
+  const int64_t x1 = range_start(k + 1, p.clusters, p.total);
+  int64_t x = range_start(k, p.clusters, p.total);
+  for (int j = 0;; ++j) {
+    if (x >= x1) return false;
+    const int b = static_cast<int>(x / p.tpb);
+    const int t0 = static_cast<int>(x % p.tpb);
+    const int64_t e = x1 < static_cast<int64_t>(b + 1) * p.tpb ? x1 : static_cast<int64_t>(b + 1) * p.tpb;
+    if (j == i) {
+      sg.b = b;
+      sg.t0 = t0;
+      sg.t1 = static_cast<int>(e - static_cast<int64_t>(b) * p.tpb);
+      sg.slot = static_cast<int>(k - cluster_of(static_cast<int64_t>(b) * p.tpb, p.clusters, p.total));
+      sg.last_of_batch = sg.t1 == p.tpb;
+      return true;
+    }
+    x = e;
+  }
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     mla_decode_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                       const __grid_constant__ CUtensorMap tv, const Params p) {
@@ -88,21 +157,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   const int warp = warp_id();
   const int h = static_cast<int>(cluster_ctarank());
   const bool leader = h == 0;
-  const int b = blockIdx.y;      // batch
-  const int slice = blockIdx.z;  // KV slice
-  const int64_t kv0 = static_cast<int64_t>(slice) * p.slice_len;
-  const int n_tiles = static_cast<int>(p.slice_len / TK);
+  const int k = blockIdx.y;  // this pair's range of (batch, tile)
+  if (threadIdx.x == 0) MT_STAMP(63, 0);
 
   if (threadIdx.x == 0) {
-    mbar_init(&s.q_full, leader ? 2 : 1);
-    for (int i = 0; i < NST; ++i) {
-      mbar_init(&s.full[i], leader ? 2 : 1);  // leader: own TMA + the peer's relay
-      mbar_init(&s.empty[i], 1);
+    // full barriers: the leader's copy is armed with both CTAs' bytes and
+    // completed by both CTAs' 2-SM TMA loads (the peer's copies are unused)
+    mbar_init(&s.q_full, 1);
+    mbar_init(&s.q_empty, 1);
+    for (int i = 0; i < NKR; ++i) {
+      mbar_init(&s.kfull[i], 1);
+      mbar_init(&s.kempty[i], 1);
     }
-    for (int k = 0; k < 2; ++k) mbar_init(&s.s_full[k], 1);
-    mbar_init(&s.p_full, 8);  // 4 softmax warps of each CTA (leader's copy is the one used)
-    mbar_init(&s.pv_done, 1);
+    for (int i = 0; i < NVR; ++i) {
+      mbar_init(&s.vfull[i], 1);
+      mbar_init(&s.vempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s.s_full[i], 1);
+      mbar_init(&s.p_full[i], 8);  // 4 softmax warps of each CTA (the leader's copy is used)
+      mbar_init(&s.pv_done[i], 1);
+    }
     mbar_init(&s.o_full, 1);
+    mbar_init(&s.o_empty, 8);  // both CTAs' epilogues have drained their O
     fence_barrier_init();
   }
   if (warp == 5) tmem_alloc_2sm<512>(&s.tmem_base);
@@ -112,161 +189,188 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   const uint32_t tmem = s.tmem_base;
   const uint32_t tS[2] = {tmem + 0, tmem + 64};
   const uint32_t tO = tmem + 256;  // + 128 j: V columns 256 j + ...
+  Segment sg;
 
   if (warp == 4) {
-    // ------------------------------------------------------------ TMA ----
+    // ------------------------------------------------------ TMA: Q, K ----
+    // 2-SM loads: bytes land in this CTA, completion on the leader's barrier
     if (elect_one()) {
       prefetch_tmap(&tq);
       prefetch_tmap(&tk);
+      int g = 0, nq = 0, gt = 0, qb = -1;
+      for (int si = 0; segment(p, k, si, sg); ++si) {
+        if (sg.b != qb) {  // a new batch: its Q once the previous batch's S MMAs are done
+          if (qb >= 0) mbar_wait(&s.q_empty, (nq - 1) & 1);
+          if (leader) mbar_arrive_expect_tx(&s.q_full, 2 * NCH * HC * 128);
+          for (int c = 0; c < NCH; ++c)
+            tma_load_2d_2sm(s.q[c], &tq, &s.q_full, c * 64, sg.b * HN + h * HC, kEvictFirst);
+          qb = sg.b;
+          ++nq;
+        }
+        const int32_t y0 = static_cast<int32_t>(static_cast<int64_t>(sg.b) * p.skv);
+        for (int t = sg.t0; t < sg.t1; ++t, ++gt)
+          for (int c = 0; c < NKS; ++c, ++g) {  // this CTA's 64 keys, all 576 columns (HBM)
+            const int sl = g % NKR;
+            mbar_wait(&s.kempty[sl], ((g / NKR) & 1) ^ 1);
+            if (c == 0) MT_STAMP(gt, 0);
+            if (c == NKS - 1) MT_STAMP(gt, 7);
+            if (leader) mbar_arrive_expect_tx(&s.kfull[sl], 2 * STB);
+            tma_load_2d_2sm(s.kr[sl], &tk, &s.kfull[sl], c * 64, y0 + t * TK + h * 64, kEvictNormal);
+          }
+      }
+    }
+  } else if (warp == 6) {
+    // --------------------------------------------------------- TMA: V ----
+    if (elect_one()) {
       prefetch_tmap(&tv);
-      mbar_arrive_expect_tx(&s.q_full, NCH * HC * 128);
-      for (int c = 0; c < NCH; ++c) tma_load_2d(s.q[c], &tq, &s.q_full, c * 64, b * HN + h * HC, kEvictFirst);
-      const int32_t y0 = static_cast<int32_t>(static_cast<int64_t>(b) * p.skv + kv0);
-      for (int t = 0; t < n_tiles; ++t) {
-        const uint32_t ph = (t & 1) ^ 1;
-        const int32_t key0 = y0 + t * TK;
-        for (int c = 0; c < NKS; ++c) {  // this CTA's 64 keys, all 576 columns (HBM)
-          mbar_wait(&s.empty[c], ph);
-          mbar_arrive_expect_tx(&s.full[c], STB);
-          tma_load_2d(s.ring[c], &tk, &s.full[c], c * 64, key0 + h * 64, kEvictNormal);
-        }
-        for (int v = 0; v < NVS; ++v) {  // all 128 keys, V columns 256 j + [128 h, +128) (L2)
-          const int st = NKS + v, j = v >> 2, kk = v & 3;
-          mbar_wait(&s.empty[st], ph);
-          mbar_arrive_expect_tx(&s.full[st], STB);
-          const int c0 = 4 * j + 2 * h;
-          tma_load_2d(s.ring[st], &tv, &s.full[st], c0 * 64, key0 + 32 * kk, kEvictFirst);
-          tma_load_2d(s.ring[st] + STB / 2, &tv, &s.full[st], (c0 + 1) * 64, key0 + 32 * kk, kEvictFirst);
-        }
+      int g = 0, gt = 0;
+      for (int si = 0; segment(p, k, si, sg); ++si) {
+        const int32_t y0 = static_cast<int32_t>(static_cast<int64_t>(sg.b) * p.skv);
+        for (int t = sg.t0; t < sg.t1; ++t, ++gt)
+          for (int v = 0; v < NVS; ++v, ++g) {  // all 128 keys, V columns 256 j + [128 h, +128) (L2)
+            const int sl = g % NVR, j = v >> 2, kk = v & 3;
+            mbar_wait(&s.vempty[sl], ((g / NVR) & 1) ^ 1);
+            if (v == 0) MT_STAMP(gt, 1);
+            if (leader) mbar_arrive_expect_tx(&s.vfull[sl], 2 * STB);
+            const int c0 = 4 * j + 2 * h;
+            const int32_t y = y0 + t * TK + 32 * kk;
+            tma_load_2d_2sm(s.vr[sl], &tv, &s.vfull[sl], c0 * 64, y, kEvictFirst);
+            tma_load_2d_2sm(s.vr[sl] + STB / 2, &tv, &s.vfull[sl], (c0 + 1) * 64, y, kEvictFirst);
+          }
       }
     }
   } else if (warp == 5) {
     if (leader) {
-      // ---------------------------------------------------------- MMA ----
+      // -------------------------------------------------------- MMA: S ----
+      // S_t may start once softmax t-2 has released P_{t-2} (it has then
+      // finished reading S buffer t & 1); P V runs from warp 7, so neither
+      // chain waits behind the other's loads (the tensor pipe interleaves the
+      // two warps' MMAs on separate accumulators).
       const uint32_t id_s = idesc_f16(HN, TK, kFmtBF16, false, false);
+      const bool el = elect_one();
+      int g = 0, gt = 0, nq = 0, qb = -1;
+      for (int si = 0; segment(p, k, si, sg); ++si) {
+        if (sg.b != qb) {
+          if (qb >= 0) {
+            if (el) mma_commit_2sm(&s.q_empty);  // the previous batch's S MMAs have read Q
+            __syncwarp();
+          }
+          mbar_wait(&s.q_full, nq & 1);
+          qb = sg.b;
+          ++nq;
+        }
+        for (int t = sg.t0; t < sg.t1; ++t, ++gt) {
+          if (gt >= 2) mbar_wait(&s.p_full[gt & 1], ((gt - 2) >> 1) & 1);
+          for (int c = 0; c < NKS; ++c, ++g) {
+            const int sl = g % NKR;
+            mbar_wait(&s.kfull[sl], (g / NKR) & 1);
+            tc_fence_after();
+            if (el) {
+              const uint32_t qa = smem_u32(s.q[c]), kb = smem_u32(s.kr[sl]);
+#pragma unroll
+              for (int k4 = 0; k4 < 4; ++k4)
+                mma_f16_ss_2sm(tS[gt & 1], sdesc_kmajor_sw128(qa + k4 * 32), sdesc_kmajor_sw128(kb + k4 * 32),
+                               id_s, (c | k4) != 0);
+              mma_commit_2sm(&s.kempty[sl]);
+              if (c + 1 == NKS) {
+                mma_commit_2sm(&s.s_full[gt & 1]);
+                MT_STAMP(gt, 2);
+              }
+            }
+            __syncwarp();
+          }
+        }
+      }
+    }
+  } else if (warp == 7) {
+    if (leader) {
+      // ------------------------------------------------------ MMA: P V ----
       const uint32_t id_o = idesc_f16(HN, 256, kFmtBF16, false, true);
       const bool el = elect_one();
-      auto issue_s = [&](int i) {  // S_i = Q K_i^T into S buffer i & 1
-        for (int c = 0; c < NKS; ++c) {
-          mbar_wait(&s.full[c], i & 1);
+      int g = 0, gt = 0;
+      for (int si = 0; segment(p, k, si, sg); ++si) {
+        for (int t = sg.t0; t < sg.t1; ++t, ++gt) {
+          mbar_wait(&s.p_full[gt & 1], (gt >> 1) & 1);
+          const bool first = t == sg.t0;
+          if (first && si > 0) mbar_wait(&s.o_empty, (si - 1) & 1);  // the previous segment's O drained
           tc_fence_after();
-          if (el) {
-            const uint32_t qa = smem_u32(s.q[c]), kb = smem_u32(s.ring[c]);
+          if (el) MT_STAMP(gt, 3);
+          const uint32_t pa = smem_u32(s.p[gt & 1][0]);
+          for (int v = 0; v < NVS; ++v, ++g) {
+            const int sl = g % NVR, j = v >> 2, kk = v & 3;
+            mbar_wait(&s.vfull[sl], (g / NVR) & 1);
+            tc_fence_after();
+            if (el) {
+              const uint32_t vb = smem_u32(s.vr[sl]);
 #pragma unroll
-            for (int k4 = 0; k4 < 4; ++k4)
-              mma_f16_ss_2sm(tS[i & 1], sdesc_kmajor_sw128(qa + k4 * 32), sdesc_kmajor_sw128(kb + k4 * 32), id_s,
-                             (c | k4) != 0);
-            mma_commit_2sm(&s.empty[c]);
-            if (c + 1 == NKS) mma_commit_2sm(&s.s_full[i & 1]);
-          }
-          __syncwarp();
-        }
-      };
-      auto issue_pv = [&](int i) {  // O += P_i V_i
-        mbar_wait(&s.p_full, i & 1);
-        tc_fence_after();
-        const uint32_t pa = smem_u32(s.p[0]);
-        for (int v = 0; v < NVS; ++v) {
-          const int st = NKS + v, j = v >> 2, kk = v & 3;
-          mbar_wait(&s.full[st], i & 1);
-          tc_fence_after();
-          if (el) {
-            const uint32_t vb = smem_u32(s.ring[st]);
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks)
-              mma_f16_ss_2sm(tO + 128 * j, sdesc_kmajor_sw128(pa + (kk >> 1) * (HC * 128) + (kk & 1) * 64 + ks * 32),
-                             sdesc_mnmajor_sw128(vb + ks * 2048, STB / 2), id_o, (i | kk | ks) != 0);
-            mma_commit_2sm(&s.empty[st]);
-            if (v + 1 == NVS) {
-              mma_commit_2sm(&s.pv_done);
-              if (i + 1 == n_tiles) mma_commit_2sm(&s.o_full);
+              for (int ks = 0; ks < 2; ++ks)
+                mma_f16_ss_2sm(tO + 128 * j,
+                               sdesc_kmajor_sw128(pa + (kk >> 1) * (HC * 128) + (kk & 1) * 64 + ks * 32),
+                               sdesc_mnmajor_sw128(vb + ks * 2048, STB / 2), id_o, !first || (kk | ks) != 0);
+              mma_commit_2sm(&s.vempty[sl]);
+              if (v + 1 == NVS) {
+                MT_STAMP(gt, 4);
+                mma_commit_2sm(&s.pv_done[gt & 1]);
+                if (t + 1 == sg.t1) mma_commit_2sm(&s.o_full);
+              }
             }
-          }
-          __syncwarp();
-        }
-      };
-      mbar_wait(&s.q_full, 0);
-      if (n_tiles > 0) issue_s(0);
-      // S_{i+1} (other S buffer, runs under softmax i) and P V_i in whichever
-      // order their inputs arrive: the tensor pipe executes in issue order,
-      // so a fixed S-first order would hold P V_i — and the V loads of tile
-      // i + 1 behind it — until tile i + 1's first K stage has landed.
-      for (int i = 0; i < n_tiles; ++i) {
-        bool s_next = i + 1 >= n_tiles;
-        for (;;) {
-          int pick = 0;
-          if (lane_id() == 0) {
-            if (!s_next && mbar_try_wait(&s.full[0], (i + 1) & 1)) pick = 1;
-            else if (mbar_try_wait(&s.p_full, i & 1)) pick = 2;
-          }
-          pick = __shfl_sync(0xffffffffu, pick, 0);
-          if (pick == 1) {
-            issue_s(i + 1);
-            s_next = true;
-          } else if (pick == 2) {
-            issue_pv(i);
-            break;
+            __syncwarp();
           }
         }
-        if (!s_next) issue_s(i + 1);
       }
-    } else if (elect_one()) {
-      // relay: this CTA's TMA stages have landed -> the leader's barriers
-      mbar_wait(&s.q_full, 0);
-      mbar_arrive_cluster(mapa_shared(smem_u32(&s.q_full), 0));
-      for (int t = 0; t < n_tiles; ++t)
-        for (int st = 0; st < NST; ++st) {
-          mbar_wait(&s.full[st], t & 1);
-          mbar_arrive_cluster(mapa_shared(smem_u32(&s.full[st]), 0));
-        }
     }
-  } else {
+  } else if (warp < 4) {
     // -------------------------- softmax / correction / epilogue (lane = thread) --
     const int lane = threadIdx.x;  // TMEM lane: row lane % 64, keys / V columns half lane / 64
     const int row = lane & (HC - 1), half = lane >> 6;
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
     const float c1 = p.scale * kLog2e;
-    const uint32_t p_row = smem_u32(s.p[half]) + (row >> 3) * 1024 + (row & 7) * 128;
-    const uint32_t pfull_leader = mapa_shared(smem_u32(&s.p_full), 0);
-    float m_true = -INFINITY, m_ref = -INFINITY, l = 0.f;
-    for (int i = 0; i < n_tiles; ++i) {
-      const int bb = i & 1;
-      mbar_wait(&s.s_full[bb], (i >> 1) & 1);
-      tc_fence_after();
-      uint32_t sv[2][32];
-      tmem_ld32(tS[bb] + lane_off, sv[0]);
-      tmem_ld32(tS[bb] + lane_off + 32, sv[1]);
-      tmem_ld_wait();
-      float mx = __uint_as_float(sv[0][0]);
-#pragma unroll
-      for (int j = 1; j < 64; ++j) mx = fmaxf(mx, __uint_as_float(sv[j >> 5][j & 31]));
-      s.xm[bb][lane] = mx;
-      named_bar_sync(1, 128);
-      mx = fmaxf(mx, s.xm[bb][lane ^ 64]);
-      m_true = fmaxf(m_true, mx * p.scale);
-      const bool need = (m_true - m_ref) * kLog2e > kRescaleThreshold;  // same in both halves
-      float alpha = 1.f;
-      if (need) {
-        alpha = ex2_mufu((m_ref - m_true) * kLog2e);  // 0 on the first tile
-        l *= alpha;
-        m_ref = m_true;
-      }
-      const float nmb = -m_ref * kLog2e;
-      uint32_t pk[32];
-      float rs = 0.f;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float p0 = ex2_mufu(fmaf(__uint_as_float(sv[j >> 4][(2 * j) & 31]), c1, nmb));
-        const float p1 = ex2_mufu(fmaf(__uint_as_float(sv[j >> 4][(2 * j + 1) & 31]), c1, nmb));
-        rs += p0 + p1;
-        pk[j] = pack_bf16x2(p0, p1);
-      }
-      l += rs;
-      // P V_{i-1} has retired: the P buffer is free and O may be rescaled
-      if (i > 0) {
-        mbar_wait(&s.pv_done, (i - 1) & 1);
+    const uint32_t p_row = smem_u32(s.p[0][half]) + (row >> 3) * 1024 + (row & 7) * 128;
+    int gt = 0;
+    for (int si = 0; segment(p, k, si, sg); ++si) {
+      float m_true = -INFINITY, m_ref = -INFINITY, l = 0.f;
+      for (int t = sg.t0; t < sg.t1; ++t, ++gt) {
+        const int bb = gt & 1;
+        mbar_wait(&s.s_full[bb], (gt >> 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, need)) {
+        if (lane == 0) MT_STAMP(gt, 5);
+        uint32_t sv[2][32];
+        tmem_ld32(tS[bb] + lane_off, sv[0]);
+        tmem_ld32(tS[bb] + lane_off + 32, sv[1]);
+        tmem_ld_wait();
+        float mx = __uint_as_float(sv[0][0]);
+#pragma unroll
+        for (int j = 1; j < 64; ++j) mx = fmaxf(mx, __uint_as_float(sv[j >> 5][j & 31]));
+        s.xm[bb][lane] = mx;
+        named_bar_sync(1, 128);
+        mx = fmaxf(mx, s.xm[bb][lane ^ 64]);
+        m_true = fmaxf(m_true, mx * p.scale);
+        const bool need = (m_true - m_ref) * kLog2e > kRescaleThreshold;  // same in both halves
+        float alpha = 1.f;
+        if (need) {
+          alpha = ex2_mufu((m_ref - m_true) * kLog2e);  // 0 on the first tile
+          l *= alpha;
+          m_ref = m_true;
+        }
+        const float nmb = -m_ref * kLog2e;
+        uint32_t pk[32];
+        float rs = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float p0 = ex2_mufu(fmaf(__uint_as_float(sv[j >> 4][(2 * j) & 31]), c1, nmb));
+          const float p1 = ex2_mufu(fmaf(__uint_as_float(sv[j >> 4][(2 * j + 1) & 31]), c1, nmb));
+          rs += p0 + p1;
+          pk[j] = pack_bf16x2(p0, p1);
+        }
+        l += rs;
+        // P buffer gt & 1 is free once P V_{gt-2} has retired; O is rescaled
+        // (rarely) once P V_{gt-1} has. pv_done[i] completes for the P V of
+        // tiles with gt & 1 = i, and neither can run ahead: the next needs
+        // this thread's P.
+        const bool resc = t > sg.t0 && __any_sync(0xffffffffu, need);
+        if (resc) {
+          mbar_wait(&s.pv_done[(gt - 1) & 1], ((gt - 1) >> 1) & 1);
+          tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < 256 / 16; ++c) {
             uint32_t r[16];
@@ -278,66 +382,98 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
           }
           tmem_st_wait();
         }
-      }
+        if (gt > 1) mbar_wait(&s.pv_done[gt & 1], ((gt - 2) >> 1) & 1);
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        sts128(p_row + ((u ^ (row & 7)) << 4), make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) {
-        if (leader) mbar_arrive(&s.p_full);
-        else mbar_arrive_cluster(pfull_leader);
-      }
-    }
-    // ---- finalize (finalize_root): d2 = the two halves' sums re-based to d1 ----
-    named_bar_sync(1, 128);  // every half has read the last max exchange
-    s.xm[0][lane] = l;
-    named_bar_sync(1, 128);
-    const float lo = s.xm[0][lane & 63], hi = s.xm[0][(lane & 63) + 64];
-    const float l_ref = lo + hi;  // same operand order in both halves
-    const float l_true = l_ref * ex2_mufu((m_ref - m_true) * kLog2e);
-    const int64_t grow = static_cast<int64_t>(b) * HN + h * HC + row;
-    if (half == 0) {
-      if (p.part_m == nullptr) {
-        p.m[grow] = m_true;
-        p.l[grow] = l_true;
-      } else {
-        p.part_m[slice * p.rows_total + grow] = m_true;
-        p.part_l[slice * p.rows_total + grow] = l_true;
-      }
-    }
-    if (n_tiles > 0) {
-      mbar_wait(&s.o_full, 0);
-      tc_fence_after();
-    }
-    const float inv_l = 1.f / l_ref;
-#pragma unroll 1
-    for (int c = 0; c < 256 / 32; ++c) {
-      uint32_t r[32];
-      tmem_ld32(tO + lane_off + c * 32, r);
-      tmem_ld_wait();
-      const int col = 256 * (c >> 2) + 128 * half + 32 * (c & 3);
-      if (p.part_o == nullptr) {
-        uint4* dst = reinterpret_cast<uint4*>(p.o + grow * DV + col);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          uint4 w;
-          w.x = pack_bf16x2(__uint_as_float(r[8 * v + 0]) * inv_l, __uint_as_float(r[8 * v + 1]) * inv_l);
-          w.y = pack_bf16x2(__uint_as_float(r[8 * v + 2]) * inv_l, __uint_as_float(r[8 * v + 3]) * inv_l);
-          w.z = pack_bf16x2(__uint_as_float(r[8 * v + 4]) * inv_l, __uint_as_float(r[8 * v + 5]) * inv_l);
-          w.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]) * inv_l, __uint_as_float(r[8 * v + 7]) * inv_l);
-          dst[v] = w;
+        for (int u = 0; u < 8; ++u)
+          sts128(p_row + (gt & 1) * (2 * HC * 128) + ((u ^ (row & 7)) << 4),
+                 make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) {
+          if (leader) mbar_arrive(&s.p_full[gt & 1]);
+          else mbar_arrive_cluster(mapa_shared(smem_u32(&s.p_full[gt & 1]), 0));
         }
-      } else {
-        float4* dst = reinterpret_cast<float4*>(p.part_o + (slice * p.rows_total + grow) * DV + col);
+        if (lane == 0) MT_STAMP(gt, 6);
+      }
+      // ---- finalize (finalize_root): d2 = the two halves' sums re-based to d1 ----
+      named_bar_sync(1, 128);  // every half has read the last max exchange
+      s.xm[0][lane] = l;
+      named_bar_sync(1, 128);
+      const float l_ref = s.xm[0][row] + s.xm[0][row + 64];  // same operand order in both halves
+      named_bar_sync(1, 128);  // xm is free for the next segment
+      const float l_true = l_ref * ex2_mufu((m_ref - m_true) * kLog2e);
+      const int64_t grow = static_cast<int64_t>(sg.b) * HN + h * HC + row;
+      const bool direct = p.part_o == nullptr;
+      if (half == 0) {
+        if (direct) {
+          p.m[grow] = m_true;
+          p.l[grow] = l_true;
+        } else {
+          p.part_m[sg.slot * p.rows_total + grow] = m_true;
+          p.part_l[sg.slot * p.rows_total + grow] = l_true;
+          if (sg.last_of_batch)  // slots no range of this batch reaches drop out of the fold
+            for (int e = sg.slot + 1; e < p.nslots; ++e) {
+              p.part_m[e * p.rows_total + grow] = -INFINITY;
+              p.part_l[e * p.rows_total + grow] = 0.f;
+            }
+        }
+      }
+      mbar_wait(&s.o_full, si & 1);
+      tc_fence_after();
+      const float inv_l = 1.f / l_ref;
+#pragma unroll 1
+      for (int c = 0; c < 256 / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tO + lane_off + c * 32, r);
+        tmem_ld_wait();
+        if (c == 256 / 32 - 1) {  // O is in registers: the next segment's P V may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if ((threadIdx.x & 31) == 0) {
+            if (leader) mbar_arrive(&s.o_empty);
+            else mbar_arrive_cluster(mapa_shared(smem_u32(&s.o_empty), 0));
+          }
+        }
+        const int col = 256 * (c >> 2) + 128 * half + 32 * (c & 3);
+        if (direct) {
+          uint4* dst = reinterpret_cast<uint4*>(p.o + grow * DV + col);
 #pragma unroll
-        for (int v = 0; v < 8; ++v)
-          dst[v] = make_float4(__uint_as_float(r[4 * v]) * inv_l, __uint_as_float(r[4 * v + 1]) * inv_l,
-                               __uint_as_float(r[4 * v + 2]) * inv_l, __uint_as_float(r[4 * v + 3]) * inv_l);
+          for (int v = 0; v < 4; ++v) {
+            uint4 w;
+            w.x = pack_bf16x2(__uint_as_float(r[8 * v + 0]) * inv_l, __uint_as_float(r[8 * v + 1]) * inv_l);
+            w.y = pack_bf16x2(__uint_as_float(r[8 * v + 2]) * inv_l, __uint_as_float(r[8 * v + 3]) * inv_l);
+            w.z = pack_bf16x2(__uint_as_float(r[8 * v + 4]) * inv_l, __uint_as_float(r[8 * v + 5]) * inv_l);
+            w.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]) * inv_l, __uint_as_float(r[8 * v + 7]) * inv_l);
+            dst[v] = w;
+          }
+        } else {
+          // through this warp's 4 KB of the (idle) P buffers: row-per-lane
+          // float4 stores would touch 32 lines per instruction; re-read so
+          // that 8 lanes cover one row's 128 B (4 whole lines per store)
+          const uint32_t stg = smem_u32(s.p[0][0]) + warp * 4096;
+          const int wr = lane & 31;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            sts128(stg + wr * 128 + ((q ^ (wr & 7)) << 4),
+                   make_uint4(__float_as_uint(__uint_as_float(r[4 * q]) * inv_l),
+                              __float_as_uint(__uint_as_float(r[4 * q + 1]) * inv_l),
+                              __float_as_uint(__uint_as_float(r[4 * q + 2]) * inv_l),
+                              __float_as_uint(__uint_as_float(r[4 * q + 3]) * inv_l)));
+          __syncwarp();
+          float* base = p.part_o + (sg.slot * p.rows_total + grow - wr) * DV + col;  // this warp's row 0
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int rr = it * 4 + (wr >> 3), q = wr & 7;
+            const uint4 v = lds128(stg + rr * 128 + ((q ^ (rr & 7)) << 4));
+            *reinterpret_cast<uint4*>(base + rr * DV + 4 * q) = v;
+          }
+          __syncwarp();
+        }
       }
     }
   }
+  if (threadIdx.x == 0) MT_STAMP(63, 1);
   tc_fence_before();
   cluster_sync();  // no remote traffic into a CTA that has exited
   if (warp == 5) tmem_dealloc_2sm<512>(tmem);
@@ -346,22 +482,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
 }  // namespace
 
 bool mla_supports(int64_t heads, int64_t skv, int64_t dv, int64_t dqk, int64_t segments) {
-  return heads == HN && dv == DV && dqk == DQK && segments >= 1 && skv % segments == 0 &&
-         (skv / segments) % TK == 0 && skv / segments > 0;
+  return heads == HN && dv == DV && dqk == DQK && segments >= 1 && skv > 0 && skv % TK == 0;
 }
 
-// Slices launched: the reference's segments, each cut into c sub-slices of
-// >= 256 keys until the grid (2 halves x bs x slices) fills the GPU.
-int64_t mla_pick_splits(int64_t bs, int64_t skv, int64_t segments) {
-  int64_t n = segments;
-  const int64_t slice = skv / segments;
-  for (int64_t c = 2; c <= 64 && 2 * bs * n < 148; c *= 2)
-    if (slice % (c * TK) == 0 && slice / c >= 256) n = segments * c;
+namespace {
+constexpr int64_t kMaxClusters = 74;  // CTA pairs resident on a 148-SM B200
+
+int64_t slots_needed(int64_t bs, int64_t tpb, int64_t clusters) {
+  const int64_t total = bs * tpb;
+  int64_t n = 1;
+  for (int64_t b = 0; b < bs; ++b)
+    n = std::max(n, cluster_of((b + 1) * tpb - 1, clusters, total) - cluster_of(b * tpb, clusters, total) + 1);
   return n;
 }
 
+// The most CTA pairs (<= one per SM pair, <= one per tile) whose ranges cut
+// no batch into more than max_slots segments.
+int64_t pick_clusters(int64_t bs, int64_t tpb, int64_t max_slots) {
+  int64_t c = std::min(kMaxClusters, bs * tpb);
+  while (c > 1 && slots_needed(bs, tpb, c) > max_slots) --c;
+  return c;
+}
+}  // namespace
+
+// Partial slots per batch (the plan's split count): what range scheduling of
+// the whole grid over the resident CTA pairs needs. KV segments of the
+// reference are folded by the same closed form, so they need no slots of
+// their own.
+int64_t mla_pick_splits(int64_t bs, int64_t skv, int64_t segments) {
+  (void)segments;
+  const int64_t tpb = skv / TK;
+  return slots_needed(bs, tpb, std::min(kMaxClusters, bs * tpb));
+}
+
 cudaError_t launch_mla_decode(const MlaArgs& a, cudaStream_t st) {
-  if (!mla_supports(HN, a.skv, DV, DQK, a.nslices)) return cudaErrorNotSupported;
+  if (!mla_supports(HN, a.skv, DV, DQK, 1)) return cudaErrorNotSupported;
   CUtensorMap tq, tk, tv;
   const uint64_t qdims[2] = {DQK, static_cast<uint64_t>(a.bs * HN)};
   const uint64_t kdims[2] = {DQK, static_cast<uint64_t>(a.bs * a.skv)};
@@ -370,22 +525,29 @@ cudaError_t launch_mla_decode(const MlaArgs& a, cudaStream_t st) {
   if (!make_tmap(&tq, a.q, 2, qdims, strides, qbox, 2) || !make_tmap(&tk, a.kv, 2, kdims, strides, kbox, 2) ||
       !make_tmap(&tv, a.kv, 2, kdims, strides, vbox, 2))
     return cudaErrorInvalidValue;
+  const int64_t tpb = a.skv / TK;
+  const int64_t clusters = pick_clusters(a.bs, tpb, a.nslices);
   Params p{};
   p.skv = a.skv;
-  p.slice_len = a.skv / a.nslices;
   p.rows_total = a.rows_total;
+  p.tpb = static_cast<int>(tpb);
+  p.total = a.bs * tpb;
+  p.clusters = static_cast<int>(clusters);
+  p.nslots = static_cast<int>(a.nslices);
   p.scale = a.scale;
   p.o = static_cast<__nv_bfloat16*>(a.o);
   p.m = a.m;
   p.l = a.l;
-  p.part_m = a.part_m;
-  p.part_l = a.part_l;
-  p.part_o = a.part_o;
+  if (a.nslices > 1) {
+    p.part_m = a.part_m;
+    p.part_l = a.part_l;
+    p.part_o = a.part_o;
+  }
   const size_t smem = sizeof(Smem) + 1024;
   cudaError_t e = cudaFuncSetAttribute(mla_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  dim3 grid(2, static_cast<unsigned>(a.bs), static_cast<unsigned>(a.nslices));
+  dim3 grid(2, static_cast<unsigned>(clusters), 1);
   mla_decode_kernel<<<grid, NT, smem, st>>>(tq, tk, tv, p);
   return cudaGetLastError();
 }
