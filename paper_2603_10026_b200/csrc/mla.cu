@@ -56,11 +56,28 @@ __device__ unsigned long long g_mla_trace[2][2][64][8];
       g_mla_trace[c_][blockIdx.x][(t)][(i)] = v_;                                                   \
     }                                                                                               \
   } while (0)
+__device__ unsigned long long g_fold_trace[1024][3];
+__device__ unsigned long long g_cta_end[256];
 extern "C" int rf_mla_trace_read(unsigned long long* out) {
   return static_cast<int>(cudaMemcpyFromSymbol(out, g_mla_trace, sizeof(g_mla_trace)));
 }
+extern "C" int rf_mla_end_trace_read(unsigned long long* out) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, g_cta_end, sizeof(g_cta_end)));
+}
+extern "C" int rf_mla_fold_trace_read(unsigned long long* out) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, g_fold_trace, sizeof(g_fold_trace)));
+}
+#define FT_STAMP(i)                                                                   \
+  do {                                                                                \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {                                      \
+      unsigned long long v_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v_));                         \
+      g_fold_trace[blockIdx.x][(i)] = v_;                                             \
+    }                                                                                 \
+  } while (0)
 #else
 #define MT_STAMP(t, i) do {} while (0)
+#define FT_STAMP(i) do {} while (0)
 #endif
 
 namespace rf {
@@ -101,7 +118,7 @@ struct Smem {
 struct Params {
   int64_t skv, rows_total;
   int tpb;        // 128-key tiles per batch
-  int64_t total;  // tiles of the whole grid (bs x tpb)
+  int64_t total;  // cost units of the whole grid (bs x (tpb + kSegCost))
   int clusters;   // CTA pairs (= gridDim.y)
   int nslots;     // partial slots per batch (1: direct output)
   float scale;
@@ -116,49 +133,150 @@ struct Params {
 // Range scheduling: the flattened (batch, tile) sequence is cut into
 // `clusters` contiguous ranges, one per CTA pair; a range covers one or more
 // batch segments, each of which writes a partial (m, l, O/l) state to slot
-// (cluster - first cluster of that batch).
-__host__ __device__ __forceinline__ int64_t range_start(int64_t k, int64_t clusters, int64_t total) {
-  return k * total / clusters;
+// (cluster - first cluster of that batch). Ranges are balanced in a cost
+// space where every batch starts with kSegCost virtual tiles: a cluster that
+// crosses into a new batch pays a Q reload (72 KB, no second Q buffer fits)
+// and one more epilogue, measured at about two tiles' time.
+constexpr int64_t kSegCost = 2;
+__host__ __device__ __forceinline__ int64_t range_start(int64_t k, int64_t clusters, int64_t units) {
+  return k * units / clusters;
 }
-__host__ __device__ __forceinline__ int64_t cluster_of(int64_t x, int64_t clusters, int64_t total) {
-  return ((x + 1) * clusters - 1) / total;
+__host__ __device__ __forceinline__ int64_t cluster_of(int64_t u, int64_t clusters, int64_t units) {
+  return ((u + 1) * clusters - 1) / units;
+}
+// First / last cluster holding tiles of batch b (w = tpb + kSegCost).
+__host__ __device__ __forceinline__ int64_t first_cluster(int64_t b, int64_t w, int64_t clusters, int64_t units) {
+  return cluster_of(b * w + kSegCost, clusters, units);
+}
+__host__ __device__ __forceinline__ int64_t last_cluster(int64_t b, int64_t w, int64_t clusters, int64_t units) {
+  return cluster_of((b + 1) * w - 1, clusters, units);
 }
 
 struct Segment {
-  int b, t0, t1, slot;
-  bool last_of_batch;
+  int b, t0, t1, slot, nseg;  // nseg: segments (ranges) the batch is cut into
 };
 // Segment `i` of cluster k's range; false when the range is exhausted.
 __device__ __forceinline__ bool segment(const Params& p, int k, int i, Segment& sg) {
+  const int64_t w = p.tpb + kSegCost;
   const int64_t x1 = range_start(k + 1, p.clusters, p.total);
   int64_t x = range_start(k, p.clusters, p.total);
-  for (int j = 0;; ++j) {
-    if (x >= x1) return false;
-    const int b = static_cast<int>(x / p.tpb);
-    const int t0 = static_cast<int>(x % p.tpb);
-    const int64_t e = x1 < static_cast<int64_t>(b + 1) * p.tpb ? x1 : static_cast<int64_t>(b + 1) * p.tpb;
-    if (j == i) {
-      sg.b = b;
-      sg.t0 = t0;
-      sg.t1 = static_cast<int>(e - static_cast<int64_t>(b) * p.tpb);
-      sg.slot = static_cast<int>(k - cluster_of(static_cast<int64_t>(b) * p.tpb, p.clusters, p.total));
-      sg.last_of_batch = sg.t1 == p.tpb;
+  for (int j = 0; x < x1;) {
+    const int64_t b = x / w;
+    const int64_t lo = x > b * w + kSegCost ? x : b * w + kSegCost;
+    const int64_t hi = x1 < (b + 1) * w ? x1 : (b + 1) * w;
+    x = (b + 1) * w;
+    if (hi <= lo) continue;  // only the batch's virtual head
+    if (j++ == i) {
+      sg.b = static_cast<int>(b);
+      sg.t0 = static_cast<int>(lo - b * w - kSegCost);
+      sg.t1 = static_cast<int>(hi - b * w - kSegCost);
+      const int64_t k0 = first_cluster(b, w, p.clusters, p.total);
+      sg.slot = static_cast<int>(k - k0);
+      sg.nseg = static_cast<int>(last_cluster(b, w, p.clusters, p.total) - k0 + 1);
       return true;
     }
-    x = e;
   }
+  return false;
+}
+
+// Fold of each batch's segment partials (the Multi-Segment merge,
+// incr_push_child / acceptance.cpp:162-178 closed form, as fold.cuh, in slot
+// order) over exactly the segments the batch was cut into. A programmatic
+// dependent of mla_decode_kernel: the decode kernel triggers its dependents
+// at start, so fold CTAs (no shared memory, <= 64 registers) are already
+// resident next to it when it drains; griddepcontrol.wait orders the reads.
+// CTA = 8 heads of one batch; thread = (head, 4 float4 columns 512 B apart:
+// a warp reads whole rows); two slots' (m, l, O) loads per round trip.
+constexpr int FR = 8;  // heads per fold CTA
+__global__ void __launch_bounds__(256, 4) mla_fold_kernel(const Params p) {
+  FT_STAMP(0);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  FT_STAMP(1);
+  const int b = blockIdx.x / (HN / FR), blk = blockIdx.x % (HN / FR);
+  const int64_t w = p.tpb + kSegCost;
+  const int ns = static_cast<int>(last_cluster(b, w, p.clusters, p.total) - first_cluster(b, w, p.clusters, p.total) + 1);
+  if (ns == 1) return;  // written directly by its only segment
+  const int r = threadIdx.x >> 5, c0 = threadIdx.x & 31;
+  const int64_t grow = static_cast<int64_t>(b) * HN + blk * FR + r;
+  // one round trip per 2 slots: (m, l) and the O rows are loaded together
+  // (every slot of the batch is written, so its O row is valid); the slot
+  // maxima are folded by re-basing, as fold.cuh does across its rounds
+  float m = -INFINITY, L = 0.f;
+  float4 acc[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int e0 = 0; e0 < ns; e0 += 2) {
+    float ms[2], ls[2];
+    float4 o[2][4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int e = e0 + j < ns ? e0 + j : ns - 1;  // (duplicates are dropped below)
+      ms[j] = __ldcg(p.part_m + e * p.rows_total + grow);
+      ls[j] = __ldcg(p.part_l + e * p.rows_total + grow);
+      const float4* src = reinterpret_cast<const float4*>(p.part_o + (e * p.rows_total + grow) * DV) + c0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[j][i] = __ldcg(src + 32 * i);
+    }
+    float mr = m;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (e0 + j < ns) mr = fmaxf(mr, ms[j]);
+    if (mr != m && L != 0.f) {  // re-base what is accumulated
+      const float f = __expf(m - mr);
+      L *= f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[i].x *= f;
+        acc[i].y *= f;
+        acc[i].z *= f;
+        acc[i].w *= f;
+      }
+    }
+    m = mr;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float w = e0 + j < ns && ls[j] != 0.f ? ls[j] * __expf(ms[j] - m) : 0.f;
+      if (w == 0.f) continue;
+      L += w;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[i].x = fmaf(o[j][i].x, w, acc[i].x);
+        acc[i].y = fmaf(o[j][i].y, w, acc[i].y);
+        acc[i].z = fmaf(o[j][i].z, w, acc[i].z);
+        acc[i].w = fmaf(o[j][i].w, w, acc[i].w);
+      }
+    }
+  }
+  const float inv = 1.f / L;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint2 v;
+    v.x = pack_bf16x2(acc[i].x * inv, acc[i].y * inv);
+    v.y = pack_bf16x2(acc[i].z * inv, acc[i].w * inv);
+    *reinterpret_cast<uint2*>(p.o + grow * DV + 4 * (c0 + 32 * i)) = v;
+  }
+  if (c0 == 0) {
+    p.m[grow] = m;
+    p.l[grow] = L;
+  }
+  FT_STAMP(2);
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     mla_decode_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                       const __grid_constant__ CUtensorMap tv, const Params p) {
-  extern __shared__ uint8_t smem_raw[];
-  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // No alignment slack: the dynamic window starts 1024-aligned (no static
+  // shared memory), and every byte counts — the decode CTA leaves exactly
+  // enough of the SM's 228 KB for mla_fold_kernel CTAs to become resident.
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if ((smem_u32(smem_raw) & 1023) != 0) __trap();
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   const int warp = warp_id();
   const int h = static_cast<int>(cluster_ctarank());
   const bool leader = h == 0;
   const int k = blockIdx.y;  // this pair's range of (batch, tile)
   if (threadIdx.x == 0) MT_STAMP(63, 0);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // mla_fold_kernel may become resident
 
   if (threadIdx.x == 0) {
     // full barriers: the leader's copy is armed with both CTAs' bytes and
@@ -186,6 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
+  if (threadIdx.x == 0) MT_STAMP(63, 2);
   const uint32_t tmem = s.tmem_base;
   const uint32_t tS[2] = {tmem + 0, tmem + 64};
   const uint32_t tO = tmem + 256;  // + 128 j: V columns 256 j + ...
@@ -201,6 +320,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       for (int si = 0; segment(p, k, si, sg); ++si) {
         if (sg.b != qb) {  // a new batch: its Q once the previous batch's S MMAs are done
           if (qb >= 0) mbar_wait(&s.q_empty, (nq - 1) & 1);
+          if (qb < 0) MT_STAMP(63, 3);
           if (leader) mbar_arrive_expect_tx(&s.q_full, 2 * NCH * HC * 128);
           for (int c = 0; c < NCH; ++c)
             tma_load_2d_2sm(s.q[c], &tq, &s.q_full, c * 64, sg.b * HN + h * HC, kEvictFirst);
@@ -404,7 +524,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       named_bar_sync(1, 128);  // xm is free for the next segment
       const float l_true = l_ref * ex2_mufu((m_ref - m_true) * kLog2e);
       const int64_t grow = static_cast<int64_t>(sg.b) * HN + h * HC + row;
-      const bool direct = p.part_o == nullptr;
+      const bool direct = sg.nseg == 1;  // the whole batch is this segment: final outputs
       if (half == 0) {
         if (direct) {
           p.m[grow] = m_true;
@@ -412,11 +532,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
         } else {
           p.part_m[sg.slot * p.rows_total + grow] = m_true;
           p.part_l[sg.slot * p.rows_total + grow] = l_true;
-          if (sg.last_of_batch)  // slots no range of this batch reaches drop out of the fold
-            for (int e = sg.slot + 1; e < p.nslots; ++e) {
-              p.part_m[e * p.rows_total + grow] = -INFINITY;
-              p.part_l[e * p.rows_total + grow] = 0.f;
-            }
         }
       }
       mbar_wait(&s.o_full, si & 1);
@@ -466,7 +581,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
           for (int it = 0; it < 8; ++it) {
             const int rr = it * 4 + (wr >> 3), q = wr & 7;
             const uint4 v = lds128(stg + rr * 128 + ((q ^ (rr & 7)) << 4));
-            *reinterpret_cast<uint4*>(base + rr * DV + 4 * q) = v;
+            stg128_hint(base + rr * DV + 4 * q, v, kEvictLast);  // kept in L2 for the fold
           }
           __syncwarp();
         }
@@ -474,6 +589,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     }
   }
   if (threadIdx.x == 0) MT_STAMP(63, 1);
+#ifdef RF_MLA_TRACE
+  if (threadIdx.x == 0) {
+    unsigned long long v_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v_));
+    g_cta_end[blockIdx.y * 2 + blockIdx.x] = v_;
+  }
+#endif
   tc_fence_before();
   cluster_sync();  // no remote traffic into a CTA that has exited
   if (warp == 5) tmem_dealloc_2sm<512>(tmem);
@@ -489,10 +611,10 @@ namespace {
 constexpr int64_t kMaxClusters = 74;  // CTA pairs resident on a 148-SM B200
 
 int64_t slots_needed(int64_t bs, int64_t tpb, int64_t clusters) {
-  const int64_t total = bs * tpb;
+  const int64_t w = tpb + kSegCost, units = bs * w;
   int64_t n = 1;
   for (int64_t b = 0; b < bs; ++b)
-    n = std::max(n, cluster_of((b + 1) * tpb - 1, clusters, total) - cluster_of(b * tpb, clusters, total) + 1);
+    n = std::max(n, last_cluster(b, w, clusters, units) - first_cluster(b, w, clusters, units) + 1);
   return n;
 }
 
@@ -531,25 +653,35 @@ cudaError_t launch_mla_decode(const MlaArgs& a, cudaStream_t st) {
   p.skv = a.skv;
   p.rows_total = a.rows_total;
   p.tpb = static_cast<int>(tpb);
-  p.total = a.bs * tpb;
+  p.total = a.bs * (tpb + kSegCost);  // cost units
   p.clusters = static_cast<int>(clusters);
   p.nslots = static_cast<int>(a.nslices);
   p.scale = a.scale;
   p.o = static_cast<__nv_bfloat16*>(a.o);
   p.m = a.m;
   p.l = a.l;
-  if (a.nslices > 1) {
-    p.part_m = a.part_m;
-    p.part_l = a.part_l;
-    p.part_o = a.part_o;
-  }
-  const size_t smem = sizeof(Smem) + 1024;
+  p.part_m = a.part_m;
+  p.part_l = a.part_l;
+  p.part_o = a.part_o;
+  const size_t smem = sizeof(Smem);
+  static_assert(sizeof(Smem) <= 226 * 1024, "leave 1 KB + 1 KB reserved for a co-resident fold CTA");
   cudaError_t e = cudaFuncSetAttribute(mla_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   dim3 grid(2, static_cast<unsigned>(clusters), 1);
   mla_decode_kernel<<<grid, NT, smem, st>>>(tq, tk, tv, p);
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (e != cudaSuccess || a.nslices == 1) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(a.bs * (HN / FR)));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, mla_fold_kernel, p);
 }
 
 }  // namespace rf

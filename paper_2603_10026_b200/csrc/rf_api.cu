@@ -280,18 +280,13 @@ rf_status run_range(const rf_plan* p, const rf_io* io, int64_t u0, int64_t nu, c
       a.nslices = p->nsplit;
       a.rows_total = p->rows_total;
       a.scale = static_cast<float>(d.softmax_scale);
-      if (p->nsplit > 1) {
+      if (p->nsplit > 1) {  // segment partials, folded by mla_fold_kernel (PDL)
         a.part_m = p->ws_m + u0 * hn;
         a.part_l = p->ws_l + u0 * hn;
         a.part_o = p->ws_o + u0 * hn * d.free_len;
       }
       cudaError_t e = rf::launch_mla_decode(a, st);
       if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("mla launch: ") + cudaGetErrorString(e));
-      if (p->nsplit > 1) {
-        e = rf::launch_attention_merge(a.part_m, a.part_l, a.part_o, p->nsplit, nu * hn, p->rows_total,
-                                       d.free_len, a.m, a.l, a.o, RF_BF16, st);
-        if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("merge launch: ") + cudaGetErrorString(e));
-      }
       return RF_OK;
     }
     case RF_PATTERN_MOE_ROUTER: {

@@ -39,9 +39,27 @@ t0 = min(at(c, x, 63, 0) for c in range(2) for x in range(2))
 us = lambda v: round((v - t0) / 1000, 2) if v else None  # noqa: E731
 for c in range(2):
     print(f"cluster {'first' if c == 0 else 'last'}: start {us(at(c, 0, 63, 0))} / {us(at(c, 1, 63, 0))}"
-          f"  end {us(at(c, 0, 63, 1))} / {us(at(c, 1, 63, 1))}")
+          f"  end {us(at(c, 0, 63, 1))} / {us(at(c, 1, 63, 1))}  setup done {us(at(c, 0, 63, 2))}"
+          f"  first Q issue {us(at(c, 0, 63, 3))}")
     print(" tile |   K0    K8    V0 |    S    Pin    PV | Srdy0  Prel0 | Srdy1  Prel1")
     for i in range(16):
         print(f" {i:4d} | {us(at(c, 0, i, 0))} {us(at(c, 0, i, 7))} {us(at(c, 0, i, 1))} | "
               f"{us(at(c, 0, i, 2))} {us(at(c, 0, i, 3))} {us(at(c, 0, i, 4))} | "
               f"{us(at(c, 0, i, 5))} {us(at(c, 0, i, 6))} | {us(at(c, 1, i, 5))} {us(at(c, 1, i, 6))}")
+
+fb = (ctypes.c_ulonglong * (1024 * 3))()
+if hasattr(lib, "rf_mla_fold_trace_read") and lib.rf_mla_fold_trace_read(fb) == 0:
+    f = list(fb)
+    n = B * 16
+    st = sorted(us(f[3 * i]) for i in range(n) if f[3 * i])
+    go = sorted(us(f[3 * i + 1]) for i in range(n) if f[3 * i + 1])
+    en = sorted(us(f[3 * i + 2]) for i in range(n) if f[3 * i + 2])
+    q = lambda v: [v[0], v[len(v) // 4], v[len(v) // 2], v[3 * len(v) // 4], v[-1]] if v else None  # noqa: E731
+    print("fold CTAs: resident at (min/q1/med/q3/max)", q(st))
+    print("           batch ready", q(go))
+    print("           done       ", q(en))
+
+eb = (ctypes.c_ulonglong * 256)()
+if hasattr(lib, "rf_mla_end_trace_read") and lib.rf_mla_end_trace_read(eb) == 0:
+    e = sorted(us(v) for v in list(eb)[:148] if v)
+    print("decode CTAs end (min/q1/med/q3/max):", [e[0], e[len(e) // 4], e[len(e) // 2], e[3 * len(e) // 4], e[-1]])
