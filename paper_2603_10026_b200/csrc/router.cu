@@ -40,8 +40,16 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 #define RT_STAMP(i) do { if (threadIdx.x % 32 == 0) g_router_trace[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + (i)] = gtime(); } while (0)
+__device__ unsigned long long g_route_trace[1024][3];
+extern "C" int rf_router_trace_read(unsigned long long* gemm, unsigned long long* route) {
+  cudaError_t e = cudaMemcpyFromSymbol(gemm, g_router_trace, sizeof(g_router_trace));
+  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(route, g_route_trace, sizeof(g_route_trace));
+  return static_cast<int>(e);
+}
+#define RR_STAMP(i) do { if (threadIdx.x == 0 && blockIdx.x < 1024) g_route_trace[blockIdx.x][(i)] = gtime(); } while (0)
 #else
 #define RT_STAMP(i) do {} while (0)
+#define RR_STAMP(i) do {} while (0)
 #endif
 
 namespace rf {
@@ -170,7 +178,9 @@ __global__ void __launch_bounds__(NT, 1)
   // splits of this row tile): CTA rank q folds rows [q*128/cs, (q+1)*128/cs)
   // of all cs staged partials in rank (= split) order through distributed
   // shared memory and writes one partial per cluster, coalesced. ----
+  if (threadIdx.x == 0) RT_STAMP(6);
   cluster_sync();  // every CTA's staged partial is visible cluster-wide
+  if (threadIdx.x == 0) RT_STAMP(7);
   if (warp < 4) {
     constexpr int RS = EN + 4;
     const uint32_t stage_u32 = smem_u32(s.a[0]);
@@ -219,7 +229,9 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
                                                            int64_t rows, int64_t part_stride, float* __restrict__ d1,
                                                            float* __restrict__ d2, int2* __restrict__ topk,
                                                            float* __restrict__ scores) {
+  RR_STAMP(0);
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  RR_STAMP(1);
   constexpr int PER = EN / 32;  // experts per lane: e = lane + 32 j
   const int lane = threadIdx.x & 31;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
@@ -238,6 +250,7 @@ __global__ void __launch_bounds__(256) router_route_kernel(const float* __restri
     for (int j = 0; j < PER; ++j) scores[row * EN + lane + 32 * j] = x[j];
   }
   warp_route<PER, K>(x, EN, lane, d1 + row, d2 + row, topk + row * K);
+  RR_STAMP(2);
 }
 
 template <int EN>
