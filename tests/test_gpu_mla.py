@@ -37,6 +37,14 @@ def test_mla_decode_paper_shapes(B, skv):
     _check(B, skv, 1, seed=B * 10000 + skv)
 
 
+@pytest.mark.parametrize("B,skv", [(80, 1024), (3, 128), (5, 384), (148, 256)])
+def test_mla_decode_range_schedule(B, skv):
+    """Range scheduling edge cases: more batches than CTA pairs (some batches
+    inside one range -> written directly, others cut -> folded: both paths in
+    one launch), one-tile batches, ragged ranges."""
+    _check(B, skv, 1, seed=B * 7 + skv)
+
+
 @pytest.mark.parametrize("segments", [2, 4, 8])
 def test_mla_decode_multisegment(segments):
     _check(2, 2048, segments, seed=segments)
