@@ -33,9 +33,14 @@
 #include <cuda_bf16.h>
 
 #include "rf_internal.h"
+#include "sm100.cuh"
 
 namespace rf {
 namespace {
+
+using sm100::f2;
+using sm100::f2split;
+using sm100::ffma2;
 
 constexpr int BM = 64;   // query rows per CTA
 constexpr int BN = 64;   // keys per tile
@@ -165,12 +170,13 @@ __global__ void __launch_bounds__(NT, D <= 64 ? 2 : 1) attn_f32_kernel(AttnArgs 
     __syncthreads();
     if (t0 + BN < kv1) fetch(t0 + BN);  // next tile in flight during this tile's math
 
-    // S block: rows ty + 16 r, keys tx + 16 j
-    float s[TR][TK];
+    // S block: rows ty + 16 r, keys tx + 16 j. Packed FFMA2 over (even,
+    // odd) d pairs: half the FMA instructions (the kernel is issue-bound)
+    uint64_t s2[TR][TK];
 #pragma unroll
     for (int r = 0; r < TR; ++r)
 #pragma unroll
-      for (int j = 0; j < TK; ++j) s[r][j] = 0.f;
+      for (int j = 0; j < TK; ++j) s2[r][j] = 0ull;
 #pragma unroll 4
     for (int dd = 0; dd < D; dd += 4) {
       float4 qv[TR], kv[TK];
@@ -182,12 +188,19 @@ __global__ void __launch_bounds__(NT, D <= 64 ? 2 : 1) attn_f32_kernel(AttnArgs 
       for (int r = 0; r < TR; ++r)
 #pragma unroll
         for (int j = 0; j < TK; ++j) {
-          s[r][j] = fmaf(qv[r].x, kv[j].x, s[r][j]);
-          s[r][j] = fmaf(qv[r].y, kv[j].y, s[r][j]);
-          s[r][j] = fmaf(qv[r].z, kv[j].z, s[r][j]);
-          s[r][j] = fmaf(qv[r].w, kv[j].w, s[r][j]);
+          s2[r][j] = ffma2(f2(qv[r].x, qv[r].y), f2(kv[j].x, kv[j].y), s2[r][j]);
+          s2[r][j] = ffma2(f2(qv[r].z, qv[r].w), f2(kv[j].z, kv[j].w), s2[r][j]);
         }
     }
+    float s[TR][TK];
+#pragma unroll
+    for (int r = 0; r < TR; ++r)
+#pragma unroll
+      for (int j = 0; j < TK; ++j) {
+        float lo, hi;
+        f2split(s2[r][j], lo, hi);
+        s[r][j] = lo + hi;
+      }
     float corr[TR], inv_l[TR];
 #pragma unroll
     for (int r = 0; r < TR; ++r) {
@@ -226,6 +239,12 @@ __global__ void __launch_bounds__(NT, D <= 64 ? 2 : 1) attn_f32_kernel(AttnArgs 
 #pragma unroll
       for (int c = 0; c < TD; ++c) acc[r][c] = 0.f;
 if constexpr (VEC) {
+    // column pairs (4 tx + 2i, +1) of P V as packed FFMA2
+    uint64_t acc2[TR][TD / 2];
+#pragma unroll
+    for (int r = 0; r < TR; ++r)
+#pragma unroll
+      for (int c = 0; c < TD / 2; ++c) acc2[r][c] = 0ull;
 #pragma unroll 2
     for (int kk = 0; kk < BN; kk += 4) {
       float4 pv[TR];
@@ -240,16 +259,19 @@ if constexpr (VEC) {
 #pragma unroll
         for (int r = 0; r < TR; ++r) {
           const float pr = f4_at(pv[r], u);
+          const uint64_t pp = f2(pr, pr);
 #pragma unroll
           for (int c4 = 0; c4 < TD4; ++c4) {
-            acc[r][4 * c4 + 0] = fmaf(pr, vv[c4].x, acc[r][4 * c4 + 0]);
-            acc[r][4 * c4 + 1] = fmaf(pr, vv[c4].y, acc[r][4 * c4 + 1]);
-            acc[r][4 * c4 + 2] = fmaf(pr, vv[c4].z, acc[r][4 * c4 + 2]);
-            acc[r][4 * c4 + 3] = fmaf(pr, vv[c4].w, acc[r][4 * c4 + 3]);
+            acc2[r][2 * c4] = ffma2(pp, f2(vv[c4].x, vv[c4].y), acc2[r][2 * c4]);
+            acc2[r][2 * c4 + 1] = ffma2(pp, f2(vv[c4].z, vv[c4].w), acc2[r][2 * c4 + 1]);
           }
         }
       }
     }
+#pragma unroll
+    for (int r = 0; r < TR; ++r)
+#pragma unroll
+      for (int c = 0; c < TD / 2; ++c) f2split(acc2[r][c], acc[r][2 * c], acc[r][2 * c + 1]);
     } else {
 #pragma unroll 4
       for (int kk = 0; kk < BN; ++kk) {
