@@ -136,8 +136,8 @@ struct Params {
 // (cluster - first cluster of that batch). Ranges are balanced in a cost
 // space where every batch starts with kSegCost virtual tiles: a cluster that
 // crosses into a new batch pays a Q reload (72 KB, no second Q buffer fits)
-// and one more epilogue, measured at about two tiles' time.
-constexpr int64_t kSegCost = 2;
+// and one more epilogue, worth about three tiles' time.
+constexpr int64_t kSegCost = 3;  // A/B on L3: 0 -> 48.1, 1 -> 48.2, 2 -> 46.7, 3 -> 45.8, 4 -> 46.4 us
 __host__ __device__ __forceinline__ int64_t range_start(int64_t k, int64_t clusters, int64_t units) {
   return k * units / clusters;
 }
