@@ -97,6 +97,9 @@ constexpr int NVS = 8;         // V stages per tile (2 halves x 4 x 32 keys x 12
 #define MLA_NKR 9
 #define MLA_NVR 6
 #endif
+#ifndef MLA_NP
+#define MLA_NP 2
+#endif
 constexpr int NKR = MLA_NKR;   // K ring slots (1.4 tiles of K in flight)
 constexpr int NVR = MLA_NVR;   // V ring slots
 constexpr int STB = 8192;      // stage bytes
@@ -108,7 +111,7 @@ struct Smem {
   uint8_t q[NCH][HC * 128];  // 9 x 8 KB
   uint8_t kr[NKR][STB];      // K ring
   uint8_t vr[NVR][STB];      // V ring
-  uint8_t p[2][2][HC * 128]; // P (double-buffered): keys [0, 64) and [64, 128), K-major SW128
+  uint8_t p[MLA_NP][2][HC * 128]; // P buffers: keys [0, 64) and [64, 128), K-major SW128
   float xm[2][HN];           // row-half exchange (max per tile, then l)
   uint64_t q_full, kfull[NKR], kempty[NKR], vfull[NVR], vempty[NVR];
   uint64_t q_empty, s_full[2], p_full[2], pv_done[2], o_full, o_empty;
@@ -415,7 +418,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
           if (first && si > 0) mbar_wait(&s.o_empty, (si - 1) & 1);  // the previous segment's O drained
           tc_fence_after();
           if (el) MT_STAMP(gt, 3);
-          const uint32_t pa = smem_u32(s.p[gt & 1][0]);
+          const uint32_t pa = smem_u32(s.p[gt % MLA_NP][0]);
           for (int v = 0; v < NVS; ++v, ++g) {
             const int sl = g % NVR, j = v >> 2, kk = v & 3;
             mbar_wait(&s.vfull[sl], (g / NVR) & 1);
@@ -502,10 +505,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
           }
           tmem_st_wait();
         }
-        if (gt > 1) mbar_wait(&s.pv_done[gt & 1], ((gt - 2) >> 1) & 1);
+        if (MLA_NP == 2 && gt > 1) mbar_wait(&s.pv_done[gt & 1], ((gt - 2) >> 1) & 1);
+        if (MLA_NP == 1 && gt > 0 && !resc) mbar_wait(&s.pv_done[(gt - 1) & 1], ((gt - 1) >> 1) & 1);
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          sts128(p_row + (gt & 1) * (2 * HC * 128) + ((u ^ (row & 7)) << 4),
+          sts128(p_row + (gt % MLA_NP) * (2 * HC * 128) + ((u ^ (row & 7)) << 4),
                  make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
         fence_proxy_async_smem();
         tc_fence_before();
