@@ -662,7 +662,9 @@ namespace qnt2 {
 
 using qnt::BK;
 using qnt::BNQ;
-constexpr int SA = 2, SW = 3, S8 = 2;
+// ring depths (A/B on cfg4, TFLOP/s): SA/SW/S8 = 3/3/2 2284, 2/3/2 2271,
+// 2/3/3 2267, 2/4/2 2235, 3/2/3 2163
+constexpr int SA = 3, SW = 3, S8 = 2;
 constexpr int NT = 192;  // warps 0-3 quantiser + epilogue, 4 TMA, 5 MMA (leader) / relay (peer)
 constexpr int ABF_BYTES = BM * BK * 2;  // 32 KB
 constexpr int W_BYTES = 2 * 128 * BK;   // 32 KB: this CTA's halves of the two 256-row blocks
