@@ -54,7 +54,7 @@ using namespace sm100;
 
 constexpr int BM = 128;       // rows per Q tile
 constexpr int BN = 128;       // keys per KV tile
-constexpr int NSLOT = 4;      // K/V ring slots
+constexpr int NSLOT = 4;      // K/V ring slots (A/B on cfg2: 3 -> 1282, 4 -> 1323, 5 -> 1310 TFLOP/s)
 constexpr int NTHREADS = 320;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
