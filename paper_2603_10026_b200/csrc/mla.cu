@@ -185,9 +185,10 @@ __device__ __forceinline__ bool segment(const Params& p, int k, int i, Segment& 
 // Fold of each batch's segment partials (the Multi-Segment merge,
 // incr_push_child / acceptance.cpp:162-178 closed form, as fold.cuh, in slot
 // order) over exactly the segments the batch was cut into. A programmatic
-// dependent of mla_decode_kernel: the decode kernel triggers its dependents
-// at start, so fold CTAs (no shared memory, <= 64 registers) are already
-// resident next to it when it drains; griddepcontrol.wait orders the reads.
+// dependent of mla_decode_kernel (launch overlaps the decode grid's drain;
+// griddepcontrol.wait orders the reads). Triggering it at the decode
+// kernel's start, so fold CTAs sit resident next to the decode CTAs, measured
+// ~1% slower.
 // CTA = 8 heads of one batch; thread = (head, 4 float4 columns 512 B apart:
 // a warp reads whole rows); two slots' (m, l, O) loads per round trip.
 constexpr int FR = 8;  // heads per fold CTA
@@ -269,8 +270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     mla_decode_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                       const __grid_constant__ CUtensorMap tv, const Params p) {
   // No alignment slack: the dynamic window starts 1024-aligned (no static
-  // shared memory), and every byte counts — the decode CTA leaves exactly
-  // enough of the SM's 228 KB for mla_fold_kernel CTAs to become resident.
+  // shared memory), and every byte counts.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023) != 0) __trap();
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
@@ -279,7 +279,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   const bool leader = h == 0;
   const int k = blockIdx.y;  // this pair's range of (batch, tile)
   if (threadIdx.x == 0) MT_STAMP(63, 0);
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // mla_fold_kernel may become resident
 
   if (threadIdx.x == 0) {
     // full barriers: the leader's copy is armed with both CTAs' bytes and
@@ -668,7 +667,7 @@ cudaError_t launch_mla_decode(const MlaArgs& a, cudaStream_t st) {
   p.part_l = a.part_l;
   p.part_o = a.part_o;
   const size_t smem = sizeof(Smem);
-  static_assert(sizeof(Smem) <= 226 * 1024, "leave 1 KB + 1 KB reserved for a co-resident fold CTA");
+  static_assert(sizeof(Smem) <= 227 * 1024, "fits the opt-in shared memory of one CTA");
   cudaError_t e = cudaFuncSetAttribute(mla_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
