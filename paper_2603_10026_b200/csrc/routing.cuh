@@ -5,9 +5,11 @@
 //   tests/test_workloads.cpp:210-224).
 // Lane l holds experts e = l + 32 j (j < PER). The top-K' is K' rounds of a
 // warp argmax under the total order (value desc, index asc), encoded as one
-// 64-bit key per candidate: every round is a 5-step butterfly of branch-free
-// 64-bit maxima, so the winner is unique and the indices are bit-exact
-// regardless of the reduction tree; the owning lane then retires the winner. Round 1's winner is d1 (exact max), after which d2 is a
+// 64-bit key per candidate: every round is two warp reductions (redux.sync
+// max of the value bits, then max of the low word among the lanes holding
+// them), so the winner is unique and the indices are bit-exact regardless of
+// the reduction order; the owning lane then retires the winner (a 5-step
+// 64-bit shuffle butterfly per round before). Round 1's winner is d1 (exact max), after which d2 is a
 // warp sum of exp(s - d1) — the incremental Eq.17 rescaling collapses because
 // the whole row is already in registers (one pass over memory).
 #pragma once
@@ -53,11 +55,13 @@ __device__ __forceinline__ void warp_route(const float (&x)[PER], int experts, i
     uint64_t best = key[0];
 #pragma unroll
     for (int j = 1; j < PER; ++j) best = key[j] > best ? key[j] : best;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const uint64_t o = __shfl_xor_sync(0xffffffffu, best, off);
-      best = o > best ? o : best;
-    }
+    // warp argmax as two warp reductions (redux.sync): the largest value
+    // bits, then the largest ~index among the lanes holding them — the same
+    // total order as a 64-bit max, without a 5-step 64-bit shuffle butterfly
+    const uint32_t hi = static_cast<uint32_t>(best >> 32);
+    const uint32_t hmax = __reduce_max_sync(0xffffffffu, hi);
+    const uint32_t lo = __reduce_max_sync(0xffffffffu, hi == hmax ? static_cast<uint32_t>(best) : 0u);
+    best = (static_cast<uint64_t>(hmax) << 32) | lo;
     // the owning lane retires the winner
 #pragma unroll
     for (int j = 0; j < PER; ++j) key[j] = key[j] == best ? 0ull : key[j];
