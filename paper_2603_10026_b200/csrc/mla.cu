@@ -124,6 +124,7 @@ struct Params {
   int64_t total;  // cost units of the whole grid (bs x (tpb + kSegCost))
   int clusters;   // CTA pairs (= gridDim.y)
   int nslots;     // partial slots per batch (1: direct output)
+  bool fast32;    // (total + 1) * clusters < 2^32: 32-bit segment math
   float scale;
   __nv_bfloat16* o;
   float* m;
@@ -141,45 +142,56 @@ struct Params {
 // crosses into a new batch pays a Q reload (72 KB, no second Q buffer fits)
 // and one more epilogue, worth about three tiles' time.
 constexpr int64_t kSegCost = 3;  // A/B on L3: 0 -> 48.1, 1 -> 48.2, 2 -> 46.7, 3 -> 45.8, 4 -> 46.4 us
-__host__ __device__ __forceinline__ int64_t range_start(int64_t k, int64_t clusters, int64_t units) {
+// The index math runs in 32 bits when (units + 1) * clusters fits (Params::
+// fast32): a 64-bit division is a long software sequence and every role
+// re-derives its segments (measured ~0.1 us per launch on L3).
+template <typename T>
+__host__ __device__ __forceinline__ T range_start(T k, T clusters, T units) {
   return k * units / clusters;
 }
-__host__ __device__ __forceinline__ int64_t cluster_of(int64_t u, int64_t clusters, int64_t units) {
+template <typename T>
+__host__ __device__ __forceinline__ T cluster_of(T u, T clusters, T units) {
   return ((u + 1) * clusters - 1) / units;
 }
 // First / last cluster holding tiles of batch b (w = tpb + kSegCost).
-__host__ __device__ __forceinline__ int64_t first_cluster(int64_t b, int64_t w, int64_t clusters, int64_t units) {
-  return cluster_of(b * w + kSegCost, clusters, units);
+template <typename T>
+__host__ __device__ __forceinline__ T first_cluster(T b, T w, T clusters, T units) {
+  return cluster_of<T>(b * w + kSegCost, clusters, units);
 }
-__host__ __device__ __forceinline__ int64_t last_cluster(int64_t b, int64_t w, int64_t clusters, int64_t units) {
-  return cluster_of((b + 1) * w - 1, clusters, units);
+template <typename T>
+__host__ __device__ __forceinline__ T last_cluster(T b, T w, T clusters, T units) {
+  return cluster_of<T>((b + 1) * w - 1, clusters, units);
 }
 
 struct Segment {
   int b, t0, t1, slot, nseg;  // nseg: segments (ranges) the batch is cut into
 };
-// Segment `i` of cluster k's range; false when the range is exhausted.
-__device__ __forceinline__ bool segment(const Params& p, int k, int i, Segment& sg) {
-  const int64_t w = p.tpb + kSegCost;
-  const int64_t x1 = range_start(k + 1, p.clusters, p.total);
-  int64_t x = range_start(k, p.clusters, p.total);
+template <typename T>
+__device__ __forceinline__ bool segment_t(const Params& p, int k, int i, Segment& sg) {
+  const T w = static_cast<T>(p.tpb + kSegCost), cl = static_cast<T>(p.clusters), un = static_cast<T>(p.total);
+  const T x1 = range_start<T>(static_cast<T>(k + 1), cl, un);
+  T x = range_start<T>(static_cast<T>(k), cl, un);
   for (int j = 0; x < x1;) {
-    const int64_t b = x / w;
-    const int64_t lo = x > b * w + kSegCost ? x : b * w + kSegCost;
-    const int64_t hi = x1 < (b + 1) * w ? x1 : (b + 1) * w;
+    const T b = x / w;
+    const T lo = x > b * w + kSegCost ? x : b * w + kSegCost;
+    const T hi = x1 < (b + 1) * w ? x1 : (b + 1) * w;
     x = (b + 1) * w;
     if (hi <= lo) continue;  // only the batch's virtual head
     if (j++ == i) {
       sg.b = static_cast<int>(b);
       sg.t0 = static_cast<int>(lo - b * w - kSegCost);
       sg.t1 = static_cast<int>(hi - b * w - kSegCost);
-      const int64_t k0 = first_cluster(b, w, p.clusters, p.total);
-      sg.slot = static_cast<int>(k - k0);
-      sg.nseg = static_cast<int>(last_cluster(b, w, p.clusters, p.total) - k0 + 1);
+      const T k0 = first_cluster<T>(b, w, cl, un);
+      sg.slot = static_cast<int>(static_cast<T>(k) - k0);
+      sg.nseg = static_cast<int>(last_cluster<T>(b, w, cl, un) - k0 + 1);
       return true;
     }
   }
   return false;
+}
+// Segment `i` of cluster k's range; false when the range is exhausted.
+__device__ __forceinline__ bool segment(const Params& p, int k, int i, Segment& sg) {
+  return p.fast32 ? segment_t<uint32_t>(p, k, i, sg) : segment_t<int64_t>(p, k, i, sg);
 }
 
 // Fold of each batch's segment partials (the Multi-Segment merge,
@@ -198,7 +210,8 @@ __global__ void __launch_bounds__(256, 4) mla_fold_kernel(const Params p) {
   FT_STAMP(1);
   const int b = blockIdx.x / (HN / FR), blk = blockIdx.x % (HN / FR);
   const int64_t w = p.tpb + kSegCost;
-  const int ns = static_cast<int>(last_cluster(b, w, p.clusters, p.total) - first_cluster(b, w, p.clusters, p.total) + 1);
+  const int ns = static_cast<int>(last_cluster<int64_t>(b, w, p.clusters, p.total) -
+                                  first_cluster<int64_t>(b, w, p.clusters, p.total) + 1);
   if (ns == 1) return;  // written directly by its only segment
   const int r = threadIdx.x >> 5, c0 = threadIdx.x & 31;
   const int64_t grow = static_cast<int64_t>(b) * HN + blk * FR + r;
@@ -617,7 +630,7 @@ int64_t slots_needed(int64_t bs, int64_t tpb, int64_t clusters) {
   const int64_t w = tpb + kSegCost, units = bs * w;
   int64_t n = 1;
   for (int64_t b = 0; b < bs; ++b)
-    n = std::max(n, last_cluster(b, w, clusters, units) - first_cluster(b, w, clusters, units) + 1);
+    n = std::max(n, last_cluster<int64_t>(b, w, clusters, units) - first_cluster<int64_t>(b, w, clusters, units) + 1);
   return n;
 }
 
@@ -657,6 +670,7 @@ cudaError_t launch_mla_decode(const MlaArgs& a, cudaStream_t st) {
   p.rows_total = a.rows_total;
   p.tpb = static_cast<int>(tpb);
   p.total = a.bs * (tpb + kSegCost);  // cost units
+  p.fast32 = (p.total + 1) * clusters < (int64_t{1} << 32);
   p.clusters = static_cast<int>(clusters);
   p.nslots = static_cast<int>(a.nslices);
   p.scale = a.scale;
