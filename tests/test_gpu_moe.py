@@ -46,3 +46,21 @@ def test_moe_routing_reference_golden_and_ties():
     s = torch.tensor([[0.3, 0.9, 0.9, -1.0, 0.5, 2.0, 0.1, 0.9]], device="cuda")
     _, _, tv, ti = moe_routing(s, 3)
     assert ti.cpu().tolist() == [[6, 2, 3]]
+
+
+@pytest.mark.parametrize("experts,k", [(128, 8), (256, 8), (64, 5), (200, 7)])
+def test_moe_routing_heavy_ties(experts, k):
+    """Scores on a 4-level grid (+0/-0 included): every round's argmax is a tie
+    across lanes and within a lane's experts; indices must follow (value desc,
+    index asc) exactly (topk_merge, proj/src/simulator.cpp:80-88)."""
+    import torch
+    from paper_2603_10026_b200 import moe_routing
+
+    g = torch.Generator().manual_seed(experts * 31 + k)
+    levels = torch.tensor([-1.0, -0.0, 0.0, 0.5])
+    s = levels[torch.randint(0, 4, (257, experts), generator=g)]
+    _, _, tv, ti = moe_routing(s.cuda(), k)
+    torch.cuda.synchronize()
+    sv = s.numpy().astype(np.float64) + 0.0  # -0 == +0
+    want = np.argsort(-sv, axis=1, kind="stable")[:, :k] + 1
+    np.testing.assert_array_equal(ti.cpu().numpy(), want)
