@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define RF_CUDA_ABI_VERSION 3
+#define RF_CUDA_ABI_VERSION 4
 
 typedef enum rf_status {
   RF_OK = 0,
@@ -187,6 +187,12 @@ void rf_plan_destroy(rf_plan* plan);
 rf_status rf_plan_describe(const rf_plan* plan, char* buf, size_t buflen);
 /* Number of kernel launches one rf_run issues (for launch accounting). */
 int64_t rf_plan_launches_per_run(const rf_plan* plan);
+/* Byte sizes of every rf_io slot the plan reads (in[0..3]) and writes
+ * (d[0..3]); 0 = slot unused. in[1] of the GEMM patterns is the packed weight
+ * (rf_packed_bytes). Lets callers reject undersized buffers before rf_run
+ * with the reference's ShapeMismatch (check_shapes, simulator.cpp:235-245)
+ * instead of letting a kernel read out of bounds. (ABI v4) */
+rf_status rf_plan_io_bytes(const rf_plan* plan, size_t in_bytes[4], size_t out_bytes[4]);
 
 /* Plan-time weight packing for the GEMM patterns (outside any timed region):
  *   QUANT_GEMM:   w [K,N] f32 (reduce-axis major, the reference layout) ->

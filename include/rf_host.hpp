@@ -874,15 +874,20 @@ inline ExecReport execute(const Program& prog, const TreeConfig& cfg, long long 
       // pad to the kernel tiles: M to 128 rows (copies of the row: never an
       // all-zero padding row), K with zeros (neutral for max|a| and sum x^2,
       // zero contributions), N with zero weight columns.
+      // RMSNorm: the kernel normalises by the mean over its (padded) K,
+      // 1/sqrt(d1/Kp + eps'). With r = L0/Kp, eps' = eps*r and g' = g*sqrt(r):
+      //   g' / sqrt(d1/Kp + eps') = g sqrt(r) / (sqrt(r) sqrt(d1/L0 + eps))
+      // which is the cascade's g / sqrt(d1/L0 + eps) exactly (d1 is unchanged).
       const long long N = prog.free_len;
       const long long Kp = round_up(L0, quant ? 128 : 64), Np = round_up(N, quant ? 512 : 256);
       const long long M = 128;
+      const double r = static_cast<double>(L0) / static_cast<double>(Kp);
       rf_desc d = base_desc(prog.pattern, RF_BF16);
       d.rows = M;
       d.len = Kp;
       d.free_len = Np;
       d.fmax = prog.fmax;
-      d.eps = prog.eps;
+      d.eps = quant ? prog.eps : prog.eps * r;
       PlanHandle h(d);
       const auto& A = st.array(prog.x).data;
       const auto& W = st.array(prog.w).data;
@@ -891,7 +896,8 @@ inline ExecReport execute(const Program& prog, const TreeConfig& cfg, long long 
         for (long long f = 0; f < N; ++f) wf[l * Np + f] = static_cast<float>(W[l * N + f]);
       if (!quant) {
         const auto& g = st.array(prog.g).data;
-        for (long long l = 0; l < L0; ++l) gf[l] = static_cast<float>(g[l]);
+        const double gs = std::sqrt(r);
+        for (long long l = 0; l < L0; ++l) gf[l] = static_cast<float>(g[l] * gs);
       }
       void* packed = nullptr;
       check(rf_pack_weight_host(h.p, wf.data(), quant ? nullptr : gf.data(), &packed));

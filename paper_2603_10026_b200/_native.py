@@ -36,7 +36,7 @@ RF_PATTERN_MOMENTS = 9
 RF_PATTERN_MOE_ROUTER = 10
 RF_PATTERN_MLA_DECODE = 11
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 # rf_dtype
 RF_F32 = 0
@@ -88,6 +88,7 @@ SIGNATURES = {
     "rf_plan_destroy": (None, [_P]),
     "rf_plan_describe": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.c_size_t]),
     "rf_plan_launches_per_run": (ctypes.c_int64, [_P]),
+    "rf_plan_io_bytes": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]),
     "rf_pack_weight": (ctypes.c_int, [_P, _P, _P, _P, _P]),
     "rf_pack_weight_host": (ctypes.c_int, [_P, _P, _P, ctypes.POINTER(_P)]),
     "rf_packed_bytes": (ctypes.c_size_t, [_P]),

@@ -56,6 +56,22 @@ rf_status fail(rf_status s, const std::string& msg) {
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+// Selects the plan's device for the duration of an entry point and restores
+// the caller's device on every return path.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 // Patterns with a plan-time packed weight in in[1] (tcgen05 GEMM tiles of 128 rows).
 bool is_gemm(int pattern) {
   return pattern == RF_PATTERN_QUANT_GEMM_E4M3 || pattern == RF_PATTERN_RMSNORM_GEMM ||
@@ -394,9 +410,7 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
   if (prop.major != 10 || prop.minor != 0)
     return bail(RF_ERR_CUDA, "librf_cuda is built for sm_100a only; device is sm_" +
                                  std::to_string(prop.major) + std::to_string(prop.minor));
-  int prev_dev = 0;
-  cudaGetDevice(&prev_dev);
-  cudaSetDevice(d.device);
+  DeviceGuard guard(d.device);
 
   // ---- kernel choice ----
   switch (d.pattern) {
@@ -532,7 +546,6 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
                 (long long)d.len, (long long)d.free_len, (long long)d.segments,
                 (long long)p->nsplit, (long long)p->launches, prop.name);
   p->describe = buf;
-  cudaSetDevice(prev_dev);
   *out = p;
   return RF_OK;
 }
@@ -558,9 +571,17 @@ rf_status rf_plan_describe(const rf_plan* p, char* buf, size_t n) {
 
 int64_t rf_plan_launches_per_run(const rf_plan* p) { return p ? p->launches : 0; }
 
+rf_status rf_plan_io_bytes(const rf_plan* p, size_t in_bytes[4], size_t out_bytes[4]) {
+  if (!p || !in_bytes || !out_bytes) return fail(RF_ERR_ARG, "null plan/arrays");
+  io_sizes(p, in_bytes, out_bytes);
+  if (is_gemm(p->d.pattern)) in_bytes[1] = rf_packed_bytes(p);
+  return RF_OK;
+}
+
 rf_status rf_pack_weight(const rf_plan* p, const void* w, const void* g, void* packed,
                          void* stream) {
   if (!p || !w || !packed) return fail(RF_ERR_ARG, "null plan/w/packed");
+  DeviceGuard guard(p->d.device);
   cudaError_t e;
   if (p->d.pattern == RF_PATTERN_QUANT_GEMM_E4M3) {
     e = rf::launch_pack_e4m3(static_cast<const float*>(w), p->d.len, p->d.free_len,
@@ -604,9 +625,7 @@ rf_status rf_pack_weight_host(const rf_plan* p, const float* w, const float* g, 
   if (needs_g && !g) return fail(RF_ERR_ARG, "rmsnorm/layernorm pack needs g");
   int64_t wk = 0, wn = 0;
   pack_dims(p->d, wk, wn);
-  int prev = 0;
-  cudaGetDevice(&prev);
-  RF_CUDA_TRY(cudaSetDevice(p->d.device));
+  DeviceGuard guard(p->d.device);
   const size_t kn = static_cast<size_t>(wk) * wn;
   float *dw = nullptr, *dg = nullptr;
   void* out = nullptr;
@@ -626,7 +645,6 @@ rf_status rf_pack_weight_host(const rf_plan* p, const float* w, const float* g, 
     return st;
   }
   *packed = out;
-  cudaSetDevice(prev);
   return RF_OK;
 }
 
@@ -643,6 +661,7 @@ rf_status rf_run(const rf_plan* p, const rf_io* io, void* stream) {
   if (is_gemm(p->d.pattern) && !io->in[1])
     return fail(RF_ERR_SHAPE, "missing packed weight in[1]");
   if (units_of(p) == 0 || p->d.rows == 0) return RF_OK;  // empty batch
+  DeviceGuard guard(p->d.device);
   return run_range(p, io, 0, units_of(p), as_stream(stream));
 }
 
@@ -651,9 +670,7 @@ rf_status rf_run_host(rf_plan* p, const rf_host_io* io) {
   size_t in[4], out[4];
   io_sizes(p, in, out);
   const bool gemm = is_gemm(p->d.pattern);
-  int prev_dev = 0;
-  cudaGetDevice(&prev_dev);
-  RF_CUDA_TRY(cudaSetDevice(p->d.device));
+  DeviceGuard guard(p->d.device);
   if (!p->staged) {
     for (int i = 0; i < 4; ++i)
       if (in[i]) RF_CUDA_TRY(cudaMalloc(&p->dev_in[i], in[i]));
@@ -662,11 +679,22 @@ rf_status rf_run_host(rf_plan* p, const rf_host_io* io) {
     for (auto& s : p->streams) RF_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     p->staged = true;
   }
+  auto drain = [&](rf_status s) {
+    cudaStreamSynchronize(p->streams[0]);
+    cudaStreamSynchronize(p->streams[1]);
+    return s;
+  };
+  for (int i = 0; i < 4; ++i)
+    if (in[i] && !(gemm && i == 1) && !io->in[i]) return fail(RF_ERR_SHAPE, "missing input " + std::to_string(i));
+  for (int i = 0; i < 3; ++i)
+    if (out[i] && !io->d[i]) return fail(RF_ERR_SHAPE, "missing output d" + std::to_string(i + 1));
+  if (gemm && !io->in[1]) return fail(RF_ERR_SHAPE, "missing packed weight in[1]");
   rf_io dio{};
   for (int i = 0; i < 4; ++i) dio.in[i] = p->dev_in[i];
   for (int i = 0; i < 4; ++i) dio.d[i] = io->d[i] ? p->dev_out[i] : nullptr;
   if (gemm) dio.in[1] = io->in[1];  // packed weight: plan-time resident device buffer
   const int64_t units = units_of(p);
+  if (units == 0 || p->d.rows == 0) return RF_OK;  // empty batch
   // Chunking: 8 chunks over independent units, alternating two streams, so
   // the H2D of chunk c+1 and the D2H of chunk c-1 overlap chunk c's kernels.
   // GEMM chunks are whole 128-row tiles.
@@ -680,23 +708,25 @@ rf_status rf_run_host(rf_plan* p, const rf_host_io* io) {
     for (int i = 0; i < 4; ++i) {
       if (!in[i] || (gemm && i == 1)) continue;
       const size_t chunk = in[i] / units * nu, off = in[i] / units * u0;
-      RF_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(p->dev_in[i]) + off,
-                                  static_cast<const char*>(io->in[i]) + off, chunk,
-                                  cudaMemcpyHostToDevice, st));
+      const cudaError_t e = cudaMemcpyAsync(static_cast<char*>(p->dev_in[i]) + off,
+                                            static_cast<const char*>(io->in[i]) + off, chunk,
+                                            cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return drain(fail(RF_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(e)));
     }
     rf_status s = run_range(p, &dio, u0, nu, st);
-    if (s != RF_OK) return s;
+    // an early return must not leave copies into the caller's host buffers in flight
+    if (s != RF_OK) return drain(s);
     for (int i = 0; i < 4; ++i) {
       if (!out[i] || !io->d[i]) continue;
       const size_t chunk = out[i] / units * nu, off = out[i] / units * u0;
-      RF_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(io->d[i]) + off,
-                                  static_cast<char*>(p->dev_out[i]) + off, chunk,
-                                  cudaMemcpyDeviceToHost, st));
+      const cudaError_t e = cudaMemcpyAsync(static_cast<char*>(io->d[i]) + off,
+                                            static_cast<char*>(p->dev_out[i]) + off, chunk,
+                                            cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) return drain(fail(RF_ERR_CUDA, std::string("D2H: ") + cudaGetErrorString(e)));
     }
   }
   RF_CUDA_TRY(cudaStreamSynchronize(p->streams[0]));
   RF_CUDA_TRY(cudaStreamSynchronize(p->streams[1]));
-  cudaSetDevice(prev_dev);
   return RF_OK;
 }
 
@@ -707,6 +737,7 @@ rf_status rf_run_partials(const rf_plan* p, const rf_io* io, int64_t slice_begin
   if (slice_begin < 0 || outp->nslices < 1 || slice_begin + outp->nslices > p->d.segments)
     return fail(RF_ERR_SEGMENTATION, "slice range outside the plan's segments");
   const rf_desc& d = p->d;
+  DeviceGuard guard(d.device);
   rf::AttnArgs a{};
   a.q = io->in[0];
   a.k = io->in[1];
@@ -741,6 +772,10 @@ rf_status rf_merge_partials(const rf_plan* p, const rf_partials* in, const rf_io
                             void* stream) {
   if (!p || !in || !io) return fail(RF_ERR_ARG, "null argument");
   if (p->d.pattern != RF_PATTERN_ATTENTION) return fail(RF_ERR_UNSUPPORTED, "merge: attention only");
+  if (in->nslices < 1) return fail(RF_ERR_SEGMENTATION, "merge: no slices");
+  if (!in->m || !in->l || !in->o || !io->d[0] || !io->d[1] || !io->d[2])
+    return fail(RF_ERR_SHAPE, "merge: missing partial or output buffer");
+  DeviceGuard guard(p->d.device);
   cudaError_t e = rf::launch_attention_merge(in->m, in->l, in->o, in->nslices, p->rows_total,
                                              p->rows_total, p->d.free_len,
                                              static_cast<float*>(io->d[0]),
@@ -752,6 +787,7 @@ rf_status rf_merge_partials(const rf_plan* p, const rf_partials* in, const rf_io
 
 rf_status rf_check_domain(const rf_plan* p, void* stream) {
   if (!p) return fail(RF_ERR_ARG, "null plan");
+  DeviceGuard guard(p->d.device);
   int flag = 0;
   RF_CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
   RF_CUDA_TRY(cudaMemcpy(&flag, p->domain_flag, sizeof(int), cudaMemcpyDeviceToHost));

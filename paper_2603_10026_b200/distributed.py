@@ -53,11 +53,16 @@ def gather_partials(m, l, o, group=None):
     world = dist.get_world_size(group)
     if world == 1:
         return m, l, o
+    # gloo has no CUDA all_gather: stage through host memory (the CPU test
+    # path and the one-GPU multi-rank smoke run); NCCL gathers in place.
+    host = dist.get_backend(group) == "gloo" and m.is_cuda
     out = []
     for t in (m, l, o):
-        parts = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(parts, t.contiguous(), group=group)
-        out.append(torch.cat(parts, dim=0))
+        src = t.contiguous().cpu() if host else t.contiguous()
+        parts = [torch.empty_like(src) for _ in range(world)]
+        dist.all_gather(parts, src, group=group)
+        cat = torch.cat(parts, dim=0)
+        out.append(cat.to(t.device) if host else cat)
     return tuple(out)
 
 
@@ -74,6 +79,9 @@ def split_kv_decode(q, k_local, v_local, segments: int, group=None, stream=None,
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
+    # the kernels read dense [B,H,S,D] buffers: a strided view (e.g.
+    # k[:, :, a:b]) must be materialised, never passed as a raw pointer
+    q, k_local, v_local = q.contiguous(), k_local.contiguous(), v_local.contiguous()
     B, H, Sq, D = q.shape
     skv_local = k_local.shape[2]
     if segments % world:
@@ -88,7 +96,7 @@ def split_kv_decode(q, k_local, v_local, segments: int, group=None, stream=None,
 
         dt = "bf16" if q.dtype == torch.bfloat16 else "f32"
         p = plan(Desc(N.RF_PATTERN_ATTENTION, dt, rows=Sq, len=skv_local, free_len=D, batch=B,
-                      heads=H, segments=local, device=q.device.index or 0))
+                      heads=H, segments=local, device=q.device.index or 0), stream)
 
         def partials_fn(q, k, v, pm, pl, po):  # noqa: F811
             p.run_partials([q, k, v], 0, pm, pl, po, stream)
@@ -102,7 +110,14 @@ def split_kv_decode(q, k_local, v_local, segments: int, group=None, stream=None,
     po = torch.empty(local, rows, D, dtype=torch.float32, device=dev)
     partials_fn(q, k_local, v_local, pm, pl, po)
     if world > 1:
+        # the collective runs on torch's current stream: order it after the
+        # partials kernel (on `stream`), and the merge (on `stream`) after it
+        cur = torch.cuda.current_stream(dev) if q.is_cuda else None
+        if cur is not None and stream is not None:
+            cur.wait_stream(stream)
         pm, pl, po = gather_partials(pm, pl, po, group)
+        if cur is not None and stream is not None:
+            stream.wait_stream(cur)
     m = torch.empty(B, H, Sq, dtype=torch.float32, device=dev)
     l = torch.empty_like(m)
     o = torch.empty_like(q)

@@ -121,6 +121,9 @@ class Plan:
         check(N.lib().rf_plan_describe(self._h, buf, 1024))
         self.info = json.loads(buf.value.decode())
         self.launches_per_run = int(N.lib().rf_plan_launches_per_run(self._h))
+        ib, ob = (ctypes.c_size_t * 4)(), (ctypes.c_size_t * 4)()
+        check(N.lib().rf_plan_io_bytes(self._h, ib, ob))
+        self.in_bytes, self.out_bytes = tuple(ib), tuple(ob)
 
     def close(self):
         if self._h:
@@ -142,12 +145,45 @@ class Plan:
             io.d[i] = _ptr(t)
         return io
 
+    def _check_io(self, inputs: Sequence, outputs: Sequence, host: bool) -> None:
+        """ShapeMismatch (check_shapes, proj/src/simulator.cpp:235-245) for any
+        buffer whose size, layout or placement disagrees with the plan — the
+        kernels take raw pointers and would otherwise read out of bounds."""
+        dev = self.desc.device
+        for kind, ts, need in (("in", inputs, self.in_bytes), ("d", outputs, self.out_bytes)):
+            _require(len(ts) <= 4, f"at most 4 {kind} buffers")
+            for i, t in enumerate(ts):
+                if t is None or isinstance(t, int) or need[i] == 0:
+                    continue
+                name = f"{kind}[{i}]" if kind == "in" else f"d{i + 1}"
+                got = t.numel() * t.element_size()
+                _require(got == need[i], f"{name}: {got} bytes, the plan needs {need[i]}")
+                _require(t.is_contiguous(), f"{name} must be contiguous")
+                # the packed weight stays device-resident on the host path too
+                want_cuda = not host or (kind == "in" and i == 1 and _packed(self) > 0)
+                if want_cuda:
+                    _require(t.is_cuda and (t.device.index or 0) == dev,
+                             f"{name} must be on cuda:{dev}")
+                else:
+                    _require(not t.is_cuda, f"{name} must be a host tensor for run_host")
+            for i in range(len(ts), 4):
+                if need[i] and not (kind == "d" and i == 3):
+                    raise ShapeMismatch(f"missing {kind} buffer {i}")
+
     def run(self, inputs: Sequence, outputs: Sequence, stream=None) -> None:
+        self._check_io(inputs, outputs, host=False)
+        io = self._io(inputs, outputs)
+        check(N.lib().rf_run(self._h, ctypes.byref(io), _stream_ptr(stream)))
+
+    def run_unchecked(self, inputs: Sequence, outputs: Sequence, stream=None) -> None:
+        """rf_run without the Python-side buffer checks (callers that validated
+        their buffers once, e.g. a CUDA-graph capture loop)."""
         io = self._io(inputs, outputs)
         check(N.lib().rf_run(self._h, ctypes.byref(io), _stream_ptr(stream)))
 
     def run_host(self, inputs: Sequence, outputs: Sequence) -> None:
         """Host (pinned) buffers in and out; copies happen inside the call."""
+        self._check_io(inputs, outputs, host=True)
         io = self._io(inputs, outputs)
         check(N.lib().rf_run_host(self._h, ctypes.byref(io)))
 
@@ -189,14 +225,31 @@ class Plan:
         check(N.lib().rf_check_domain(self._h, _stream_ptr(stream)))
 
 
+def _packed(p: "Plan") -> int:
+    return int(N.lib().rf_packed_bytes(p._h))
+
+
 _plans: dict = {}
 
 
-def plan(desc: Desc) -> Plan:
-    p = _plans.get(desc)
+def plan(desc: Desc, stream=None) -> Plan:
+    """The cached plan for (desc, stream). A plan owns its split workspace, so
+    calls on different streams get different plans and never share it
+    (rf_cuda.h: one plan per stream for concurrent execution)."""
+    key = (desc, _stream_ptr(stream) if stream is not None or _cuda_ok() else 0)
+    p = _plans.get(key)
     if p is None:
-        p = _plans[desc] = Plan(desc)
+        p = _plans[key] = Plan(desc)
     return p
+
+
+def _cuda_ok() -> bool:
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        return False
 
 
 # ----------------------------------------------------------- batched ops ---
@@ -224,7 +277,7 @@ def attention(q, k, v, segments: int = 1, softmax_scale: float = 1.0, stream=Non
         raise UnsupportedPattern(f"attention: dtype {q.dtype}")
     p = plan(Desc(N.RF_PATTERN_ATTENTION, dt, rows=Sq, len=k.shape[2], free_len=D, batch=B,
                   heads=H, segments=segments, softmax_scale=softmax_scale,
-                  device=q.device.index or 0))
+                  device=q.device.index or 0), stream)
     m = torch.empty((B, H, Sq), dtype=torch.float32, device=q.device)
     l = torch.empty_like(m)
     o = torch.empty_like(q)
@@ -238,35 +291,45 @@ def safe_softmax(x, stream=None):
 
     _require(x.dim() == 2 and x.dtype == torch.float32, "x must be float32 [rows, n]")
     p = plan(Desc(N.RF_PATTERN_SAFE_SOFTMAX, "f32", rows=x.shape[0], len=x.shape[1],
-                  device=x.device.index or 0))
+                  device=x.device.index or 0), stream)
     d1 = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
     d2 = torch.empty_like(d1)
     p.run([x.contiguous()], [d1, d2], stream)
     return d1, d2
 
 
-def quant_gemm_plan(m: int, k: int, n: int, fmax: float = 448.0, device: int = 0) -> Plan:
+def quant_gemm_plan(m: int, k: int, n: int, fmax: float = 448.0, device: int = 0,
+                    stream=None) -> Plan:
     return plan(Desc(N.RF_PATTERN_QUANT_GEMM_E4M3, "bf16", rows=m, len=k, free_len=n,
-                     fmax=fmax, device=device))
+                     fmax=fmax, device=device), stream)
 
 
-def quant_gemm(a, w_packed, fmax: float = 448.0, stream=None):
+def quant_gemm(a, w_packed, fmax: float = 448.0, stream=None, check_domain: bool = True):
     """Per-token absmax -> e4m3 quantise -> GEMM. a: [M,K] bf16; w_packed from
-    Plan.pack_weight. Returns (d1 = amax [M] f32, d2 = C [M,N] f32)."""
+    Plan.pack_weight. Returns (d1 = amax [M] f32, d2 = C [M,N] f32).
+    check_domain: raise DomainError, as the reference does at finalize
+    (simulator.cpp:611-621), when a row's absmax is 0 (synchronises the
+    stream; pass False inside graphs / timed loops and call
+    Plan.check_domain later)."""
     import torch
 
+    _require(a.dim() == 2 and a.dtype == torch.bfloat16, "a must be bfloat16 [M, K]")
     M, K = a.shape
+    _require(w_packed.dim() == 2 and w_packed.shape[1] == K, "w_packed must be [N, K]")
     Nn = w_packed.shape[0]
-    p = quant_gemm_plan(M, K, Nn, fmax, a.device.index or 0)
+    p = quant_gemm_plan(M, K, Nn, fmax, a.device.index or 0, stream)
     amax = torch.empty(M, dtype=torch.float32, device=a.device)
     c = torch.empty((M, Nn), dtype=torch.float32, device=a.device)
     p.run([a.contiguous(), w_packed], [amax, c], stream)
+    if check_domain:
+        p.check_domain(stream)
     return amax, c
 
 
-def rmsnorm_gemm_plan(t: int, k: int, n: int, eps: float = 1e-6, device: int = 0) -> Plan:
+def rmsnorm_gemm_plan(t: int, k: int, n: int, eps: float = 1e-6, device: int = 0,
+                      stream=None) -> Plan:
     return plan(Desc(N.RF_PATTERN_RMSNORM_GEMM, "bf16", rows=t, len=k, free_len=n, eps=eps,
-                     device=device))
+                     device=device), stream)
 
 
 def rmsnorm_gemm(x, w_packed, eps: float = 1e-6, stream=None):
@@ -275,18 +338,21 @@ def rmsnorm_gemm(x, w_packed, eps: float = 1e-6, stream=None):
     d2 = Y [T,N] bf16)."""
     import torch
 
+    _require(x.dim() == 2 and x.dtype == torch.bfloat16, "x must be bfloat16 [T, K]")
     T, K = x.shape
+    _require(w_packed.dim() == 2 and w_packed.shape[1] == K, "w_packed must be [N, K]")
     Nn = w_packed.shape[0]
-    p = rmsnorm_gemm_plan(T, K, Nn, eps, x.device.index or 0)
+    p = rmsnorm_gemm_plan(T, K, Nn, eps, x.device.index or 0, stream)
     ss = torch.empty(T, dtype=torch.float32, device=x.device)
     y = torch.empty((T, Nn), dtype=torch.bfloat16, device=x.device)
     p.run([x.contiguous(), w_packed], [ss, y], stream)
     return ss, y
 
 
-def layernorm_gemm_plan(t: int, k: int, n: int, eps: float = 1e-5, device: int = 0) -> Plan:
+def layernorm_gemm_plan(t: int, k: int, n: int, eps: float = 1e-5, device: int = 0,
+                        stream=None) -> Plan:
     return plan(Desc(N.RF_PATTERN_LAYERNORM_GEMM, "bf16", rows=t, len=k, free_len=n, eps=eps,
-                     device=device))
+                     device=device), stream)
 
 
 def layernorm_gemm(x, w_packed, n: int, eps: float = 1e-5, with_d4: bool = True, stream=None):
@@ -297,8 +363,9 @@ def layernorm_gemm(x, w_packed, n: int, eps: float = 1e-5, with_d4: bool = True,
     (d1 [T] f32, d2 [T] f32, d3 [T,N] bf16, d4 [T,N] bf16 or None)."""
     import torch
 
+    _require(x.dim() == 2 and x.dtype == torch.bfloat16, "x must be bfloat16 [T, K]")
     T, K = x.shape
-    p = layernorm_gemm_plan(T, K, n, eps, x.device.index or 0)
+    p = layernorm_gemm_plan(T, K, n, eps, x.device.index or 0, stream)
     _require(w_packed.numel() * w_packed.element_size() == N.lib().rf_packed_bytes(p._h),
              "w_packed size does not match the plan")
     d1 = torch.empty(T, dtype=torch.float32, device=x.device)
@@ -319,7 +386,7 @@ def moe_routing(logits, k: int, stream=None):
     _require(logits.dim() == 2 and logits.dtype == torch.float32, "logits must be float32 [rows, experts]")
     rows, experts = logits.shape
     p = plan(Desc(N.RF_PATTERN_MOE_ROUTING, "f32", rows=rows, len=experts, free_len=k,
-                  device=logits.device.index or 0))
+                  device=logits.device.index or 0), stream)
     d1 = torch.empty(rows, dtype=torch.float32, device=logits.device)
     d2 = torch.empty_like(d1)
     rec = torch.empty(rows, k, 2, dtype=torch.int32, device=logits.device)
@@ -327,9 +394,10 @@ def moe_routing(logits, k: int, stream=None):
     return d1, d2, rec[..., 0].view(torch.float32), rec[..., 1]
 
 
-def moe_router_plan(tokens: int, hd: int, experts: int, k: int, device: int = 0) -> Plan:
+def moe_router_plan(tokens: int, hd: int, experts: int, k: int, device: int = 0,
+                    stream=None) -> Plan:
     return plan(Desc(N.RF_PATTERN_MOE_ROUTER, "bf16", rows=tokens, len=experts, free_len=k,
-                     producer_len=hd, device=device))
+                     producer_len=hd, device=device), stream)
 
 
 def moe_router(x, w_packed, k: int, with_scores: bool = False, stream=None):
@@ -341,8 +409,9 @@ def moe_router(x, w_packed, k: int, with_scores: bool = False, stream=None):
 
     _require(x.dim() == 2 and x.dtype == torch.bfloat16, "x must be bfloat16 [tokens, hd]")
     tokens, hd = x.shape
+    _require(w_packed.dim() == 2 and w_packed.shape[1] == hd, "w_packed must be [experts, hd]")
     experts = w_packed.shape[0]
-    p = moe_router_plan(tokens, hd, experts, k, x.device.index or 0)
+    p = moe_router_plan(tokens, hd, experts, k, x.device.index or 0, stream)
     d1 = torch.empty(tokens, dtype=torch.float32, device=x.device)
     d2 = torch.empty_like(d1)
     rec = torch.empty(tokens, k, 2, dtype=torch.int32, device=x.device)
@@ -366,7 +435,7 @@ def mla_decode(q, cache, segments: int = 1, softmax_scale: float = 1.0, stream=N
     skv = cache.shape[1]
     p = plan(Desc(N.RF_PATTERN_MLA_DECODE, "bf16", rows=1, len=skv, free_len=512, batch=B, heads=hn,
                   segments=segments, softmax_scale=softmax_scale, producer_len=dqk,
-                  device=q.device.index or 0))
+                  device=q.device.index or 0), stream)
     m = torch.empty(B, hn, dtype=torch.float32, device=q.device)
     l = torch.empty_like(m)
     o = torch.empty(B, hn, 512, dtype=torch.bfloat16, device=q.device)
@@ -389,7 +458,7 @@ def variance(x, segments: int = 1, stream=None):
     _require(x.dim() == 2, "x must be [rows, n]")
     (x,) = _rows_f32("variance", x)
     p = plan(Desc(N.RF_PATTERN_VARIANCE, "f32", rows=x.shape[0], len=x.shape[1],
-                  segments=segments, device=x.device.index or 0))
+                  segments=segments, device=x.device.index or 0), stream)
     d1 = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
     d2 = torch.empty_like(d1)
     p.run([x], [d1, d2], stream)
@@ -403,7 +472,7 @@ def sum_sum(x1, x2, offset: float = 10.0, eps: float = 1e-12, segments: int = 1,
     _require(x1.dim() == 2 and x1.shape == x2.shape, "x1, x2 must be [rows, n]")
     x1, x2 = _rows_f32("sum_sum", x1, x2)
     p = plan(Desc(N.RF_PATTERN_SUM_SUM, "f32", rows=x1.shape[0], len=x1.shape[1], eps=eps,
-                  offset=offset, segments=segments, device=x1.device.index or 0))
+                  offset=offset, segments=segments, device=x1.device.index or 0), stream)
     d1 = torch.empty(x1.shape[0], dtype=torch.float32, device=x1.device)
     d2 = torch.empty_like(d1)
     p.run([x1, x2], [d1, d2], stream)
@@ -420,7 +489,7 @@ def moments(mass, pos, segments: int = 1, stream=None):
     mass, pos = _rows_f32("moments", mass, pos)
     rows, n, F = pos.shape
     p = plan(Desc(N.RF_PATTERN_MOMENTS, "f32", rows=rows, len=n, free_len=F, segments=segments,
-                  device=mass.device.index or 0))
+                  device=mass.device.index or 0), stream)
     d1 = torch.empty(rows, dtype=torch.float32, device=mass.device)
     d2 = torch.empty(rows, F, dtype=torch.float32, device=mass.device)
     d3 = torch.empty_like(d2)

@@ -287,13 +287,12 @@ TEST(topk_reduction_ties_lowest_index) {  // test_simulator.cpp:254-271
   CHECK(r.outputs[0].v[0] == 2.0);
 }
 
-TEST(rmsnorm_gemm_matches_direct_loop) {
-  const long long k = 256, n = 48;
+static void rms_case(long long k, long long n, unsigned seed) {
   Program p = plan(rms_dsl(k, n));
   TensorStore st;
-  st.define("x", k, 0, random_vec(k, 1, -1, 1));
-  st.define("g", k, 0, random_vec(k, 2, -1, 1));
-  st.define("w", k, n, random_vec(k * n, 3, -1, 1));
+  st.define("x", k, 0, random_vec(k, seed, -1, 1));
+  st.define("g", k, 0, random_vec(k, seed + 1, -1, 1));
+  st.define("w", k, n, random_vec(k * n, seed + 2, -1, 1));
   ExecReport r = run_incremental(p, TreeConfig{{k, 1}}, st);
   const auto &x = st.array("x").data, &g = st.array("g").data, &w = st.array("w").data;
   double ss = 0;
@@ -303,9 +302,18 @@ TEST(rmsnorm_gemm_matches_direct_loop) {
   for (long long l = 0; l < k; ++l)
     for (long long f = 0; f < n; ++f)
       want.outputs[1].v[f] += x[l] * g[l] / std::sqrt(ss / k + 1e-6) * w[l * n + f];
-  DiffReport d = compare_reports(r, want, 0.1);  // bf16 operands (unrounded reference)
+  DiffReport d = compare_reports(r, want, 2e-2);  // bf16 operands (unrounded reference)
   CHECK(d.pass);
-  std::printf("  rmsnorm scaled err vs unrounded reference: %.3g (%s)\n", d.max_rel_err, d.worst.c_str());
+  std::printf("  rmsnorm k=%lld scaled err vs unrounded reference: %.3g (%s)\n", k, d.max_rel_err,
+              d.worst.c_str());
+}
+
+TEST(rmsnorm_gemm_matches_direct_loop) {
+  rms_case(256, 48, 1);
+  // K not a multiple of the kernel's 64-wide K tile: the host pads K with
+  // zeros and must still normalise by the cascade's own mean d1 / L0
+  rms_case(100, 48, 11);
+  rms_case(4000, 40, 21);
 }
 
 TEST(layernorm_gemm_matches_direct_loop) {

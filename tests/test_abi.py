@@ -35,7 +35,7 @@ def test_abi_version_and_status_strings():
     from paper_2603_10026_b200 import _native as N
 
     L = N.lib()
-    assert L.rf_abi_version() == N.ABI_VERSION == 3
+    assert L.rf_abi_version() == N.ABI_VERSION == 4
     assert b"ShapeMismatch" in L.rf_status_string(N.RF_ERR_SHAPE)
     assert b"IncompatibleSegmentation" in L.rf_status_string(N.RF_ERR_SEGMENTATION)
     assert b"DomainError" in L.rf_status_string(N.RF_ERR_DOMAIN)
