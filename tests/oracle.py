@@ -155,6 +155,46 @@ def quant_gemm_e4m3(a, w, fmax=448.0, tile_k=128):
     return d1, c
 
 
+def quant_gemm_e4m3_torch(a, w, fmax=448.0, tile_k=128, pow2=True):
+    """Independent emulation (torch float8_e4m3fn casts, not rf_oracle.c) of
+    the single-loop FP8 quant GEMM over K tiles of `tile_k`:
+      m_t   = running max |a| (fp32, as the kernel keeps it)
+      ref_t = 2^ceil(log2 m_t)  (pow2=True: the kernel's H' proxy)
+              m_t               (pow2=False: SURVEY §7.3's true running amax)
+      q     = e4m3(fp32(a * (fmax / ref_t)))          (RNE, |q| <= fmax)
+      acc   = acc * (ref_{t-1} / ref_t) + q . w       (Eq.17 correction d1'/d1)
+      c     = acc * ref_T / m_T                       (finalize_root retarget)
+    The real-arithmetic reference (make_quant_gemm, workloads.cpp:192-207) is
+    c = sum (fmax a / m_T) w; both forms equal it without the rounding."""
+    import torch
+
+    A = torch.as_tensor(_f64(a)).to(torch.float32)
+    W = torch.as_tensor(_f64(w))
+    M, K = A.shape
+    acc = torch.zeros(M, W.shape[1], dtype=torch.float64)
+    amax = torch.zeros(M, dtype=torch.float32)
+    ref = torch.zeros(M, dtype=torch.float32)
+    for l0 in range(0, K, tile_k):
+        blk = A[:, l0:l0 + tile_k]
+        amax = torch.maximum(amax, blk.abs().amax(dim=1))
+        if pow2:
+            mant, ex = torch.frexp(amax)
+            nref = torch.where(mant == 0.5, torch.ldexp(torch.ones_like(amax), ex - 1),
+                               torch.ldexp(torch.ones_like(amax), ex))
+        else:
+            nref = amax.clone()
+        if l0 > 0:
+            corr = torch.where((ref > 0) & (nref != ref), ref.double() / nref.double(),
+                               torch.ones_like(ref, dtype=torch.float64))
+            acc *= corr[:, None]
+        ref = nref
+        scale = (torch.full_like(ref, float(fmax)) / ref)[:, None]
+        qv = (blk * scale).to(torch.float8_e4m3fn).to(torch.float64)
+        acc += qv @ W[l0:l0 + tile_k]
+    fin = ref.double() / amax.double()
+    return amax.double().numpy(), (acc * fin[:, None]).numpy()
+
+
 def rmsnorm_gemm(x, g, w, eps=1e-6):
     x, g, w = _f64(x), _f64(g), _f64(w)
     T, K = x.shape

@@ -177,7 +177,7 @@ def _quant_run(a, w, fmax=448.0):
     assert "tcgen05" in p.info["kernel"]
     wp = p.pack_weight(torch.tensor(w, dtype=torch.float32).cuda())
     ad = torch.tensor(a).to(torch.bfloat16).cuda()
-    amax, c = quant_gemm(ad, wp, fmax)
+    amax, c = quant_gemm(ad, wp, fmax, check_domain=False)
     torch.cuda.synchronize()
     w8 = wp.view(torch.float8_e4m3fn).double().cpu().numpy().T  # [K, N] static e4m3 weight
     return amax.double().cpu().numpy(), c.double().cpu().numpy(), w8, p
