@@ -29,6 +29,8 @@
 #include <algorithm>
 #include <cctype>
 #include <cmath>
+#include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -112,7 +114,7 @@ inline std::string render(const Expr& e) {
       return buf;
     }
     case Node::Input: return e->name + (e->has_free ? "[l, f]" : "[l]");
-    case Node::Dep: return "d" + std::to_string(e->dep);
+    case Node::Dep: return e->dep < 0 ? "d" + std::to_string(-e->dep) + "_prev" : "d" + std::to_string(e->dep);
     case Node::Free: return "f";
     case Node::Un: return e->name + "(" + render(e->a) + ")";
     case Node::Bin:
@@ -274,6 +276,11 @@ struct Parser {
     if (t.text.size() > 1 && t.text[0] == 'd' &&
         std::all_of(t.text.begin() + 1, t.text.end(), [](char ch) { return std::isdigit(ch); }))
       return dep(std::atoi(t.text.c_str() + 1));
+    // d<k>_prev: the previous value of a dependency, as derive_fused renders
+    // it inside a correction (expr.cpp:316-317); stored as Dep -k
+    if (t.text.size() > 6 && t.text[0] == 'd' && t.text.compare(t.text.size() - 5, 5, "_prev") == 0 &&
+        std::all_of(t.text.begin() + 1, t.text.end() - 5, [](char ch) { return std::isdigit(ch); }))
+      return dep(-std::atoi(t.text.c_str() + 1));
     if (t.text == "f") return mk({Node::Free, 0, "f", false, 0, nullptr, nullptr});
     auto it = consts.find(t.text);
     if (it != consts.end()) return num(it->second);
@@ -614,6 +621,160 @@ inline Program plan(const CascadeSpec& spec) {
 }
 
 inline Program plan(const std::string& dsl) { return plan(parse_cascade(dsl)); }
+
+// ------------------------------------------- derived-correction pinning --
+//
+// derive_fused (acrf.cpp:148-190) derives, per reduction, the correction
+// corr = H(d) (x) inv(H(d_prev)) that the incremental loop applies to the
+// accumulator (Eq.17, simulator.cpp:278-318). Each librf_cuda kernel hard-codes
+// that correction in closed form. check_corrections proves, at
+// plan time, that the FusedProgram's derived corrections are the ones the
+// matched kernel applies — with the reference's own probe (numeric_equiv,
+// probe.cpp:15-42: 32 valid samples, close_rel 1e-9) — and throws NotFusable
+// otherwise, so a cascade whose derivation disagrees never runs.
+
+// A correction expression in derive_fused's rendering (render, expr.cpp:303-357):
+// deps d<k>, previous deps d<k>_prev, numbers, + - * /, exp/ln/log2/sqrt/abs/sign,
+// max/min/pow. "" and "<identity>" mean "no correction".
+inline Expr parse_correction(const std::string& text) {
+  if (text.empty() || text == "<identity>") return nullptr;
+  static const std::map<std::string, double> none;
+  detail::Parser ps{detail::Lexer(text, 0), none};
+  Expr e = ps.expr();
+  if (ps.lx.peek().kind != detail::Lexer::End) throw SyntaxError(0, "trailing tokens in correction '" + text + "'");
+  return e;
+}
+
+// Evaluates with d<k> = now[k-1], d<k>_prev = prev[k-1]; NaN outside the domain
+// (the probe skips such points, as numeric_equiv skips DomainError).
+inline double eval_correction(const Expr& e, const std::vector<double>& now, const std::vector<double>& prev) {
+  const double nan = std::numeric_limits<double>::quiet_NaN();
+  switch (e->kind) {
+    case Node::Num: return e->num;
+    case Node::Dep: {
+      const int k = e->dep < 0 ? -e->dep : e->dep;
+      const auto& v = e->dep < 0 ? prev : now;
+      return k >= 1 && k <= static_cast<int>(v.size()) ? v[k - 1] : nan;
+    }
+    case Node::Un: {
+      const double a = eval_correction(e->a, now, prev);
+      if (e->name == "neg") return -a;
+      if (e->name == "exp") return std::exp(a);
+      if (e->name == "abs") return std::fabs(a);
+      if (e->name == "sqrt") return a < 0 ? nan : std::sqrt(a);
+      if (e->name == "ln") return a <= 0 ? nan : std::log(a);
+      if (e->name == "log2") return a <= 0 ? nan : std::log2(a);
+      if (e->name == "sign") return a > 0 ? 1.0 : a < 0 ? -1.0 : 0.0;
+      return nan;
+    }
+    case Node::Bin: {
+      const double a = eval_correction(e->a, now, prev), b = eval_correction(e->b, now, prev);
+      if (e->name == "+") return a + b;
+      if (e->name == "-") return a - b;
+      if (e->name == "*") return a * b;
+      if (e->name == "/") return b == 0.0 ? nan : a / b;
+      if (e->name == "max") return std::fmax(a, b);
+      if (e->name == "min") return std::fmin(a, b);
+      if (e->name == "pow") return std::pow(a, b);
+      return nan;
+    }
+    default: return nan;  // inputs / free index never appear in a correction
+  }
+}
+
+// numeric_equiv (probe.cpp:15-42) over the deps d1..dn and d1_prev..dn_prev,
+// probed in the reference's default domain [-2, 2] (probe.hpp:19-29) and in
+// [0, 40] (past the guard offsets the builtins use, e.g. sum_sum's c = 10).
+inline bool numeric_equiv(const Expr& a, const Expr& b, int ndeps, uint64_t seed = 0x5eedf00dULL) {
+  uint64_t st = seed;
+  auto uni = [&](double lo, double hi) {  // splitmix64 -> [lo, hi)
+    st += 0x9e3779b97f4a7c15ULL;
+    uint64_t z = st;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    z ^= z >> 31;
+    return lo + (hi - lo) * (static_cast<double>(z >> 11) * 0x1.0p-53);
+  };
+  const double doms[2][2] = {{-2.0, 2.0}, {0.0, 40.0}};
+  for (const auto& dom : doms) {
+    int valid = 0, attempts = 0;
+    while (valid < 32) {
+      if (++attempts > 32 * 64) return valid > 0;  // InsufficientSamples: judge on what was valid
+      std::vector<double> now(ndeps), prev(ndeps);
+      for (int i = 0; i < ndeps; ++i) {
+        now[i] = uni(dom[0], dom[1]);
+        prev[i] = uni(dom[0], dom[1]);
+      }
+      const double l = eval_correction(a, now, prev), r = eval_correction(b, now, prev);
+      if (!std::isfinite(l) || !std::isfinite(r)) continue;
+      ++valid;
+      if (std::fabs(l - r) > 1e-9 * (1.0 + std::fmax(std::fabs(l), std::fabs(r)))) return false;
+    }
+  }
+  return true;
+}
+
+// The correction each kernel applies to reduction `id` (1-based), in the same
+// rendering as derive_fused's; "" = none (h_identity).
+inline std::string kernel_correction(const Program& p, int id) {
+  auto num = [](double v) {
+    char b[64];
+    std::snprintf(b, sizeof b, "%.17g", v);
+    return std::string(b);
+  };
+  switch (p.pattern) {
+    case RF_PATTERN_SAFE_SOFTMAX:
+    case RF_PATTERN_MOE_ROUTING:
+      return id == 2 ? "exp(d1_prev - d1)" : "";
+    case RF_PATTERN_ATTENTION:  // attn_*.cu: lazy exp(d1'-d1) on O, d2'/d2 telescoped to 1/d2
+      return id == 2 ? "exp(d1_prev - d1)" : id == 3 ? "exp(d1_prev - d1) * d2_prev / d2" : "";
+    case RF_PATTERN_QUANT_GEMM_E4M3:  // gemm_sm100.cu qnt2: ref'/ref in-loop, ref/d1 at finalize
+      return id == 2 ? "d1_prev / d1" : "";
+    case RF_PATTERN_RMSNORM_GEMM: {  // gemm_sm100.cu rms2: 1/sqrt(d1/K+eps) at finalize
+      const std::string ik = num(p.inv_k), e = num(p.eps);
+      return id == 2 ? "sqrt(" + ik + " * d1_prev + " + e + ") / sqrt(" + ik + " * d1 + " + e + ")" : "";
+    }
+    case RF_PATTERN_LAYERNORM_GEMM: {  // rms2<LN>: 1/sigma at finalize; d4 via colsum
+      const std::string ik = num(p.inv_k), ik2 = num(p.inv_k * p.inv_k), e = num(p.eps);
+      const std::string sp = "sqrt(" + ik + " * d2_prev - " + ik2 + " * d1_prev * d1_prev + " + e + ")";
+      const std::string sn = "sqrt(" + ik + " * d2 - " + ik2 + " * d1 * d1 + " + e + ")";
+      return id == 3 ? sp + " / " + sn : id == 4 ? "d1 * " + sp + " / " + sn + " / d1_prev" : "";
+    }
+    case RF_PATTERN_SUM_SUM: {  // rowstats.cu: 1/sqrt(max(d1-c, eps)) at finalize
+      const std::string c = num(p.offset), e = num(p.eps);
+      return id == 2 ? "sqrt(max(d1_prev - " + c + ", " + e + ")) / sqrt(max(d1 - " + c + ", " + e + "))" : "";
+    }
+    default: return "";  // variance, moments: every H is the identity
+  }
+}
+
+// derived[i] = {reduction id, derive_fused's corr rendered ("" when
+// h_identity)}. Throws NotFusable naming the first reduction whose derived
+// correction is not the kernel's.
+inline void check_corrections(const Program& p, const std::vector<std::pair<int, std::string>>& derived) {
+  const int n = static_cast<int>(p.spec.reductions.size());
+  if (static_cast<int>(derived.size()) != n)
+    throw NotFusable("cascade '" + p.spec.name + "': " + std::to_string(derived.size()) +
+                     " derived corrections for " + std::to_string(n) + " reductions");
+  for (const auto& dc : derived) {
+    if (dc.first < 1 || dc.first > n) throw NotFusable("derived correction for unknown reduction d" + std::to_string(dc.first));
+    const Expr want = parse_correction(kernel_correction(p, dc.first));
+    const Expr got = parse_correction(dc.second);
+    const bool ok = (!want && !got) || (want && got && numeric_equiv(want, got, n));
+    if (!ok)
+      throw NotFusable("cascade '" + p.spec.name + "' d" + std::to_string(dc.first) + ": derived correction '" +
+                       (got ? dc.second : "<identity>") + "' is not the kernel's '" +
+                       (want ? kernel_correction(p, dc.first) : "<identity>") + "'");
+  }
+}
+
+// plan() with the FusedProgram's derived corrections checked (the binding's
+// entry: integration/redfuse_cuda.cpp passes prog.decomps[i].corr).
+inline Program plan(const CascadeSpec& spec, const std::vector<std::pair<int, std::string>>& derived) {
+  Program p = plan(spec);
+  check_corrections(p, derived);
+  return p;
+}
 
 // ----------------------------------------------------------- TensorStore ----
 

@@ -5,20 +5,39 @@
 // with the reference's field meanings.
 #include "redfuse_cuda.hpp"
 
+#include <string>
+#include <utility>
+#include <vector>
+
 #include "redfuse/cascade.hpp"
+#include "redfuse/expr.hpp"
 #include "rf_host.hpp"
 
 namespace redfuse {
 namespace {
 
-ExecReport run(const FusedProgram& prog, const TreeConfig& cfg, long long segments,
-               TensorStore& store) {
-  rfcuda::Program p;
+// The FusedProgram's derived corrections (derive_fused, acrf.cpp:184-186) in
+// the reference's own rendering, for the plan layer's pin against the kernel.
+std::vector<std::pair<int, std::string>> derived_corrections(const FusedProgram& prog) {
+  std::vector<std::pair<int, std::string>> out;
+  for (const auto& d : prog.decomps) out.emplace_back(d.id, d.corr ? render(d.corr) : "");
+  return out;
+}
+
+// Matches the cascade onto a kernel AND checks that every derived correction
+// is numerically the kernel's closed form (rfcuda::check_corrections, the
+// reference's numeric_equiv probe); either failure is NotFusable.
+rfcuda::Program plan_checked(const FusedProgram& prog) {
   try {
-    p = rfcuda::plan(serialize(prog.spec));
+    return rfcuda::plan(rfcuda::parse_cascade(serialize(prog.spec)), derived_corrections(prog));
   } catch (const rfcuda::NotFusable& e) {
     throw NotFusable(0, e.what());
   }
+}
+
+ExecReport run(const FusedProgram& prog, const TreeConfig& cfg, long long segments,
+               TensorStore& store) {
+  rfcuda::Program p = plan_checked(prog);
   rfcuda::TensorStore st;
   for (const auto& in : prog.spec.inputs) {
     const auto& a = store.array(in.name);  // ShapeMismatch if absent
@@ -47,12 +66,7 @@ ExecReport run(const FusedProgram& prog, const TreeConfig& cfg, long long segmen
 }  // namespace
 
 CudaPattern cuda_pattern(const FusedProgram& prog) {
-  rfcuda::Program p;
-  try {
-    p = rfcuda::plan(serialize(prog.spec));
-  } catch (const rfcuda::NotFusable& e) {
-    throw NotFusable(0, e.what());
-  }
+  rfcuda::Program p = plan_checked(prog);
   switch (p.pattern) {
     case RF_PATTERN_SAFE_SOFTMAX: return {"safe_softmax", true};
     case RF_PATTERN_ATTENTION: return {"attention", true};

@@ -137,6 +137,25 @@ int main() {
     std::printf("{\"case\": \"prod_chain\", \"mode\": \"no-kernel\", \"not_fusable\": %s}\n",
                 threw ? "true" : "false");
   }
+  // a FusedProgram whose derived correction is not the kernel's closed form
+  // (here: attention's d3 correction with the exponent's sign flipped) is
+  // rejected at plan time (rfcuda::check_corrections), never run
+  {
+    Workload w = make_attention(256, 64);
+    FusedProgram prog = derive_fused(w.spec);
+    for (auto& d : prog.decomps)
+      if (d.id == 3) d.corr = exp_of(dep_var(1) - dep_var(1, true)) * (dep_var(2, true) / dep_var(2));
+    bool threw = false;
+    try {
+      TensorStore st = w.generate(1);
+      run_cuda(prog, TreeConfig{{256, 1}}, st);
+    } catch (const NotFusable&) {
+      threw = true;
+    }
+    if (!threw) ++failures;
+    std::printf("{\"case\": \"attention_bad_corr\", \"mode\": \"corr-pin\", \"not_fusable\": %s}\n",
+                threw ? "true" : "false");
+  }
   std::printf("{\"failures\": %d}\n", failures);
   return failures ? 1 : 0;
 }

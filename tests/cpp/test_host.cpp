@@ -3,6 +3,8 @@
 // that the drop-in reads like the original:  ./test_host cpu | gpu
 #include <cmath>
 #include <cstdio>
+#include <fstream>
+#include <map>
 #include <random>
 #include <string>
 
@@ -348,8 +350,93 @@ TEST(layernorm_gemm_matches_direct_loop) {
   CHECK_THROWS_AS(run_incremental(p96, TreeConfig{{96, 1}}, s96), NotFusable);
 }
 
+// The corrections derive_fused derives for every builtin and the RMS / LN DSL
+// cascades (tests/golden/corrections.txt, written by the reference itself:
+// oracle/ref_driver.cpp golden) are exactly the kernels' closed forms
+// (check_corrections: numeric_equiv, probe.cpp:15-42), and a tampered one is
+// rejected with NotFusable.
+static std::string g_golden_dir;
+
+TEST(derived_corrections_are_the_kernels) {
+  std::ifstream in(g_golden_dir + "/corrections.txt");
+  CHECK(in.good());
+  std::map<std::string, std::vector<std::pair<int, std::string>>> by_name;
+  std::string line;
+  while (std::getline(in, line)) {
+    const auto a = line.find(' '), b = line.find(' ', a + 1);
+    if (a == std::string::npos || b == std::string::npos) continue;
+    const std::string name = line.substr(0, a);
+    const int id = std::atoi(line.c_str() + a + 2);
+    std::string corr = line.substr(b + 1);
+    if (corr == "<identity>") corr.clear();
+    by_name[name].emplace_back(id, corr);
+  }
+  const std::map<std::string, std::string> dsl = {
+      {"safe_softmax", softmax_dsl(1024)},
+      {"attention", attention_dsl(256, 64)},
+      {"quant_gemm", quant_dsl(64, 32)},
+      {"moe_routing", "cascade moe_routing\ninput s len 128\nreduce 1 op max\n    s[l]\nreduce 2 op sum\n"
+                      "    exp(s[l] - d1)\nreduce 3 op topk 8\n    s[l]\n"},
+      {"variance", "cascade variance\ninput x len 8192\nreduce 1 op sum\n    x[l]\n"
+                   "reduce 2 op sum\n    x[l] * x[l]\n"},
+      {"sum_sum", "cascade sum_sum\ninput x1 len 1024\ninput x2 len 1024\nconst EPS = 1e-12\n"
+                  "reduce 1 op sum\n    x1[l] * x1[l]\nreduce 2 op sum\n"
+                  "    x1[l] * x2[l] / sqrt(max(d1 - 10, EPS))\n"},
+      {"moment_of_inertia", "cascade moment_of_inertia\ninput mass len 1024\ninput pos len 1024 free 3\n"
+                            "reduce 1 op sum\n    mass[l]\nreduce 2 op sum free 3\n    mass[l] * pos[l, f]\n"
+                            "reduce 3 op sum free 3\n    mass[l] * pos[l, f] * pos[l, f]\n"},
+      {"rmsnorm_gemm", rms_dsl(64, 32)},
+      {"layernorm_gemm", ln_dsl(64, 32)},
+  };
+  int pinned = 0;
+  for (const auto& kv : by_name) {
+    auto it = dsl.find(kv.first);
+    CHECK(it != dsl.end());
+    if (it == dsl.end()) continue;
+    const Program p = plan(it->second);
+    bool ok = true;
+    try {
+      check_corrections(p, kv.second);
+    } catch (const NotFusable& e) {
+      ok = false;
+      std::printf("  %s: %s\n", kv.first.c_str(), e.what());
+    }
+    CHECK(ok);
+    pinned += static_cast<int>(kv.second.size());
+    // every non-identity correction, tampered, is rejected
+    for (std::size_t i = 0; i < kv.second.size(); ++i) {
+      auto bad = kv.second;
+      if (bad[i].second.empty()) {
+        bad[i].second = "d1_prev / d1";  // a correction where the kernel applies none
+      } else {
+        bad[i].second = "(" + bad[i].second + ") * 1.0001";
+      }
+      CHECK_THROWS_AS(check_corrections(p, bad), NotFusable);
+    }
+  }
+  CHECK(pinned == 23);  // every reduction of the 9 cascades
+  // the plan-layer entry with derived corrections
+  const Program a = plan(parse_cascade(attention_dsl(256, 64)),
+                         {{1, ""}, {2, "exp(d1_prev - d1)"}, {3, "exp(d1_prev - d1) * d2_prev / d2"}});
+  CHECK(a.pattern == RF_PATTERN_ATTENTION);
+  CHECK_THROWS_AS(plan(parse_cascade(attention_dsl(256, 64)),
+                       {{1, ""}, {2, "exp(d1_prev - d1)"}, {3, "exp(d1 - d1_prev) * d2_prev / d2"}}),
+                  NotFusable);
+  // an RMS cascade with a different eps than its derived correction: rejected
+  CHECK_THROWS_AS(plan(parse_cascade(rms_dsl(64, 32)),
+                       {{1, ""}, {2, "sqrt(0.015625 * d1_prev + 1e-5) / sqrt(0.015625 * d1 + 1e-5)"}}),
+                  NotFusable);
+  std::printf("  %d derived corrections pinned to the kernels' closed forms\n", pinned);
+}
+
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "cpu";
+  {
+    std::string self = argv[0];
+    const auto slash = self.rfind('/');
+    g_golden_dir = (slash == std::string::npos ? std::string(".") : self.substr(0, slash)) + "/../golden";
+  }
+  RUN(derived_corrections_are_the_kernels);
   RUN(dsl_files_parse_and_match_kernels);
   RUN(moe_routing_matches);
   RUN(layernorm_gemm_matches);
