@@ -1,3 +1,5 @@
+// EXPERIMENTAL, not part of librf_cuda: measured slower than attn_sm100.cu on
+// cfg2; kept for the record and the probe library's traces.
 // bf16 safe-softmax -> GEMM attention on a CTA PAIR (2-SM UMMA, sm_100a).
 //
 // Same cascade and incremental form as attn_sm100.cu (the reference's
@@ -27,8 +29,8 @@
 //        16 TMA, 17 MMA issuer (leader) / K-V + Q relay (peer), 18 P relay (peer).
 #include <cuda_bf16.h>
 
-#include "rf_internal.h"
-#include "sm100.cuh"
+#include "../rf_internal.h"
+#include "../sm100.cuh"
 
 #ifdef RF_ATTN_TRACE
 // Test-only timeline of the first cluster: [rank*1024 + ...] (tools/trace_attention.py)

@@ -1,3 +1,5 @@
+// EXPERIMENTAL, not part of librf_cuda: measured slower than attn_sm100.cu on
+// cfg2; kept for the record and the probe library's traces.
 // bf16 safe-softmax -> GEMM attention: the 1-SM ping-pong kernel
 // (attn_sm100.cu) on a CTA PAIR with 2-SM UMMA (cta_group::2), sm_100a.
 //
@@ -24,8 +26,8 @@
 // 8 TMA, 9 MMA issuer (leader) / K-V + Q relay (peer), 10-11 P relays (peer).
 #include <cuda_bf16.h>
 
-#include "rf_internal.h"
-#include "sm100.cuh"
+#include "../rf_internal.h"
+#include "../sm100.cuh"
 
 namespace rf {
 namespace {

@@ -1,5 +1,5 @@
 // TEST-ONLY: timeline reader for the traced 2-SM attention kernel.
-#include "../attn_sm100_2sm.cu"
+#include "../experimental/attn_sm100_2sm.cu"
 
 extern "C" int rf_probe_attn2_trace(const void* q, const void* k, const void* v, void* o, float* m,
                                     float* l, long long bh, long long s, long long* out) {

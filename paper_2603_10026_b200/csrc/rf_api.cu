@@ -163,8 +163,6 @@ const char* kernel_name(rf::Kernel k) {
     case rf::Kernel::SoftmaxRows: return "softmax_rows (SIMT, single pass)";
     case rf::Kernel::AttentionF32: return "attention_f32 (SIMT, paper form)";
     case rf::Kernel::AttentionSm100: return "attention_sm100 (bf16 tcgen05/TMEM/TMA)";
-    case rf::Kernel::AttentionSm100x2: return "attention_sm100_2sm (bf16 tcgen05 cta_group::2 pair/TMEM/TMA)";
-    case rf::Kernel::AttentionSm100Pair: return "attention_sm100_pair (bf16 tcgen05 cta_group::2, ping-pong Q tiles/TMEM/TMA)";
     case rf::Kernel::AttentionDecode: return "attention_decode (bf16 split-KV, TMA bulk)";
     case rf::Kernel::QuantGemmSm100: return "quant_gemm_sm100 (e4m3 tcgen05 kind::f8f6f4)";
     case rf::Kernel::RmsGemmSm100: return "rmsnorm_gemm_sm100 (bf16 tcgen05 kind::f16)";
@@ -221,8 +219,6 @@ rf_status attention_run(const rf_plan* p, const rf_io* io, int64_t bh0, int64_t 
   cudaError_t e;
   switch (p->kernel) {
     case rf::Kernel::AttentionSm100: e = rf::launch_attention_sm100(a, st); break;
-    case rf::Kernel::AttentionSm100x2: e = rf::launch_attention_sm100_2sm(a, st); break;
-    case rf::Kernel::AttentionSm100Pair: e = rf::launch_attention_sm100_pair(a, st); break;
     case rf::Kernel::AttentionDecode: e = rf::launch_attention_decode(a, st); break;
     default: e = rf::launch_attention_f32(a, st); break;
   }
@@ -441,22 +437,8 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
       } else if (d.rows == 1) {
         p->kernel = rf::Kernel::AttentionDecode;
         p->nsplit = pick_decode_splits(d.batch * d.heads, d.len, d.segments);
-      } else if (rf::attention_sm100_pair_supports(d.rows, d.len, d.free_len, d.segments) &&
-                 std::getenv("RF_ATTN_PAIR") && std::string(std::getenv("RF_ATTN_PAIR")) == "2") {
-        // ping-pong Q tiles on a CTA pair (cta_group::2): correct, measured ~2 %
-        // slower than the 1-SM kernel on cfg2 (the peer's P relay lengthens
-        // the softmax -> PV -> S chain); opt-in
-        p->kernel = rf::Kernel::AttentionSm100Pair;
-      } else if (rf::attention_sm100_2sm_supports(d.rows, d.len, d.free_len, d.segments) &&
-                 std::getenv("RF_ATTN_PAIR")) {
-        // CTA-pair kernel (cta_group::2): correct, but measured ~8% slower than
-        // the 1-SM ping-pong kernel on cfg2 (softmax-bound);
-        // opt-in until it is made persistent.
-        p->kernel = rf::Kernel::AttentionSm100x2;
       } else if (rf::attention_sm100_supports(d.rows, d.len, d.free_len, d.segments)) {
         p->kernel = rf::Kernel::AttentionSm100;
-      } else if (rf::attention_sm100_2sm_supports(d.rows, d.len, d.free_len, d.segments)) {
-        p->kernel = rf::Kernel::AttentionSm100x2;
       } else {
         p->kernel = rf::Kernel::AttentionF32;  // SIMT CUDA path for odd shapes
       }
@@ -759,8 +741,6 @@ rf_status rf_run_partials(const rf_plan* p, const rf_io* io, int64_t slice_begin
   cudaError_t e;
   switch (p->kernel) {
     case rf::Kernel::AttentionSm100: e = rf::launch_attention_sm100(a, as_stream(stream)); break;
-    case rf::Kernel::AttentionSm100x2: e = rf::launch_attention_sm100_2sm(a, as_stream(stream)); break;
-    case rf::Kernel::AttentionSm100Pair: e = rf::launch_attention_sm100_pair(a, as_stream(stream)); break;
     case rf::Kernel::AttentionDecode: e = rf::launch_attention_decode(a, as_stream(stream)); break;
     default: e = rf::launch_attention_f32(a, as_stream(stream)); break;
   }

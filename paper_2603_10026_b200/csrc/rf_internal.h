@@ -27,8 +27,6 @@ enum class Kernel {
   SoftmaxRows,        // softmax.cu
   AttentionF32,       // attn_f32.cu   (SIMT, paper form, cfg1)
   AttentionSm100,     // attn_sm100.cu (bf16 tcgen05/TMEM/TMA prefill)
-  AttentionSm100x2,   // attn_sm100_2sm.cu (bf16, CTA pair, cta_group::2, one Q tile per CTA)
-  AttentionSm100Pair, // attn_sm100_pair.cu (bf16, CTA pair, cta_group::2, ping-pong Q tiles; cfg2)
   AttentionDecode,    // attn_decode.cu (bf16 split-KV streaming, cfg3)
   QuantGemmSm100,     // gemm_sm100.cu (e4m3 kind::f8f6f4, cfg4)
   RmsGemmSm100,       // gemm_sm100.cu (bf16 kind::f16, cfg5)
@@ -115,10 +113,9 @@ cudaError_t launch_attention_decode(const AttnArgs& a, cudaStream_t st);
 // Returns cudaErrorNotSupported when the shape has no tcgen05 instantiation.
 cudaError_t launch_attention_sm100(const AttnArgs& a, cudaStream_t st);
 bool attention_sm100_supports(int64_t sq, int64_t skv, int64_t d, int64_t segments);
+// experimental/attn_sm100_2sm.cu (probe library only; not in librf_cuda)
 cudaError_t launch_attention_sm100_2sm(const AttnArgs& a, cudaStream_t st);
 bool attention_sm100_2sm_supports(int64_t sq, int64_t skv, int64_t d, int64_t segments);
-cudaError_t launch_attention_sm100_pair(const AttnArgs& a, cudaStream_t st);
-bool attention_sm100_pair_supports(int64_t sq, int64_t skv, int64_t d, int64_t segments);
 
 // Slice-ordered fold of partial (m, l, O) states (incr_push_child).
 cudaError_t launch_attention_merge(const float* pm, const float* pl, const float* po,

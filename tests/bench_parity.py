@@ -155,16 +155,19 @@ def check_quant(wl):
     t1, tc = O.quant_gemm_e4m3_torch(A, W, fmax, 128, pow2=True)
     _, uc = O.quant_gemm(A, W, fmax)
     _, ac = O.quant_gemm_e4m3_torch(A, W, fmax, 128, pow2=False)
-    errs = {"d1": _err(g1, r1), "d2": _err(gc, rc),
-            "vs_torch_emulation_d2": _err(gc, tc),
-            "vs_true_amax_e4m3_d2": _err(gc, ac),
-            "vs_unrounded_reference_d2": _err(gc, uc)}
-    rms = float(np.sqrt(np.mean((gc - uc) ** 2)) / np.sqrt(np.mean(uc ** 2)))
+    def rms(x, y):  # RMS relative error: the max scaled error of outputs that
+        # differ by ~1 % of their norm is dominated by elements near zero
+        return float(f"{np.sqrt(np.mean((x - y) ** 2) / np.mean(y ** 2)):.3e}")
+
+    errs = {"d1": _err(g1, r1), "d2": _err(gc, rc), "vs_torch_emulation_d2": _err(gc, tc)}
     return _result(errs, len(rows), TOL["bf16"],
                    "rfo_quant_gemm_e4m3 (C restatement of the kernel's e4m3 scheme on the same "
-                   "bf16 A / e4m3 W); vs_* = not gated",
+                   "bf16 A / e4m3 W), cross-checked by an independent torch float8_e4m3fn "
+                   "emulation; rms_rel_* = not gated",
                    {"oracle_pair_agreement_d2": float(f"{_err(rc, tc):.3e}"),
-                    "rms_rel_vs_unrounded_reference": float(f"{rms:.3e}")})
+                    "rms_rel_vs_true_amax_e4m3": rms(gc, ac),
+                    "rms_rel_vs_unrounded_reference": rms(gc, uc),
+                    "rms_rel_true_amax_vs_unrounded_reference": rms(ac, uc)})
 
 
 def check_rms(wl, ln=False):

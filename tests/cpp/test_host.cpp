@@ -301,12 +301,23 @@ static void rms_case(long long k, long long n, unsigned seed) {
   for (double v : x) ss += v * v;
   ExecReport want;
   want.outputs = {{1, {ss}, {}}, {2, std::vector<double>(n, 0.0), {}}};
-  for (long long l = 0; l < k; ++l)
+  // the reference on the same rounded inputs: bf16 x and the bf16(g * w) the
+  // kernel's packed weight holds
+  using rfcuda::detail::from_bf16;
+  using rfcuda::detail::to_bf16;
+  double ssr = 0;
+  for (double v : x) ssr += static_cast<double>(from_bf16(to_bf16(static_cast<float>(v)))) *
+                            from_bf16(to_bf16(static_cast<float>(v)));
+  want.outputs[0].v[0] = ssr;
+  for (long long l = 0; l < k; ++l) {
+    const double xr = from_bf16(to_bf16(static_cast<float>(x[l])));
     for (long long f = 0; f < n; ++f)
-      want.outputs[1].v[f] += x[l] * g[l] / std::sqrt(ss / k + 1e-6) * w[l * n + f];
-  DiffReport d = compare_reports(r, want, 2e-2);  // bf16 operands (unrounded reference)
+      want.outputs[1].v[f] += xr * from_bf16(to_bf16(static_cast<float>(g[l] * w[l * n + f]))) /
+                              std::sqrt(ssr / k + 1e-6);
+  }
+  DiffReport d = compare_reports(r, want, 2e-2);  // north_star: 2e-2 on the same rounded inputs
   CHECK(d.pass);
-  std::printf("  rmsnorm k=%lld scaled err vs unrounded reference: %.3g (%s)\n", k, d.max_rel_err,
+  std::printf("  rmsnorm k=%lld scaled err vs the same-rounded reference: %.3g (%s)\n", k, d.max_rel_err,
               d.worst.c_str());
 }
 

@@ -37,51 +37,6 @@ def test_tcgen05_prefill_vs_oracle(D, shape):
     assert max(errs) < TOL
 
 
-@pytest.mark.parametrize("segments", [1, 2])
-def test_cta_pair_kernel(monkeypatch, segments):
-    """The CTA-pair kernel (tcgen05.mma.cta_group::2, attn_sm100_2sm.cu), opt-in."""
-    monkeypatch.setenv("RF_ATTN_PAIR", "1")
-    for shape in [(1, 2, 256, 1024), (2, 1, 512, 256), (1, 1, 1024, 4096)]:
-        errs, (m, l, o) = _run(*shape, 128, seed=3, segments=segments, expect="2sm")
-        assert max(errs) < TOL
-
-
-@pytest.mark.parametrize("segments", [1, 2])
-def test_cta_pair_pingpong_kernel(monkeypatch, segments):
-    """The ping-pong CTA-pair kernel (two Q tiles per CTA, cta_group::2,
-    attn_sm100_pair.cu), opt-in with RF_ATTN_PAIR=2; incl. the rescale path."""
-    import torch
-    from paper_2603_10026_b200 import attention
-
-    monkeypatch.setenv("RF_ATTN_PAIR", "2")
-    for shape in [(1, 2, 512, 1024), (2, 1, 1024, 512)]:
-        errs, (m, l, o) = _run(*shape, 128, seed=5, segments=segments, expect="attention_sm100_pair")
-        assert max(errs) < TOL
-    B, H, Sq, Skv, D = 1, 1, 512, 2048, 128
-    q, k, v = _inputs(B, H, Sq, Skv, D, 9, torch.float64)
-    k = k * (1 + torch.linspace(0.0, 8.0, Skv, dtype=torch.float64).view(1, 1, Skv, 1))
-    q, k, v = (t.to(torch.bfloat16) for t in (q, k, v))
-    m, l, o = attention(q.cuda(), k.cuda(), v.cuda(), segments=segments)
-    torch.cuda.synchronize()
-    _check(q, k, v, m, l, o, TOL)
-
-
-def test_cta_pair_rescale_path(monkeypatch):
-    """Growing logits: the pair kernel's lazy correction waits for PV_{i-1}."""
-    import torch
-    from paper_2603_10026_b200 import attention
-
-    monkeypatch.setenv("RF_ATTN_PAIR", "1")
-    B, H, Sq, Skv, D = 1, 2, 512, 2048, 128
-    q, k, v = _inputs(B, H, Sq, Skv, D, 9, torch.float64)
-    ramp = torch.linspace(0.0, 8.0, Skv, dtype=torch.float64).view(1, 1, Skv, 1)
-    k = k * (1 + ramp)
-    q, k, v = (t.to(torch.bfloat16) for t in (q, k, v))
-    m, l, o = attention(q.cuda(), k.cuda(), v.cuda(), segments=2)
-    torch.cuda.synchronize()
-    _check(q, k, v, m, l, o, TOL)
-
-
 @pytest.mark.parametrize("segments", [2, 4])
 def test_tcgen05_prefill_multisegment(segments):
     errs, _ = _run(1, 2, 256, 1024, 128, segments=segments, expect="tcgen05")
