@@ -900,20 +900,6 @@ inline float from_bf16(uint16_t h) {
 }
 inline long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
 
-inline void check_shapes(const Program& prog, const TreeConfig& cfg, const TensorStore& st) {
-  // validate_tree (cascade.cpp:37-66) + store shapes (simulator.cpp:235-245)
-  if (cfg.levels.size() < 2 || cfg.levels.front() != prog.L0 || cfg.levels.back() != 1)
-    throw ShapeMismatch("BadTree: levels must run from L0 = " + std::to_string(prog.L0) + " to 1");
-  for (std::size_t k = 1; k < cfg.levels.size(); ++k)
-    if (cfg.levels[k] <= 0 || cfg.levels[k - 1] % cfg.levels[k] != 0)
-      throw ShapeMismatch("BadTree: level widths must divide");
-  for (const auto& in : prog.spec.inputs) {
-    const auto& a = st.array(in.name);
-    if (a.len != in.len || a.free_len != in.free_len)
-      throw ShapeMismatch(in.name + ": store shape does not match the spec");
-  }
-}
-
 // The fused loop's counters: every input element loaded once
 // (acceptance crit 6), root dependency reads once per corrected reduction at
 // finalize (crit 7, simulator.cpp:617), O(1) auxiliary state per level (crit 8).
@@ -929,208 +915,267 @@ inline void fill_counters(const Program& prog, const TreeConfig& cfg, ExecReport
   for (int m = 1; m <= cfg.depth(); ++m) r.peak_aux_slots[m] = arity;
 }
 
-inline ExecReport execute(const Program& prog, const TreeConfig& cfg, long long segments,
-                          TensorStore& st, const std::string& strategy) {
-  check_shapes(prog, cfg, st);
+// One host-side operand of a batched run: R rows of [len(, free)] values,
+// or one array every row shares (a static weight).
+inline const double* row_ptr(const std::vector<double>& data, bool shared, long long per_row, long long r) {
+  return data.data() + (shared ? 0 : r * per_row);
+}
+
+}  // namespace detail
+
+// ----------------------------------------------------------- BatchedStore --
+//
+// The rows axis the reference lacks (it exists only as scalar_ir's
+// EmitStrategy.rows, scalar_ir.hpp:77): R instances of one cascade, each the
+// reference's TensorStore row. An input is per row ([R, len(, free)],
+// row-major, reduce-axis-major inside a row like TensorStore) or shared by
+// every row ([len(, free)], e.g. the static GEMM weight and gamma).
+class BatchedStore {
+ public:
+  struct Array {
+    std::vector<double> data;
+    long long rows = 1, len = 0, free_len = 0;
+    bool shared = false;
+    long long per_row() const { return free_len > 0 ? len * free_len : len; }
+  };
+  void define_rows(const std::string& name, long long rows, long long len, long long free_len,
+                   std::vector<double> data) {
+    Array a;
+    a.rows = rows;
+    a.len = len;
+    a.free_len = free_len;
+    if (rows < 0 || static_cast<long long>(data.size()) != rows * a.per_row())
+      throw ShapeMismatch(name + ": got " + std::to_string(data.size()) + " values, want " +
+                          std::to_string(rows) + " x " + std::to_string(a.per_row()));
+    a.data = std::move(data);
+    arrays_[name] = std::move(a);
+  }
+  void define_shared(const std::string& name, long long len, long long free_len, std::vector<double> data) {
+    define_rows(name, 1, len, free_len, std::move(data));
+    arrays_[name].shared = true;
+  }
+  const Array& array(const std::string& name) const {
+    auto it = arrays_.find(name);
+    if (it == arrays_.end()) throw ShapeMismatch("no array named " + name);
+    return it->second;
+  }
+  // The common row count of the per-row arrays (1 if every array is shared).
+  long long rows() const {
+    long long r = -1;
+    for (const auto& kv : arrays_) {
+      if (kv.second.shared) continue;
+      if (r >= 0 && kv.second.rows != r) throw ShapeMismatch(kv.first + ": row count disagrees with the batch");
+      r = kv.second.rows;
+    }
+    return r < 0 ? 1 : r;
+  }
+
+ private:
+  std::map<std::string, Array> arrays_;
+};
+
+namespace detail {
+
+// The batched fused loop: every row of `st` through one kernel launch
+// sequence (rf_run_host), one ExecReport per row with the reference's field
+// meanings. Single-row run_incremental / run_multisegment are R = 1.
+inline std::vector<ExecReport> execute_batched(const Program& prog, const TreeConfig& cfg, long long segments,
+                                               const BatchedStore& st, const std::string& strategy) {
+  // validate_tree (cascade.cpp:37-66) + store shapes (simulator.cpp:235-245)
+  if (cfg.levels.size() < 2 || cfg.levels.front() != prog.L0 || cfg.levels.back() != 1)
+    throw ShapeMismatch("BadTree: levels must run from L0 = " + std::to_string(prog.L0) + " to 1");
+  for (std::size_t k = 1; k < cfg.levels.size(); ++k)
+    if (cfg.levels[k] <= 0 || cfg.levels[k - 1] % cfg.levels[k] != 0)
+      throw ShapeMismatch("BadTree: level widths must divide");
+  for (const auto& in : prog.spec.inputs) {
+    const auto& a = st.array(in.name);
+    if (a.len != in.len || a.free_len != in.free_len)
+      throw ShapeMismatch(in.name + ": store shape does not match the spec");
+  }
   if (segments < 1 || prog.L0 % segments != 0)  // simulator.cpp:668-671
     throw IncompatibleSegmentation(std::to_string(segments) + " segments do not divide L0 = " +
                                    std::to_string(prog.L0));
-  ExecReport rep;
-  rep.strategy = strategy;
+  const long long R = st.rows();
+  std::vector<ExecReport> reps(R);
+  for (auto& r : reps) r.strategy = strategy;
+  if (R == 0) return reps;
   const long long L0 = prog.L0;
-  auto out = [&](int id, std::vector<double> v) {
+  auto out = [&](long long r, int id, std::vector<double> v) {
     OutputVal o;
     o.id = id;
     o.v = std::move(v);
-    rep.outputs.push_back(std::move(o));
+    reps[r].outputs.push_back(std::move(o));
+  };
+  // per-row operand r of input `name`, as float
+  auto rows_f = [&](const std::string& name, long long rows) {
+    const auto& a = st.array(name);
+    std::vector<float> f(rows * a.per_row());
+    for (long long r = 0; r < rows; ++r) {
+      const double* src = row_ptr(a.data, a.shared, a.per_row(), std::min(r, a.rows - 1));
+      std::copy(src, src + a.per_row(), f.begin() + r * a.per_row());
+    }
+    return f;
+  };
+  // the GEMM patterns share one static weight over the batch (it is packed
+  // once into the kernel's K-major tiles)
+  auto shared_weight = [&](const std::string& name) {
+    const auto& a = st.array(name);
+    if (!a.shared && a.rows != 1)
+      throw NotFusable(name + ": batched GEMM rows must share the weight (define_shared)");
+    return a.data.data();
   };
   switch (prog.pattern) {
-    case RF_PATTERN_SAFE_SOFTMAX: {
-      rf_desc d = base_desc(RF_PATTERN_SAFE_SOFTMAX, RF_F32);
-      d.rows = 1;
+    case RF_PATTERN_SAFE_SOFTMAX:
+    case RF_PATTERN_MOE_ROUTING: {
+      const bool moe = prog.pattern == RF_PATTERN_MOE_ROUTING;
+      const int K = moe ? static_cast<int>(prog.free_len) : 0;
+      rf_desc d = base_desc(prog.pattern, RF_F32);
+      d.rows = R;
       d.len = L0;
+      d.free_len = K;
       PlanHandle h(d);
-      const auto& x = st.array(prog.x).data;
-      std::vector<float> xf(x.begin(), x.end());
-      float m = 0, t = 0;
+      std::vector<float> xf = rows_f(prog.x, R), m(R), t(R);
+      std::vector<int32_t> rec(moe ? 2 * K * R : 0);
       rf_host_io io{};
       io.in[0] = xf.data();
-      io.d[0] = &m;
-      io.d[1] = &t;
+      io.d[0] = m.data();
+      io.d[1] = t.data();
+      io.d[2] = moe ? rec.data() : nullptr;
       check(rf_run_host(h.p, &io));
-      out(1, {m});
-      out(2, {t});
+      for (long long r = 0; r < R; ++r) {
+        out(r, 1, {m[r]});
+        out(r, 2, {t[r]});
+        if (!moe) continue;
+        OutputVal o;
+        o.id = 3;
+        for (int j = 0; j < K; ++j) {
+          const int32_t* e = &rec[2 * (r * K + j)];
+          if (e[1] == 0) break;  // fewer experts than K'
+          float v;
+          std::memcpy(&v, &e[0], 4);
+          o.topk.emplace_back(static_cast<double>(v), static_cast<long long>(e[1]));
+        }
+        reps[r].outputs.push_back(std::move(o));
+      }
       break;
     }
     case RF_PATTERN_ATTENTION: {
-      // One cascade row: P and V. The kernel consumes Q, K, V with P = Q K^T;
-      // q = e_0 and K[l] = (P[l], 0, ...) reproduce P exactly in fp32.
+      // Each row is one (b,h) unit with one query: P and V. The kernel
+      // consumes Q, K, V with P = Q K^T; q = e_0 and K[l] = (P[l], 0, ...)
+      // reproduce P exactly in fp32.
       const long long hd = prog.free_len;
       long long D = 16;
       while (D < hd) D *= 2;
       if (D > 128) throw NotFusable("attention head dim > 128");
       rf_desc d = base_desc(RF_PATTERN_ATTENTION, RF_F32);
+      d.heads = R;
       d.rows = 1;
       d.len = L0;
       d.free_len = D;
       d.segments = segments;
       PlanHandle h(d);
-      const auto& P = st.array(prog.x).data;
-      const auto& V = st.array(prog.v).data;
-      std::vector<float> q(D, 0.f), k(L0 * D, 0.f), v(L0 * D, 0.f), o(D);
-      q[0] = 1.f;
-      for (long long l = 0; l < L0; ++l) {
-        k[l * D] = static_cast<float>(P[l]);
-        for (long long f = 0; f < hd; ++f) v[l * D + f] = static_cast<float>(V[l * hd + f]);
+      const auto& P = st.array(prog.x);
+      const auto& V = st.array(prog.v);
+      std::vector<float> q(R * D, 0.f), k(R * L0 * D, 0.f), v(R * L0 * D, 0.f), o(R * D), m(R), t(R);
+      for (long long r = 0; r < R; ++r) {
+        q[r * D] = 1.f;
+        const double* pr = row_ptr(P.data, P.shared, P.per_row(), std::min(r, P.rows - 1));
+        const double* vr = row_ptr(V.data, V.shared, V.per_row(), std::min(r, V.rows - 1));
+        for (long long l = 0; l < L0; ++l) {
+          k[(r * L0 + l) * D] = static_cast<float>(pr[l]);
+          for (long long f = 0; f < hd; ++f) v[(r * L0 + l) * D + f] = static_cast<float>(vr[l * hd + f]);
+        }
       }
-      float m = 0, t = 0;
       rf_host_io io{};
       io.in[0] = q.data();
       io.in[1] = k.data();
       io.in[2] = v.data();
-      io.d[0] = &m;
-      io.d[1] = &t;
+      io.d[0] = m.data();
+      io.d[1] = t.data();
       io.d[2] = o.data();
       check(rf_run_host(h.p, &io));
-      out(1, {m});
-      out(2, {t});
-      out(3, std::vector<double>(o.begin(), o.begin() + hd));
-      break;
-    }
-    case RF_PATTERN_MOE_ROUTING: {
-      const int K = static_cast<int>(prog.free_len);
-      rf_desc d = base_desc(RF_PATTERN_MOE_ROUTING, RF_F32);
-      d.rows = 1;
-      d.len = L0;
-      d.free_len = K;
-      PlanHandle h(d);
-      const auto& x = st.array(prog.x).data;
-      std::vector<float> xf(x.begin(), x.end());
-      float m = 0, t = 0;
-      std::vector<int32_t> rec(2 * K);
-      rf_host_io io{};
-      io.in[0] = xf.data();
-      io.d[0] = &m;
-      io.d[1] = &t;
-      io.d[2] = rec.data();
-      check(rf_run_host(h.p, &io));
-      out(1, {m});
-      out(2, {t});
-      OutputVal o;
-      o.id = 3;
-      for (int j = 0; j < K; ++j) {
-        if (rec[2 * j + 1] == 0) break;  // fewer experts than K'
-        float v;
-        std::memcpy(&v, &rec[2 * j], 4);
-        o.topk.emplace_back(static_cast<double>(v), static_cast<long long>(rec[2 * j + 1]));
+      for (long long r = 0; r < R; ++r) {
+        out(r, 1, {m[r]});
+        out(r, 2, {t[r]});
+        out(r, 3, std::vector<double>(o.begin() + r * D, o.begin() + r * D + hd));
       }
-      rep.outputs.push_back(std::move(o));
       break;
     }
     case RF_PATTERN_QUANT_GEMM_E4M3:
-    case RF_PATTERN_RMSNORM_GEMM: {
+    case RF_PATTERN_RMSNORM_GEMM:
+    case RF_PATTERN_LAYERNORM_GEMM: {
       const bool quant = prog.pattern == RF_PATTERN_QUANT_GEMM_E4M3;
+      const bool ln = prog.pattern == RF_PATTERN_LAYERNORM_GEMM;
       // segments: S | L0 was checked above; the kernel's K loop is already a
       // tile-segmented Eq.16 fold, so S changes nothing but the divisibility.
-      // pad to the kernel tiles: M to 128 rows (copies of the row: never an
-      // all-zero padding row), K with zeros (neutral for max|a| and sum x^2,
-      // zero contributions), N with zero weight columns.
+      // Pad to the kernel tiles: M to whole row tiles (copies of row 0: never
+      // an all-zero padding row), K with zeros (neutral for max|a| and sum
+      // x^2, zero contributions) — LayerNorm excepted: zeros would shift the
+      // mean d1/K — and N with zero weight columns.
       // RMSNorm: the kernel normalises by the mean over its (padded) K,
       // 1/sqrt(d1/Kp + eps'). With r = L0/Kp, eps' = eps*r and g' = g*sqrt(r):
       //   g' / sqrt(d1/Kp + eps') = g sqrt(r) / (sqrt(r) sqrt(d1/L0 + eps))
       // which is the cascade's g / sqrt(d1/L0 + eps) exactly (d1 is unchanged).
+      if (ln && L0 % 64) throw NotFusable("layernorm_gemm: reduce length must be a multiple of 64");
       const long long N = prog.free_len;
       const long long Kp = round_up(L0, quant ? 128 : 64), Np = round_up(N, quant ? 512 : 256);
-      const long long M = 128;
-      const double r = static_cast<double>(L0) / static_cast<double>(Kp);
+      const long long M = round_up(R, ln ? 256 : 128);
+      const double ratio = static_cast<double>(L0) / static_cast<double>(Kp);
       rf_desc d = base_desc(prog.pattern, RF_BF16);
       d.rows = M;
       d.len = Kp;
       d.free_len = Np;
       d.fmax = prog.fmax;
-      d.eps = quant ? prog.eps : prog.eps * r;
+      d.eps = quant || ln ? prog.eps : prog.eps * ratio;
       PlanHandle h(d);
-      const auto& A = st.array(prog.x).data;
-      const auto& W = st.array(prog.w).data;
+      const double* W = shared_weight(prog.w);
       std::vector<float> wf(Kp * Np, 0.f), gf(Kp, 0.f);
       for (long long l = 0; l < L0; ++l)
         for (long long f = 0; f < N; ++f) wf[l * Np + f] = static_cast<float>(W[l * N + f]);
       if (!quant) {
-        const auto& g = st.array(prog.g).data;
-        const double gs = std::sqrt(r);
+        const double* g = shared_weight(prog.g);
+        const double gs = ln ? 1.0 : std::sqrt(ratio);
         for (long long l = 0; l < L0; ++l) gf[l] = static_cast<float>(g[l] * gs);
       }
       void* packed = nullptr;
       check(rf_pack_weight_host(h.p, wf.data(), quant ? nullptr : gf.data(), &packed));
+      const auto& A = st.array(prog.x);
       std::vector<uint16_t> a(M * Kp, 0);
-      for (long long r = 0; r < M; ++r)
-        for (long long l = 0; l < L0; ++l) a[r * Kp + l] = to_bf16(static_cast<float>(A[l]));
-      std::vector<float> d1(M);
-      std::vector<float> cf(quant ? M * Np : 0);
-      std::vector<uint16_t> cb(quant ? 0 : M * Np);
-      rf_host_io io{};
-      io.in[0] = a.data();
-      io.in[1] = packed;
-      io.d[0] = d1.data();
-      io.d[1] = quant ? static_cast<void*>(cf.data()) : static_cast<void*>(cb.data());
-      const rf_status s = rf_run_host(h.p, &io);
-      rf_buffer_free(packed);
-      check(s);
-      std::vector<double> c(N);
-      for (long long f = 0; f < N; ++f) c[f] = quant ? cf[f] : from_bf16(cb[f]);
-      out(1, {d1[0]});
-      out(2, c);
-      if (quant && !(d1[0] > 0.0f))  // finalize_root: 0/0 faults propagate
-        throw DomainError("division by zero");
-      break;
-    }
-    case RF_PATTERN_LAYERNORM_GEMM: {
-      // segments: S | L0 was checked above; the kernel's K loop is already a
-      // tile-segmented Eq.16 fold, so S changes nothing but the divisibility.
-      // pad: M to one 256-row pair tile (copies of the row), K with zeros —
-      // which would shift the mean, so K must already be a multiple of 64
-      // (padding changes d1/K and d2/K) — and N with zero weight columns.
-      const long long N = prog.free_len;
-      if (L0 % 64) throw NotFusable("layernorm_gemm: reduce length must be a multiple of 64");
-      const long long Np = round_up(N, 256), M = 256;
-      rf_desc d = base_desc(RF_PATTERN_LAYERNORM_GEMM, RF_BF16);
-      d.rows = M;
-      d.len = L0;
-      d.free_len = Np;
-      d.eps = prog.eps;
-      PlanHandle h(d);
-      const auto& A = st.array(prog.x).data;
-      const auto& W = st.array(prog.w).data;
-      const auto& g = st.array(prog.g).data;
-      std::vector<float> wf(L0 * Np, 0.f), gf(g.begin(), g.end());
-      for (long long l = 0; l < L0; ++l)
-        for (long long f = 0; f < N; ++f) wf[l * Np + f] = static_cast<float>(W[l * N + f]);
-      void* packed = nullptr;
-      check(rf_pack_weight_host(h.p, wf.data(), gf.data(), &packed));
-      std::vector<uint16_t> a(M * L0);
-      for (long long r = 0; r < M; ++r)
-        for (long long l = 0; l < L0; ++l) a[r * L0 + l] = to_bf16(static_cast<float>(A[l]));
-      std::vector<float> d1(M), d2(M);
-      std::vector<uint16_t> c3(M * Np), c4(M * Np);
-      rf_host_io io{};
-      io.in[0] = a.data();
-      io.in[1] = packed;
-      io.d[0] = d1.data();
-      io.d[1] = d2.data();
-      io.d[2] = c3.data();
-      io.d[3] = c4.data();
-      const rf_status s = rf_run_host(h.p, &io);
-      rf_buffer_free(packed);
-      check(s);
-      std::vector<double> y3(N), y4(N);
-      for (long long f = 0; f < N; ++f) {
-        y3[f] = from_bf16(c3[f]);
-        y4[f] = from_bf16(c4[f]);
+      for (long long r = 0; r < M; ++r) {
+        const double* ar = row_ptr(A.data, A.shared, A.per_row(), r < R ? std::min(r, A.rows - 1) : 0);
+        for (long long l = 0; l < L0; ++l) a[r * Kp + l] = to_bf16(static_cast<float>(ar[l]));
       }
-      out(1, {d1[0]});
-      out(2, {d2[0]});
-      out(3, y3);
-      out(4, y4);
+      std::vector<float> d1(M), d2(ln ? M : 0), cf(quant ? M * Np : 0);
+      std::vector<uint16_t> cb(quant ? 0 : M * Np), c4(ln ? M * Np : 0);
+      rf_host_io io{};
+      io.in[0] = a.data();
+      io.in[1] = packed;
+      io.d[0] = d1.data();
+      if (ln) {
+        io.d[1] = d2.data();
+        io.d[2] = cb.data();
+        io.d[3] = c4.data();
+      } else {
+        io.d[1] = quant ? static_cast<void*>(cf.data()) : static_cast<void*>(cb.data());
+      }
+      const rf_status s = rf_run_host(h.p, &io);
+      rf_buffer_free(packed);
+      check(s);
+      bool domain = false;
+      for (long long r = 0; r < R; ++r) {
+        std::vector<double> c(N), c4r(ln ? N : 0);
+        for (long long f = 0; f < N; ++f) {
+          c[f] = quant ? cf[r * Np + f] : from_bf16(cb[r * Np + f]);
+          if (ln) c4r[f] = from_bf16(c4[r * Np + f]);
+        }
+        out(r, 1, {d1[r]});
+        if (ln) out(r, 2, {d2[r]});
+        out(r, ln ? 3 : 2, c);
+        if (ln) out(r, 4, c4r);
+        if (quant && !(d1[r] > 0.0f)) domain = true;
+      }
+      if (domain)  // finalize_root: 0/0 faults propagate (a row's absmax is 0)
+        throw DomainError("division by zero");
       break;
     }
     case RF_PATTERN_VARIANCE:
@@ -1139,37 +1184,44 @@ inline ExecReport execute(const Program& prog, const TreeConfig& cfg, long long 
       const bool mom = prog.pattern == RF_PATTERN_MOMENTS;
       const long long F = mom ? prog.free_len : 1;
       rf_desc d = base_desc(prog.pattern, RF_F32);
-      d.rows = 1;
+      d.rows = R;
       d.len = L0;
       d.free_len = mom ? F : 0;
       d.segments = segments;
       d.eps = prog.eps;
       d.offset = prog.offset;
       PlanHandle h(d);
-      const auto& x = st.array(prog.x).data;
-      std::vector<float> xf(x.begin(), x.end()), yf;
-      if (prog.pattern != RF_PATTERN_VARIANCE) {
-        const auto& y = st.array(prog.v).data;
-        yf.assign(y.begin(), y.end());
-      }
-      float o1 = 0;
-      std::vector<float> o2(F), o3(F);
+      std::vector<float> xf = rows_f(prog.x, R), yf;
+      if (prog.pattern != RF_PATTERN_VARIANCE) yf = rows_f(prog.v, R);
+      std::vector<float> o1(R), o2(R * F), o3(mom ? R * F : 0);
       rf_host_io io{};
       io.in[0] = xf.data();
       io.in[1] = yf.empty() ? nullptr : yf.data();
-      io.d[0] = &o1;
+      io.d[0] = o1.data();
       io.d[1] = o2.data();
       io.d[2] = mom ? o3.data() : nullptr;
       check(rf_run_host(h.p, &io));
-      out(1, {o1});
-      out(2, std::vector<double>(o2.begin(), o2.end()));
-      if (mom) out(3, std::vector<double>(o3.begin(), o3.end()));
+      for (long long r = 0; r < R; ++r) {
+        out(r, 1, {o1[r]});
+        out(r, 2, std::vector<double>(o2.begin() + r * F, o2.begin() + (r + 1) * F));
+        if (mom) out(r, 3, std::vector<double>(o3.begin() + r * F, o3.begin() + (r + 1) * F));
+      }
       break;
     }
     default: throw NotFusable("unknown pattern");
   }
-  fill_counters(prog, cfg, rep);
-  return rep;
+  for (auto& r : reps) fill_counters(prog, cfg, r);
+  return reps;
+}
+
+inline ExecReport execute(const Program& prog, const TreeConfig& cfg, long long segments,
+                          TensorStore& st, const std::string& strategy) {
+  BatchedStore b;
+  for (const auto& in : prog.spec.inputs) {
+    const auto& a = st.array(in.name);  // ShapeMismatch if absent
+    b.define_rows(in.name, 1, a.len, a.free_len, a.data);
+  }
+  return execute_batched(prog, cfg, segments, b, strategy).front();
 }
 
 }  // namespace detail
@@ -1184,6 +1236,14 @@ inline ExecReport run_incremental(const Program& prog, const TreeConfig& cfg, Te
 inline ExecReport run_multisegment(const Program& prog, const TreeConfig& cfg, long long num_segments,
                                    TensorStore& store) {
   return detail::execute(prog, cfg, num_segments, store, "multi:" + std::to_string(num_segments));
+}
+
+// The batched executors: every row of the store in one run, one ExecReport
+// per row (the reference's executors take one TensorStore = one row).
+inline std::vector<ExecReport> run_batched(const Program& prog, const TreeConfig& cfg, const BatchedStore& store,
+                                           long long num_segments = 1) {
+  return detail::execute_batched(prog, cfg, num_segments, store,
+                                 num_segments == 1 ? "incremental" : "multi:" + std::to_string(num_segments));
 }
 
 }  // namespace rfcuda

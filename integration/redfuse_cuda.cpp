@@ -35,6 +35,16 @@ rfcuda::Program plan_checked(const FusedProgram& prog) {
   }
 }
 
+ExecReport to_reference(const rfcuda::ExecReport& r) {
+  ExecReport out;
+  out.strategy = "cuda:" + r.strategy;
+  for (const auto& o : r.outputs) out.outputs.push_back(OutputVal{o.id, o.v, o.topk});
+  out.input_loads = r.input_loads;
+  out.dep_root_loads = r.dep_root_loads;
+  out.peak_aux_slots = r.peak_aux_slots;
+  return out;
+}
+
 ExecReport run(const FusedProgram& prog, const TreeConfig& cfg, long long segments,
                TensorStore& store) {
   rfcuda::Program p = plan_checked(prog);
@@ -53,17 +63,57 @@ ExecReport run(const FusedProgram& prog, const TreeConfig& cfg, long long segmen
     throw IncompatibleSegmentation(e.what());
   } catch (const rfcuda::DomainError& e) {
     throw DomainError(e.what());
+  } catch (const rfcuda::NotFusable& e) {
+    throw NotFusable(0, e.what());
   }
-  ExecReport out;
-  out.strategy = "cuda:" + r.strategy;
-  for (const auto& o : r.outputs) out.outputs.push_back(OutputVal{o.id, o.v, o.topk});
-  out.input_loads = r.input_loads;
-  out.dep_root_loads = r.dep_root_loads;
-  out.peak_aux_slots = r.peak_aux_slots;
-  return out;
+  return to_reference(r);
 }
 
 }  // namespace
+
+std::vector<ExecReport> run_cuda_batched(const FusedProgram& prog, const TreeConfig& cfg,
+                                         std::vector<TensorStore>& stores, long long num_segments) {
+  rfcuda::Program p = plan_checked(prog);
+  std::vector<ExecReport> out;
+  if (stores.empty()) return out;
+  rfcuda::BatchedStore b;
+  const long long R = static_cast<long long>(stores.size());
+  for (const auto& in : prog.spec.inputs) {
+    const auto& a0 = stores[0].array(in.name);  // ShapeMismatch if absent
+    bool same = R > 1;
+    for (long long r = 1; r < R && same; ++r) {
+      const auto& ar = stores[r].array(in.name);
+      same = ar.len == a0.len && ar.free_len == a0.free_len && ar.data == a0.data;
+    }
+    if (same) {
+      b.define_shared(in.name, a0.len, a0.free_len, a0.data);
+      continue;
+    }
+    std::vector<double> rows;
+    rows.reserve(a0.data.size() * R);
+    for (long long r = 0; r < R; ++r) {
+      const auto& ar = stores[r].array(in.name);
+      if (ar.len != a0.len || ar.free_len != a0.free_len)
+        throw ShapeMismatch(in.name + ": batched rows disagree in shape");
+      rows.insert(rows.end(), ar.data.begin(), ar.data.end());
+    }
+    b.define_rows(in.name, R, a0.len, a0.free_len, std::move(rows));
+  }
+  std::vector<rfcuda::ExecReport> reps;
+  try {
+    reps = rfcuda::run_batched(p, rfcuda::TreeConfig{cfg.levels}, b, num_segments);
+  } catch (const rfcuda::ShapeMismatch& e) {
+    throw ShapeMismatch(e.what());
+  } catch (const rfcuda::IncompatibleSegmentation& e) {
+    throw IncompatibleSegmentation(e.what());
+  } catch (const rfcuda::DomainError& e) {
+    throw DomainError(e.what());
+  } catch (const rfcuda::NotFusable& e) {
+    throw NotFusable(0, e.what());
+  }
+  for (const auto& r : reps) out.push_back(to_reference(r));
+  return out;
+}
 
 CudaPattern cuda_pattern(const FusedProgram& prog) {
   rfcuda::Program p = plan_checked(prog);

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <string>
+#include <vector>
 
 #include "redfuse/acrf.hpp"
 #include "redfuse/simulator.hpp"
@@ -17,6 +18,15 @@ namespace redfuse {
 ExecReport run_cuda(const FusedProgram& prog, const TreeConfig& cfg, TensorStore& store);
 ExecReport run_cuda_multisegment(const FusedProgram& prog, const TreeConfig& cfg,
                                  long long num_segments, TensorStore& store);
+
+// Batched drop-in (the rows axis the reference only has as scalar_ir's
+// EmitStrategy.rows, scalar_ir.hpp:77): R cascade rows — one TensorStore
+// each, as run_incremental takes them — in ONE librf_cuda run, one
+// ExecReport per row. Inputs identical in every store (the static GEMM
+// weight, gamma) are passed once; the GEMM patterns require that.
+// num_segments > 1 is run_multisegment per row.
+std::vector<ExecReport> run_cuda_batched(const FusedProgram& prog, const TreeConfig& cfg,
+                                         std::vector<TensorStore>& stores, long long num_segments = 1);
 
 // The librf_cuda pattern a cascade maps onto ("attention", "safe_softmax",
 // "moe_routing", "quant_gemm_e4m3", "rmsnorm_gemm", "layernorm_gemm"), and

@@ -137,6 +137,45 @@ int main() {
     std::printf("{\"case\": \"prod_chain\", \"mode\": \"no-kernel\", \"not_fusable\": %s}\n",
                 threw ? "true" : "false");
   }
+  // the batched drop-in: R reference rows in one librf_cuda run, each row's
+  // report against the reference executor on that row's store
+  auto check_batched = [&](const std::string& name, const Workload& w, double tol, int rows,
+                           long long segs, bool share_static) {
+    FusedProgram prog = derive_fused(w.spec);
+    const long long l0 = w.spec.axis_len();
+    std::vector<TensorStore> stores, refs;
+    for (int r = 0; r < rows; ++r) {
+      TensorStore st = w.generate(200 + r);
+      if (share_static && r > 0)  // the GEMM weight (and gamma) are shared by the batch
+        for (const char* nm : {"w", "g"})
+          if (stores[0].has(nm)) {
+            const auto& a = stores[0].array(nm);
+            st.define(nm, a.len, a.free_len, a.data);
+          }
+      stores.push_back(st);
+      refs.push_back(st);
+    }
+    TreeConfig cfg{{l0, 1}};
+    std::vector<ExecReport> got = run_cuda_batched(prog, cfg, stores, segs);
+    for (int r = 0; r < rows; ++r) {
+      ExecReport want = segs == 1 ? run_incremental(prog, cfg, refs[r]) : run_multisegment(prog, cfg, segs, refs[r]);
+      report(name + "/row" + std::to_string(r), "batched:" + std::to_string(segs), want, got[r], tol);
+    }
+  };
+  check_batched("attention_256x64", make_attention(256, 64), 1e-5, 16, 1, false);
+  check_batched("attention_256x64", make_attention(256, 64), 1e-5, 8, 4, false);
+  check_batched("safe_softmax_1024", make_safe_softmax(1024), 1e-5, 32, 1, false);
+  check_batched("moe_routing_128x8", make_moe_routing(128, 8), 1e-5, 32, 1, false);
+  check_batched("quant_gemm_512x256", make_quant_gemm(512, 256), -0.06, 200, 1, true);
+  check_batched("variance_8192", builtin("variance"), 1e-5, 8, 2, false);
+  check_batched("sum_sum_1024", builtin("sum_sum"), 1e-5, 8, 1, false);
+  check_batched("rmsnorm_gemm_256x48",
+                dsl_workload("rmsnorm_gemm",
+                             "cascade rmsnorm_gemm\ninput x len 256\ninput g len 256\n"
+                             "input w len 256 free 48\nconst INVK = 0.00390625\nconst EPS = 1e-6\n"
+                             "reduce 1 op sum\n    x[l] * x[l]\nreduce 2 op sum free 48\n"
+                             "    x[l] * g[l] / sqrt(d1 * INVK + EPS) * w[l, f]\n"),
+                -0.02, 130, 1, true);
   // a FusedProgram whose derived correction is not the kernel's closed form
   // (here: attention's d3 correction with the exponent's sign flipped) is
   // rejected at plan time (rfcuda::check_corrections), never run

@@ -440,6 +440,71 @@ TEST(derived_corrections_are_the_kernels) {
   std::printf("  %d derived corrections pinned to the kernels' closed forms\n", pinned);
 }
 
+// run_batched: R rows in one run equal R single-row runs (same kernels; the
+// attention rows become (b,h) units of one launch).
+TEST(batched_rows_match_single_rows) {
+  {
+    const long long kv = 512, hd = 64, R = 12;
+    Program p = plan(attention_dsl(kv, hd));
+    BatchedStore b;
+    std::vector<double> P, V;
+    std::vector<TensorStore> singles(R);
+    for (long long r = 0; r < R; ++r) {
+      auto pr = random_vec(kv, 40 + r, -3, 3), vr = random_vec(kv * hd, 80 + r, -1, 1);
+      singles[r].define("P", kv, 0, pr);
+      singles[r].define("V", kv, hd, vr);
+      P.insert(P.end(), pr.begin(), pr.end());
+      V.insert(V.end(), vr.begin(), vr.end());
+    }
+    b.define_rows("P", R, kv, 0, P);
+    b.define_rows("V", R, kv, hd, V);
+    for (long long segs : {1LL, 4LL}) {
+      auto reps = run_batched(p, TreeConfig{{kv, 1}}, b, segs);
+      CHECK(static_cast<long long>(reps.size()) == R);
+      for (long long r = 0; r < R; ++r) {
+        ExecReport one = run_multisegment(p, TreeConfig{{kv, 1}}, segs, singles[r]);
+        CHECK(compare_reports(reps[r], one, 1e-6).pass);
+        CHECK(reps[r].input_loads == one.input_loads);
+      }
+    }
+  }
+  {
+    const long long k = 100, n = 40, R = 130;  // K padded, M spans two row tiles
+    Program p = plan(rms_dsl(k, n));
+    BatchedStore b;
+    std::vector<double> X;
+    const auto g = random_vec(k, 5, -1, 1), w = random_vec(k * n, 6, -1, 1);
+    for (long long r = 0; r < R; ++r) {
+      auto xr = random_vec(k, 300 + r, -1, 1);
+      X.insert(X.end(), xr.begin(), xr.end());
+    }
+    b.define_rows("x", R, k, 0, X);
+    b.define_shared("g", k, 0, g);
+    b.define_shared("w", k, n, w);
+    auto reps = run_batched(p, TreeConfig{{k, 1}}, b);
+    CHECK(static_cast<long long>(reps.size()) == R);
+    for (long long r : {0LL, 1LL, 127LL, 128LL, 129LL}) {
+      TensorStore one;
+      one.define("x", k, 0, std::vector<double>(X.begin() + r * k, X.begin() + (r + 1) * k));
+      one.define("g", k, 0, g);
+      one.define("w", k, n, w);
+      ExecReport single = run_incremental(p, TreeConfig{{k, 1}}, one);
+      // M = 256 runs the 2-SM tile, a single row the 1-SM one: the bf16 outputs
+      // may differ by a rounding step
+      CHECK(compare_reports(reps[r], single, 1e-2).pass);
+      CHECK(reps[r].outputs[0].v[0] == single.outputs[0].v[0]);
+    }
+    // a per-row weight cannot be packed once: NotFusable
+    BatchedStore bad;
+    bad.define_rows("x", 2, k, 0, std::vector<double>(X.begin(), X.begin() + 2 * k));
+    bad.define_shared("g", k, 0, g);
+    std::vector<double> w2(w);
+    w2.insert(w2.end(), w.begin(), w.end());
+    bad.define_rows("w", 2, k, n, w2);
+    CHECK_THROWS_AS(run_batched(p, TreeConfig{{k, 1}}, bad), NotFusable);
+  }
+}
+
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "cpu";
   {
@@ -465,6 +530,7 @@ int main(int argc, char** argv) {
     RUN(rmsnorm_gemm_matches_direct_loop);
     RUN(topk_reduction_ties_lowest_index);
     RUN(layernorm_gemm_matches_direct_loop);
+    RUN(batched_rows_match_single_rows);
   }
   std::printf("%d checks, %d failures\n", checks, failures);
   return failures ? 1 : 0;
