@@ -492,7 +492,7 @@ TEST(batched_rows_match_single_rows) {
       // M = 256 runs the 2-SM tile, a single row the 1-SM one: the bf16 outputs
       // may differ by a rounding step
       CHECK(compare_reports(reps[r], single, 1e-2).pass);
-      CHECK(reps[r].outputs[0].v[0] == single.outputs[0].v[0]);
+      CHECK(std::fabs(reps[r].outputs[0].v[0] - single.outputs[0].v[0]) <= 1e-5 * single.outputs[0].v[0]);
     }
     // a per-row weight cannot be packed once: NotFusable
     BatchedStore bad;
