@@ -26,6 +26,8 @@
 // Tiles: BM = 128 rows (tokens) x BN = 256 (N) per CTA, UMMA M=128 N=256.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "rf_internal.h"
 #include "sm100.cuh"
 
@@ -44,8 +46,22 @@ __device__ __forceinline__ float bf_hi(uint32_t u) { return __uint_as_float(u & 
 // M-tiles, so a panel of the static weight (gn x BN x K) stays L2-resident
 // while the activations stream, instead of re-reading the whole weight from
 // HBM once per M-tile (the output stream would evict it).
+// gn < 0: panels of -gn M-tiles instead, walking M fastest inside a panel and
+// then every N tile: each activation panel is read from HBM once while the
+// whole weight streams past it (L2-resident when it fits, evict-last).
 __device__ __forceinline__ void tile_of(int b, int mt_count, int nt_count, int gn, int& mt,
                                         int& nt) {
+  if (gn < 0) {
+    const int gm = -gn;
+    const int per_group = gm * nt_count;
+    const int g = b / per_group;
+    const int first_m = g * gm;
+    const int height = min(gm, mt_count - first_m);
+    const int w = b - g * per_group;
+    nt = w / height;
+    mt = first_m + w % height;
+    return;
+  }
   const int per_group = gn * mt_count;
   const int g = b / per_group;
   const int first_n = g * gn;
@@ -923,6 +939,13 @@ bool gemm_sm100_supports(int pattern, int64_t m, int64_t n, int64_t k) {
   return false;
 }
 
+// Rasterisation group (tile_of): default per kernel, RF_GEMM_GROUP overrides
+// (tuning experiments only).
+static int group_param(int dflt) {
+  static const char* env = std::getenv("RF_GEMM_GROUP");
+  return env ? std::atoi(env) : dflt;
+}
+
 static cudaError_t launch_rms_like(const GemmArgs& g, cudaStream_t st, bool ln) {
   if (!gemm_sm100_supports(ln ? RF_PATTERN_LAYERNORM_GEMM : RF_PATTERN_RMSNORM_GEMM, g.m, g.n, g.k))
     return cudaErrorNotSupported;
@@ -949,7 +972,7 @@ static cudaError_t launch_rms_like(const GemmArgs& g, cudaStream_t st, bool ln) 
   }
   if (pair) {  // 2-SM path
     rms::Params p{g.d1, g.k, 1.f / static_cast<float>(g.k), g.eps, static_cast<int>(g.m / (2 * BM)),
-                  static_cast<int>(g.n / BN), 8, g.d2, g.colsum, g.c4 != nullptr};
+                  static_cast<int>(g.n / BN), group_param(8), g.d2, g.colsum, g.c4 != nullptr};
     const size_t smem = sizeof(rms2::Smem) + 1024;
     auto kern = ln ? rms2::rms_gemm_2sm_kernel<true> : rms2::rms_gemm_2sm_kernel<false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1002,7 +1025,7 @@ cudaError_t launch_quant_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
   }
   if (g.m % (2 * BM) == 0) {  // 2-SM path
     qnt::Params p{g.d1, g.domain_flag, g.k, g.fmax, static_cast<int>(g.m / (2 * BM)),
-                  static_cast<int>(g.n / qnt::BNQ), 4};
+                  static_cast<int>(g.n / qnt::BNQ), group_param(4)};
     const size_t smem = sizeof(qnt2::Smem) + 1024;
     cudaError_t e = cudaFuncSetAttribute(qnt2::quant_gemm_2sm_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
