@@ -1106,8 +1106,6 @@ inline std::vector<ExecReport> execute_batched(const Program& prog, const TreeCo
     case RF_PATTERN_LAYERNORM_GEMM: {
       const bool quant = prog.pattern == RF_PATTERN_QUANT_GEMM_E4M3;
       const bool ln = prog.pattern == RF_PATTERN_LAYERNORM_GEMM;
-      // segments: S | L0 was checked above; the kernel's K loop is already a
-      // tile-segmented Eq.16 fold, so S changes nothing but the divisibility.
       // Pad to the kernel tiles: M to whole row tiles (copies of row 0: never
       // an all-zero padding row), K with zeros (neutral for max|a| and sum
       // x^2, zero contributions) — LayerNorm excepted: zeros would shift the
@@ -1125,6 +1123,11 @@ inline std::vector<ExecReport> execute_batched(const Program& prog, const TreeCo
       d.rows = M;
       d.len = Kp;
       d.free_len = Np;
+      // run_multisegment: the kernels split K into S slices (split-K partials
+      // + slice-ordered fold, gemm_fold.cu) when the reference's slices of
+      // L0 / S are whole K tiles; otherwise one segment (equal in exact
+      // arithmetic; the S | L0 contract was checked above)
+      d.segments = L0 % (segments * (quant ? 128 : 64)) == 0 ? segments : 1;
       d.fmax = prog.fmax;
       d.eps = quant || ln ? prog.eps : prog.eps * ratio;
       PlanHandle h(d);

@@ -287,7 +287,10 @@ static void quant_e4m3_row(void* vctx, int64_t row) {
       for (int64_t f = 0; f < q->N; ++f) cr[f] *= corr;
     }
     ref = nref;
-    float scale = (float)q->fmax / ref; /* exact: fmax * 2^-e */
+    /* exact: fmax * 2^-e; while the running absmax is 0 every element so far is
+     * 0 and the guarded H' is the identity (the reference's repair): the tile
+     * contributes 0 (a scale of fmax / 0 would turn 0 * inf into NaN) */
+    float scale = ref > 0.0f ? (float)q->fmax / ref : 0.0f;
     for (int64_t l = l0; l < l1; ++l) {
       double qv = (double)rfo_round_e4m3((float)ar[l] * scale);
       const double* wr = q->w + l * q->N;

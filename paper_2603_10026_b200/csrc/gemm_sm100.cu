@@ -102,7 +102,47 @@ struct Params {
   float* d2;            // layernorm: sum x^2 (d1 then holds sum x)
   const float* colsum;  // layernorm: column sums of the packed g*w
   int write_d4;         // layernorm: d4 requested
+  // Multi-Segment (run_multisegment, simulator.cpp:660-687) as split-K: CTA
+  // (tile, blockIdx.y = s) streams K slice s of k_slice elements from fresh
+  // state and writes its raw partial state — the fp32 accumulator (H' = 1)
+  // through `ty` (an fp32 map over [S * ws_rows, N]) and the slice's
+  // statistics to ws_d1 / ws_d2 [S, ws_rows]; gemm_fold.cu folds the slices
+  // in order. partial = 0: the single-segment loop (k_slice = k).
+  int64_t k_slice;
+  float* ws_d1;
+  float* ws_d2;
+  int64_t ws_rows;
+  int partial;
 };
+
+// The raw fp32 accumulator of this warpgroup's 128 TMEM lanes (row r) x NCOLS
+// columns -> smem staging, RND chunks of 32 columns (16 KB each) per round ->
+// TMA store at (n0, row0). Called by the 128 statistics/epilogue threads.
+template <int NCOLS, int RND>
+__device__ __forceinline__ void store_acc_f32(uint32_t tmem_row, int r, uint8_t* stage_ptr,
+                                              const CUtensorMap* tm, int n0, int row0) {
+  const uint32_t stage = smem_u32(stage_ptr);
+#pragma unroll 1
+  for (int c0 = 0; c0 < NCOLS / 32; c0 += RND) {
+#pragma unroll 1
+    for (int c = 0; c < RND; ++c) {
+      uint32_t v[32];
+      tmem_ld32(tmem_row + (c0 + c) * 32, v);
+      tmem_ld_wait();
+      const uint32_t chunk = stage + c * (BM * 128);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sts128(chunk + sw128(r, u), make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]));
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (threadIdx.x == 0) {
+      for (int c = 0; c < RND; ++c) tma_store_2d(tm, stage_ptr + c * (BM * 128), n0 + (c0 + c) * 32, row0);
+      bulk_commit();
+      bulk_wait_read0();
+    }
+    named_bar_sync(1, 128);
+  }
+}
 
 __global__ void __launch_bounds__(NT, 1)
     rms_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
@@ -114,7 +154,8 @@ __global__ void __launch_bounds__(NT, 1)
   tile_of(blockIdx.x, p.mt_count, p.nt_count, p.group_n, mt, nt);
   const int n0 = nt * BN;
   const int m0 = mt * BM;
-  const int kt = static_cast<int>(p.k / BK);
+  const int kt = static_cast<int>(p.k_slice / BK);
+  const int k0 = static_cast<int>(blockIdx.y * p.k_slice);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -139,8 +180,8 @@ __global__ void __launch_bounds__(NT, 1)
         const int st = t % STAGES;
         mbar_wait(&s.empty[st], ((t / STAGES) & 1) ^ 1);
         mbar_arrive_expect_tx(&s.full[st], A_BYTES + B_BYTES);
-        tma_load_2d(s.a[st], &ta, &s.full[st], t * BK, m0, kEvictNormal);
-        tma_load_2d(s.b[st], &tb, &s.full[st], t * BK, n0, kEvictLast);
+        tma_load_2d(s.a[st], &ta, &s.full[st], k0 + t * BK, m0, kEvictNormal);
+        tma_load_2d(s.b[st], &tb, &s.full[st], k0 + t * BK, n0, kEvictLast);
       }
     }
   } else if (warp == 5) {
@@ -189,12 +230,16 @@ __global__ void __launch_bounds__(NT, 1)
     }
     // ---- finalize: d2 = acc * 1/sqrt(d1/K + eps) -> bf16 -> smem -> TMA store ----
     const float inv = rsqrtf(fmaf(ss, p.inv_k, p.eps));
-    if (nt == 0) p.d1[m0 + r] = ss;
     named_bar_sync(1, 128);  // every stats warp is done reading the stages
     mbar_wait(&s.acc_full, 0);
     tc_fence_after();
     const uint32_t stage = smem_u32(s.a[0]);  // all stages are drained: reuse 64 KB as the Y tile
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    if (p.partial) {  // slice partial state: raw accumulator + sum x^2 of the slice
+      if (nt == 0) p.ws_d1[blockIdx.y * p.ws_rows + m0 + r] = ss;
+      store_acc_f32<BN, 8>(tmem + lane_off, r, s.a[0], &ty, n0, static_cast<int>(blockIdx.y * p.ws_rows) + m0);
+    } else {
+    if (nt == 0) p.d1[m0 + r] = ss;
 #pragma unroll
     for (int c = 0; c < BN / 32; ++c) {
       uint32_t v[32];
@@ -217,8 +262,9 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
       for (int c = 0; c < BN / 64; ++c) tma_store_2d(&ty, s.a[0] + c * (BM * 128), n0 + 64 * c, m0);
       bulk_commit();
-      bulk_wait0();
     }
+    }
+    if (threadIdx.x == 0) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();
@@ -269,7 +315,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 2)
   tile_of(blockIdx.x >> 1, p.mt_count, p.nt_count, p.group_n, mt, nt);
   const int n0 = nt * BN;
   const int m0 = mt * 2 * BM + static_cast<int>(rank) * BM;  // this CTA's 128 rows
-  const int kt = static_cast<int>(p.k / BK);
+  const int kt = static_cast<int>(p.k_slice / BK);
+  const int k0 = static_cast<int>(blockIdx.y * p.k_slice);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -295,8 +342,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 2)
         const int st = t % STAGES;
         mbar_wait(&s.empty[st], ((t / STAGES) & 1) ^ 1);
         mbar_arrive_expect_tx(&s.full[st], A_BYTES + B_BYTES);
-        tma_load_2d(s.a[st], &ta, &s.full[st], t * BK, m0, kEvictNormal);
-        tma_load_2d(s.b[st], &tb, &s.full[st], t * BK, n0 + static_cast<int>(rank) * 128, kEvictLast);
+        tma_load_2d(s.a[st], &ta, &s.full[st], k0 + t * BK, m0, kEvictNormal);
+        tma_load_2d(s.b[st], &tb, &s.full[st], k0 + t * BK, n0 + static_cast<int>(rank) * 128, kEvictLast);
       }
     }
   } else if (warp == 5) {
@@ -352,7 +399,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 2)
       if ((threadIdx.x & 31) == 0) mbar_arrive(&s.empty[st]);
     }
     float inv, mean = 0.f;
-    if (LN) {
+    if (p.partial) {  // slice partial state: statistics of the slice only
+      if (nt == 0) {
+        p.ws_d1[blockIdx.y * p.ws_rows + m0 + r] = LN ? sx : ss;
+        if (LN) p.ws_d2[blockIdx.y * p.ws_rows + m0 + r] = ss;
+      }
+      inv = 0.f;
+    } else if (LN) {
       mean = sx * p.inv_k;
       inv = rsqrtf(fmaf(ss, p.inv_k, -mean * mean) + p.eps);  // 1/sigma
       if (nt == 0) {
@@ -368,6 +421,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 2)
     tc_fence_after();
     const uint32_t stage = smem_u32(s.a[0]);  // drained: 64 KB of A stages for the Y tile
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    if (p.partial) {
+      // raw accumulator (H' = 1) of the slice: 4 x 16 KB staged per round (the
+      // drained A stages hold 48 KB with 3 stages)
+      rms::store_acc_f32<BN, 2>(tmem + lane_off, r, s.a[0], &ty, n0, static_cast<int>(blockIdx.y * p.ws_rows) + m0);
+    } else {
 #pragma unroll
     for (int c = 0; c < BN / 32; ++c) {
       uint32_t v[32];
@@ -420,6 +478,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 2)
         bulk_commit();
       }
     }
+    }
     if (threadIdx.x == 0) bulk_wait0();
   }
   tc_fence_before();
@@ -457,6 +516,14 @@ struct Params {
   int64_t k;
   float fmax;
   int mt_count, nt_count, group_n;
+  // Multi-Segment split-K (see rms::Params): slice s = blockIdx.y from fresh
+  // state; partial = 1 writes acc * ref_s (the slice's accumulator in units of
+  // fmax * a / 1, i.e. H' retargeted to 1) through `tc` over [S * ws_rows, N]
+  // and the slice's absmax to ws_d1; gemm_fold.cu finishes c = sum / d1.
+  int64_t k_slice;
+  float* ws_d1;
+  int64_t ws_rows;
+  int partial;
 };
 
 __device__ __forceinline__ float pow2_ceil(float x) {
@@ -491,7 +558,8 @@ __global__ void __launch_bounds__(NT, 1)
   tile_of(blockIdx.x, p.mt_count, p.nt_count, p.group_n, mt, nt);
   const int n0 = nt * BNQ;
   const int m0 = mt * BM;
-  const int kt = static_cast<int>(p.k / BK);
+  const int kt = static_cast<int>(p.k_slice / BK);
+  const int k0 = static_cast<int>(blockIdx.y * p.k_slice);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < SA; ++i) {
@@ -524,12 +592,12 @@ __global__ void __launch_bounds__(NT, 1)
         const int sa = t % SA, sw = t % SW;
         mbar_wait(&s.abf_empty[sa], ((t / SA) & 1) ^ 1);
         mbar_arrive_expect_tx(&s.abf_full[sa], ABF_BYTES);
-        tma_load_2d(s.abf[sa], &ta, &s.abf_full[sa], t * BK, m0, kEvictFirst);
-        tma_load_2d(s.abf[sa] + BM * 128, &ta, &s.abf_full[sa], t * BK + 64, m0, kEvictFirst);
+        tma_load_2d(s.abf[sa], &ta, &s.abf_full[sa], k0 + t * BK, m0, kEvictFirst);
+        tma_load_2d(s.abf[sa] + BM * 128, &ta, &s.abf_full[sa], k0 + t * BK + 64, m0, kEvictFirst);
         mbar_wait(&s.w_empty[sw], ((t / SW) & 1) ^ 1);
         mbar_arrive_expect_tx(&s.w_full[sw], W_BYTES);
-        tma_load_2d(s.w[sw], &tw, &s.w_full[sw], t * BK, n0, kEvictLast);
-        tma_load_2d(s.w[sw] + 256 * 128, &tw, &s.w_full[sw], t * BK, n0 + 256, kEvictLast);
+        tma_load_2d(s.w[sw], &tw, &s.w_full[sw], k0 + t * BK, n0, kEvictLast);
+        tma_load_2d(s.w[sw] + 256 * 128, &tw, &s.w_full[sw], k0 + t * BK, n0 + 256, kEvictLast);
       }
     }
   } else if (warp == 5) {
@@ -602,7 +670,11 @@ __global__ void __launch_bounds__(NT, 1)
         tc_fence_before();
       }
       ref = nref;
-      const float sc = p.fmax / ref;  // exact: fmax * 2^-e
+      // exact: fmax * 2^-e. While the running absmax is still 0 every element
+      // seen is 0: H is not invertible and the guarded H' is the identity
+      // (the reference's repair), so the tile contributes 0 — a scale of 0,
+      // not fmax / 0 (0 * inf would poison the accumulator with NaN).
+      const float sc = ref > 0.f ? p.fmax / ref : 0.f;
       uint64_t sc2;
       asm("mov.b64 %0, {%1, %1};" : "=l"(sc2) : "f"(sc));
       mbar_wait(&s.a8_empty[s8], ((t / S8) & 1) ^ 1);
@@ -623,9 +695,15 @@ __global__ void __launch_bounds__(NT, 1)
       if ((threadIdx.x & 31) == 0) mbar_arrive(&s.a8_full[s8]);
     }
     // ---- finalize_root: retarget H'(ref) -> H(d1): c = acc * ref / d1 ----
-    const float fin = ref / amax;  // 0/0 -> NaN for an all-zero row (DomainError)
-    if (!(amax > 0.f)) atomicExch(p.domain_flag, 1);
-    if (nt == 0) p.d1[m0 + r] = amax;
+    // (partial: the slice's state, retargeted to H' = 1: acc * ref)
+    const float fin = p.partial ? ref : ref / amax;  // 0/0 -> NaN for an all-zero row (DomainError)
+    if (p.partial) {
+      if (nt == 0) p.ws_d1[blockIdx.y * p.ws_rows + m0 + r] = amax;
+    } else {
+      if (!(amax > 0.f)) atomicExch(p.domain_flag, 1);
+      if (nt == 0) p.d1[m0 + r] = amax;
+    }
+    const int crow = p.partial ? static_cast<int>(blockIdx.y * p.ws_rows) + m0 : m0;
     named_bar_sync(1, 128);
     mbar_wait(&s.acc_full, 0);
     tc_fence_after();
@@ -651,7 +729,7 @@ __global__ void __launch_bounds__(NT, 1)
       if (threadIdx.x == 0) {
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-          tma_store_2d(&tc, s.abf[0] + c * (BM * 128), n0 + h * 256 + 32 * c, m0);
+          tma_store_2d(&tc, s.abf[0] + c * (BM * 128), n0 + h * 256 + 32 * c, crow);
         bulk_commit();
         bulk_wait_read0();
       }
@@ -707,7 +785,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   tile_of(blockIdx.x >> 1, p.mt_count, p.nt_count, p.group_n, mt, nt);
   const int n0 = nt * BNQ;
   const int m0 = mt * 2 * BM + static_cast<int>(rank) * BM;
-  const int kt = static_cast<int>(p.k / BK);
+  const int kt = static_cast<int>(p.k_slice / BK);
+  const int k0 = static_cast<int>(blockIdx.y * p.k_slice);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < SA; ++i) {
@@ -740,12 +819,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
         const int sa = t % SA, sw = t % SW;
         mbar_wait(&s.abf_empty[sa], ((t / SA) & 1) ^ 1);
         mbar_arrive_expect_tx(&s.abf_full[sa], ABF_BYTES);
-        tma_load_2d(s.abf[sa], &ta, &s.abf_full[sa], t * BK, m0, kEvictFirst);
-        tma_load_2d(s.abf[sa] + BM * 128, &ta, &s.abf_full[sa], t * BK + 64, m0, kEvictFirst);
+        tma_load_2d(s.abf[sa], &ta, &s.abf_full[sa], k0 + t * BK, m0, kEvictFirst);
+        tma_load_2d(s.abf[sa] + BM * 128, &ta, &s.abf_full[sa], k0 + t * BK + 64, m0, kEvictFirst);
         mbar_wait(&s.w_empty[sw], ((t / SW) & 1) ^ 1);
         mbar_arrive_expect_tx(&s.w_full[sw], W_BYTES);
         for (int h = 0; h < 2; ++h)
-          tma_load_2d(s.w[sw] + h * 128 * 128, &tw, &s.w_full[sw], t * BK,
+          tma_load_2d(s.w[sw] + h * 128 * 128, &tw, &s.w_full[sw], k0 + t * BK,
                       n0 + 256 * h + 128 * static_cast<int>(rank), kEvictLast);
       }
     }
@@ -835,7 +914,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
         tc_fence_before();
       }
       ref = nref;
-      const float sc = p.fmax / ref;
+      const float sc = ref > 0.f ? p.fmax / ref : 0.f;  // see quant_gemm_kernel
       uint64_t sc2;
       asm("mov.b64 %0, {%1, %1};" : "=l"(sc2) : "f"(sc));
       mbar_wait(&s.a8_empty[s8], ((t / S8) & 1) ^ 1);
@@ -855,9 +934,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(&s.a8_full[s8]);
     }
-    const float fin = ref / amax;
-    if (!(amax > 0.f)) atomicExch(p.domain_flag, 1);
-    if (nt == 0) p.d1[m0 + r] = amax;
+    const float fin = p.partial ? ref : ref / amax;
+    if (p.partial) {
+      if (nt == 0) p.ws_d1[blockIdx.y * p.ws_rows + m0 + r] = amax;
+    } else {
+      if (!(amax > 0.f)) atomicExch(p.domain_flag, 1);
+      if (nt == 0) p.d1[m0 + r] = amax;
+    }
+    const int crow = p.partial ? static_cast<int>(blockIdx.y * p.ws_rows) + m0 : m0;
     named_bar_sync(1, 128);
     mbar_wait(&s.acc_full, 0);
     tc_fence_after();
@@ -883,7 +967,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       if (threadIdx.x == 0) {
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-          tma_store_2d(&tc, s.abf[0] + c * (BM * 128), n0 + h * 256 + 32 * c, m0);
+          tma_store_2d(&tc, s.abf[0] + c * (BM * 128), n0 + h * 256 + 32 * c, crow);
         bulk_commit();
         bulk_wait_read0();
       }
@@ -963,6 +1047,9 @@ static cudaError_t launch_rms_like(const GemmArgs& g, cudaStream_t st, bool ln) 
     const uint32_t box[2] = {rms::BK, pair ? 128u : static_cast<uint32_t>(BN)};
     if (!make_tmap(&tb, g.b, 2, dims, str, box, 2)) return cudaErrorInvalidValue;
   }
+  const int64_t S = g.segments > 1 ? g.segments : 1;
+  const int64_t k_slice = g.k / S;
+  if (g.k % S || k_slice % rms::BK) return cudaErrorNotSupported;
   {
     const uint64_t dims[2] = {static_cast<uint64_t>(g.n), static_cast<uint64_t>(g.m)};
     const uint64_t str[1] = {static_cast<uint64_t>(g.n) * 2};
@@ -970,28 +1057,38 @@ static cudaError_t launch_rms_like(const GemmArgs& g, cudaStream_t st, bool ln) 
     if (!make_tmap(&ty, g.c, 2, dims, str, box, 2)) return cudaErrorInvalidValue;
     if (!make_tmap(&ty4, ln && g.c4 ? g.c4 : g.c, 2, dims, str, box, 2)) return cudaErrorInvalidValue;
   }
+  if (S > 1) {  // slice partials: the raw fp32 accumulators into the workspace
+    const uint64_t dims[2] = {static_cast<uint64_t>(g.n), static_cast<uint64_t>((S - 1) * g.ws_rows + g.m)};
+    const uint64_t str[1] = {static_cast<uint64_t>(g.n) * 4};
+    const uint32_t box[2] = {32, BM};
+    if (!make_tmap(&ty, g.ws, 2, dims, str, box, 4)) return cudaErrorInvalidValue;
+  }
+  cudaError_t e;
   if (pair) {  // 2-SM path
     rms::Params p{g.d1, g.k, 1.f / static_cast<float>(g.k), g.eps, static_cast<int>(g.m / (2 * BM)),
-                  static_cast<int>(g.n / BN), group_param(8), g.d2, g.colsum, g.c4 != nullptr};
+                  static_cast<int>(g.n / BN), group_param(8), g.d2, g.colsum, g.c4 != nullptr,
+                  k_slice, g.ws_d1, g.ws_d2, g.ws_rows, S > 1};
     const size_t smem = sizeof(rms2::Smem) + 1024;
     auto kern = ln ? rms2::rms_gemm_2sm_kernel<true> : rms2::rms_gemm_2sm_kernel<false>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    dim3 grid(static_cast<unsigned>(2 * (g.n / BN) * (g.m / (2 * BM))));
+    dim3 grid(static_cast<unsigned>(2 * (g.n / BN) * (g.m / (2 * BM))), static_cast<unsigned>(S));
     kern<<<grid, rms2::NT, smem, st>>>(ta, tb, ty, ty4, p);
-    return cudaGetLastError();
+  } else {
+    if (ln) return cudaErrorNotSupported;  // layernorm: 2-SM tiles only (M % 256)
+    rms::Params p{g.d1, g.k, 1.f / static_cast<float>(g.k), g.eps, static_cast<int>(g.m / BM),
+                  static_cast<int>(g.n / BN), group_param(8), nullptr, nullptr, 0,
+                  k_slice, g.ws_d1, nullptr, g.ws_rows, S > 1};
+    const size_t smem = sizeof(rms::Smem) + 1024;
+    e = cudaFuncSetAttribute(rms::rms_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    dim3 grid(static_cast<unsigned>((g.n / BN) * (g.m / BM)), static_cast<unsigned>(S));
+    rms::rms_gemm_kernel<<<grid, rms::NT, smem, st>>>(ta, tb, ty, p);
   }
-  if (ln) return cudaErrorNotSupported;  // layernorm: 2-SM tiles only (M % 256)
-  rms::Params p{g.d1, g.k, 1.f / static_cast<float>(g.k), g.eps, static_cast<int>(g.m / BM),
-                static_cast<int>(g.n / BN), 8, nullptr, nullptr, 0};
-  const size_t smem = sizeof(rms::Smem) + 1024;
-  cudaError_t e = cudaFuncSetAttribute(rms::rms_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  dim3 grid(static_cast<unsigned>((g.n / BN) * (g.m / BM)));
-  rms::rms_gemm_kernel<<<grid, rms::NT, smem, st>>>(ta, tb, ty, p);
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (e != cudaSuccess || S == 1) return e;
+  return launch_gemm_fold(ln ? RF_PATTERN_LAYERNORM_GEMM : RF_PATTERN_RMSNORM_GEMM, g, st);
 }
 
 cudaError_t launch_rms_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
@@ -1017,34 +1114,40 @@ cudaError_t launch_quant_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
     const uint32_t box[2] = {qnt::BK, g.m % (2 * BM) == 0 ? 128u : 256u};
     if (!make_tmap(&tw, g.b, 2, dims, str, box, 1)) return cudaErrorInvalidValue;
   }
+  const int64_t S = g.segments > 1 ? g.segments : 1;
+  const int64_t k_slice = g.k / S;
+  if (g.k % S || k_slice % qnt::BK) return cudaErrorNotSupported;
   {
-    const uint64_t dims[2] = {static_cast<uint64_t>(g.n), static_cast<uint64_t>(g.m)};
+    const uint64_t rows = S > 1 ? static_cast<uint64_t>((S - 1) * g.ws_rows + g.m) : static_cast<uint64_t>(g.m);
+    const uint64_t dims[2] = {static_cast<uint64_t>(g.n), rows};
     const uint64_t str[1] = {static_cast<uint64_t>(g.n) * 4};
     const uint32_t box[2] = {32, BM};
-    if (!make_tmap(&tc, g.c, 2, dims, str, box, 4)) return cudaErrorInvalidValue;
+    if (!make_tmap(&tc, S > 1 ? static_cast<void*>(g.ws) : g.c, 2, dims, str, box, 4))
+      return cudaErrorInvalidValue;
   }
+  cudaError_t e;
   if (g.m % (2 * BM) == 0) {  // 2-SM path
     qnt::Params p{g.d1, g.domain_flag, g.k, g.fmax, static_cast<int>(g.m / (2 * BM)),
-                  static_cast<int>(g.n / qnt::BNQ), group_param(4)};
+                  static_cast<int>(g.n / qnt::BNQ), group_param(4), k_slice, g.ws_d1, g.ws_rows, S > 1};
     const size_t smem = sizeof(qnt2::Smem) + 1024;
-    cudaError_t e = cudaFuncSetAttribute(qnt2::quant_gemm_2sm_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    e = cudaFuncSetAttribute(qnt2::quant_gemm_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    dim3 grid(static_cast<unsigned>(2 * (g.n / qnt::BNQ) * (g.m / (2 * BM))));
+    dim3 grid(static_cast<unsigned>(2 * (g.n / qnt::BNQ) * (g.m / (2 * BM))), static_cast<unsigned>(S));
     qnt2::quant_gemm_2sm_kernel<<<grid, qnt2::NT, smem, st>>>(ta, tw, tc, p);
-    return cudaGetLastError();
+  } else {
+    qnt::Params p{g.d1, g.domain_flag, g.k, g.fmax, static_cast<int>(g.m / BM),
+                  static_cast<int>(g.n / qnt::BNQ), 4, k_slice, g.ws_d1, g.ws_rows, S > 1};
+    const size_t smem = sizeof(qnt::Smem) + 1024;
+    e = cudaFuncSetAttribute(qnt::quant_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    dim3 grid(static_cast<unsigned>((g.n / qnt::BNQ) * (g.m / BM)), static_cast<unsigned>(S));
+    qnt::quant_gemm_kernel<<<grid, qnt::NT, smem, st>>>(ta, tw, tc, p);
   }
-  qnt::Params p{g.d1, g.domain_flag, g.k, g.fmax, static_cast<int>(g.m / BM),
-                static_cast<int>(g.n / qnt::BNQ), 4};
-  const size_t smem = sizeof(qnt::Smem) + 1024;
-  cudaError_t e = cudaFuncSetAttribute(qnt::quant_gemm_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  dim3 grid(static_cast<unsigned>((g.n / qnt::BNQ) * (g.m / BM)));
-  qnt::quant_gemm_kernel<<<grid, qnt::NT, smem, st>>>(ta, tw, tc, p);
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (e != cudaSuccess || S == 1) return e;
+  return launch_gemm_fold(RF_PATTERN_QUANT_GEMM_E4M3, g, st);
 }
 
 cudaError_t launch_pack_e4m3(const float* w, int64_t k, int64_t n, uint8_t* packed, cudaStream_t st) {

@@ -253,6 +253,13 @@ rf_status gemm_run(const rf_plan* p, const rf_io* io, int64_t m0, int64_t nm, cu
   g.k = d.len;
   g.fmax = static_cast<float>(d.fmax);
   g.eps = static_cast<float>(d.eps);
+  g.segments = d.segments;
+  g.ws_rows = d.rows;
+  if (d.segments > 1) {  // run_multisegment: slice partials + ordered fold (gemm_fold.cu)
+    g.ws = p->ws_o + m0 * d.free_len;
+    g.ws_d1 = p->ws_m + m0;
+    g.ws_d2 = p->ws_l ? p->ws_l + m0 : nullptr;
+  }
   cudaError_t e = d.pattern == RF_PATTERN_QUANT_GEMM_E4M3 ? rf::launch_quant_gemm_sm100(g, st)
                   : d.pattern == RF_PATTERN_LAYERNORM_GEMM  ? rf::launch_layernorm_gemm_sm100(g, st)
                                                             : rf::launch_rms_gemm_sm100(g, st);
@@ -447,12 +454,16 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
     case RF_PATTERN_RMSNORM_GEMM:
     case RF_PATTERN_LAYERNORM_GEMM:
       if (d.dtype != RF_BF16) return bail(RF_ERR_UNSUPPORTED, "GEMM patterns take bf16 activations");
-      // segments > 1 (run_multisegment): S | K was checked above; the K-tile loop
-      // is itself a segmented Eq.16 fold, so the kernel is the same.
+      // segments > 1 (run_multisegment): S | K was checked above; the kernels
+      // stream the S K-slices from fresh state (split-K partials) and
+      // gemm_fold.cu merges them in slice order.
       if (!rf::gemm_sm100_supports(d.pattern, d.rows, d.free_len, d.len))
         return bail(RF_ERR_UNSUPPORTED,
                     "GEMM shape has no tcgen05 tiling (quant: M%128, N%512, K%128; rms: M%128, "
                     "N%256, K%64; layernorm: M%256, N%256, K%64)");
+      if (d.segments > 1 && (d.len / d.segments) % (d.pattern == RF_PATTERN_QUANT_GEMM_E4M3 ? 128 : 64))
+        return bail(RF_ERR_UNSUPPORTED, "multi-segment GEMM: K / segments must be a multiple of the "
+                                        "K tile (quant 128, rms / layernorm 64)");
       p->kernel = d.pattern == RF_PATTERN_QUANT_GEMM_E4M3 ? rf::Kernel::QuantGemmSm100
                   : d.pattern == RF_PATTERN_LAYERNORM_GEMM ? rf::Kernel::LayerNormGemmSm100
                                                            : rf::Kernel::RmsGemmSm100;
@@ -499,9 +510,11 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
     default:
       return bail(RF_ERR_UNSUPPORTED, "unknown pattern");
   }
+  if (is_gemm(p->d.pattern) && p->d.pattern != RF_PATTERN_MOE_ROUTER) p->nsplit = d.segments;
   p->launches = (((p->d.pattern == RF_PATTERN_ATTENTION || p->d.pattern == RF_PATTERN_MLA_DECODE) &&
                   p->nsplit > 1) ||
-                 p->d.pattern == RF_PATTERN_MOE_ROUTER) ? 2 : 1;
+                 p->d.pattern == RF_PATTERN_MOE_ROUTER ||
+                 (is_gemm(p->d.pattern) && p->nsplit > 1)) ? 2 : 1;
 
   // ---- persistent workspace ----
   if (cudaMalloc(&p->domain_flag, sizeof(int)) != cudaSuccess ||
@@ -513,6 +526,14 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
         cudaMalloc(&p->ws_l, n * sizeof(float)) != cudaSuccess ||
         cudaMalloc(&p->ws_o, n * d.free_len * sizeof(float)) != cudaSuccess)
       return bail(RF_ERR_CUDA, "segment workspace allocation failed");
+  }
+  if (is_gemm(p->d.pattern) && p->d.pattern != RF_PATTERN_MOE_ROUTER && p->nsplit > 1) {
+    // Multi-Segment GEMM: [S, M, N] f32 slice accumulators + [S, M] statistics
+    const size_t sm = static_cast<size_t>(p->nsplit) * p->d.rows;
+    if (cudaMalloc(&p->ws_o, sm * p->d.free_len * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&p->ws_m, sm * sizeof(float)) != cudaSuccess ||
+        (p->d.pattern == RF_PATTERN_LAYERNORM_GEMM && cudaMalloc(&p->ws_l, sm * sizeof(float)) != cudaSuccess))
+      return bail(RF_ERR_CUDA, "multi-segment GEMM workspace allocation failed");
   }
   if (p->d.pattern == RF_PATTERN_MOE_ROUTER) {  // split-K partial scores (L2-resident)
     const size_t n = static_cast<size_t>(p->nsplit) * p->d.rows * p->d.len;

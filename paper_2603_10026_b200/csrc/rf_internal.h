@@ -138,7 +138,15 @@ struct GemmArgs {
   int* domain_flag;    // device int, set to 1 on 0/0 at finalize
   int64_t m, n, k;
   float fmax, eps;
+  // Multi-Segment (segments > 1): split-K slice partials + ordered fold
+  int64_t segments;    // S (1 = single segment)
+  int64_t ws_rows;     // rows between slices in the workspace (the plan's M)
+  float* ws;           // [S, ws_rows, N] f32 slice accumulators (this call's row offset applied)
+  float* ws_d1;        // [S, ws_rows] slice statistic (sum x^2 | sum x | absmax)
+  float* ws_d2;        // [S, ws_rows] layernorm: slice sum x^2
 };
+// Folds the S slice partials of a GEMM pattern in slice order (gemm_fold.cu).
+cudaError_t launch_gemm_fold(int pattern, const GemmArgs& g, cudaStream_t st);
 cudaError_t launch_quant_gemm_sm100(const GemmArgs& g, cudaStream_t st);
 cudaError_t launch_rms_gemm_sm100(const GemmArgs& g, cudaStream_t st);
 cudaError_t launch_layernorm_gemm_sm100(const GemmArgs& g, cudaStream_t st);

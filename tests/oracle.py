@@ -188,7 +188,7 @@ def quant_gemm_e4m3_torch(a, w, fmax=448.0, tile_k=128, pow2=True):
                                torch.ones_like(ref, dtype=torch.float64))
             acc *= corr[:, None]
         ref = nref
-        scale = (torch.full_like(ref, float(fmax)) / ref)[:, None]
+        scale = torch.where(ref > 0, torch.full_like(ref, float(fmax)) / ref, torch.zeros_like(ref))[:, None]
         qv = (blk * scale).to(torch.float8_e4m3fn).to(torch.float64)
         acc += qv @ W[l0:l0 + tile_k]
     fin = ref.double() / amax.double()

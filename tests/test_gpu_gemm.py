@@ -32,7 +32,8 @@ def _rms_run(x, g, w, eps=1e-6):
 
 
 @pytest.mark.parametrize("shape", [(128, 64, 256), (256, 512, 512), (384, 1024, 768),
-                                   (512, 4096, 512)])
+                                   (512, 4096, 512), (128, 4032, 256), (256, 4032, 256),
+                                   (128, 192, 256)])
 def test_rmsnorm_gemm_vs_oracle(shape):
     T, K, N = shape
     rng = np.random.default_rng(T + K + N)
@@ -254,3 +255,108 @@ def test_quant_gemm_against_reference_goldens(name):
     rel = np.sqrt(np.mean((c[0, :N] - gd["oracle.d2"]) ** 2)) / np.sqrt(np.mean(gd["oracle.d2"] ** 2))
     assert rel < 0.06
     assert abs(amax[0] - gd["oracle.d1"][0]) <= 2e-2 * gd["oracle.d1"][0]
+
+
+# ---------------------------------------------------------- Multi-Segment --
+# run_multisegment (proj/src/simulator.cpp:660-687) for the GEMM cascades: S
+# K-slices streamed from fresh state by the split-K kernels, folded in slice
+# order by gemm_fold.cu (Eq.16, incr_push_child).
+
+
+def _gemm_plan(pattern, M, K, N, segments, eps=1e-6):
+    from paper_2603_10026_b200 import Desc, Plan, _native as N_
+
+    pat = {"quant": N_.RF_PATTERN_QUANT_GEMM_E4M3, "rms": N_.RF_PATTERN_RMSNORM_GEMM,
+           "ln": N_.RF_PATTERN_LAYERNORM_GEMM}[pattern]
+    p = Plan(Desc(pat, "bf16", rows=M, len=K, free_len=N, segments=segments, eps=eps))
+    assert p.info["slices_launched"] == segments and p.launches_per_run == (2 if segments > 1 else 1)
+    return p
+
+
+@pytest.mark.parametrize("M", [128, 256])
+@pytest.mark.parametrize("S", [2, 4])
+def test_rms_and_layernorm_multisegment(M, S):
+    import torch
+
+    K, N = 512, 512
+    rng = np.random.default_rng(M + S)
+    x = O.round_bf16(rng.uniform(-1, 2, (M, K)))
+    w = torch.tensor(rng.uniform(-1, 1, (K, N)), dtype=torch.float32).cuda()
+    g = torch.tensor(rng.uniform(-1, 1, K), dtype=torch.float32).cuda()
+    xd = torch.tensor(x).bfloat16().cuda()
+    p = _gemm_plan("rms", M, K, N, S)
+    wp = p.pack_weight(w, g)
+    ss, y = torch.empty(M, device="cuda"), torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    p.run([xd, wp], [ss, y])
+    p1 = _gemm_plan("rms", M, K, N, 1)
+    ss1, y1 = torch.empty_like(ss), torch.empty_like(y)
+    p1.run([xd, wp], [ss1, y1])
+    torch.cuda.synchronize()
+    d1, yr = O.rmsnorm_gemm(x, np.ones(K), wp.double().cpu().numpy().T)
+    assert _err(ss.cpu(), d1) < 1e-5 and _err(y.float().cpu(), yr) < TOL
+    assert _err(y.float().cpu(), y1.float().cpu()) < 8e-3  # = single segment up to bf16 rounding
+    if M % 256 == 0:  # layernorm: 2-SM tiles
+        pl = _gemm_plan("ln", M, K, N, S, eps=1e-5)
+        wl = pl.pack_weight(w, g)
+        outs = [torch.empty(M, device="cuda"), torch.empty(M, device="cuda"),
+                torch.empty(M, N, dtype=torch.bfloat16, device="cuda"),
+                torch.empty(M, N, dtype=torch.bfloat16, device="cuda")]
+        pl.run([xd, wl], outs)
+        torch.cuda.synchronize()
+        wt = wl[:2 * N * K].view(torch.bfloat16).view(N, K).double().cpu().numpy().T
+        r1, r2, r3, r4 = O.layernorm_gemm(x, np.ones(K), wt, 1e-5)
+        for got, want, tol in zip(outs, (r1, r2, r3, r4), (1e-5, 1e-5, TOL, TOL)):
+            assert _err(got.float().cpu(), want) < tol
+
+
+@pytest.mark.parametrize("S", [2, 4])
+def test_quant_multisegment_matches_sliced_restatement(S):
+    """Each slice quantises with its own running absmax (fresh state); the
+    fold is c = sum_s c_s m_s / max_s m_s (acceptance.cpp:209-216)."""
+    import torch
+
+    M, K, N = 256, 1024, 512
+    rng = np.random.default_rng(S)
+    a = O.round_bf16(rng.uniform(-2, 2, (M, K)) * np.linspace(0.1, 1.0, K)[None])
+    p = _gemm_plan("quant", M, K, N, S)
+    wp = p.pack_weight(torch.tensor(rng.uniform(-1, 1, (K, N)), dtype=torch.float32).cuda())
+    amax, c = torch.empty(M, device="cuda"), torch.empty(M, N, device="cuda")
+    p.run([torch.tensor(a).bfloat16().cuda(), wp], [amax, c])
+    torch.cuda.synchronize()
+    w8 = wp.view(torch.float8_e4m3fn).double().cpu().numpy().T
+    L = K // S
+    parts = [O.quant_gemm_e4m3(a[:, s * L:(s + 1) * L], w8[s * L:(s + 1) * L], 448.0, 128) for s in range(S)]
+    m = np.max([d for d, _ in parts], axis=0)
+    want = sum(cs * ds[:, None] for ds, cs in parts) / m[:, None]
+    assert _err(amax.cpu(), m) == 0.0
+    assert _err(c.cpu(), want) < 1e-3
+    _, creal = O.quant_gemm(a, w8)
+    assert np.sqrt(np.mean((c.cpu().numpy() - creal) ** 2) / np.mean(creal ** 2)) < 0.06
+
+
+def test_quant_leading_zero_tiles_are_guarded():
+    """A row whose first K tiles are all zero: the guarded H' is the identity
+    while d1 = 0 (the reference's repair), so they contribute 0 — not
+    0 * fmax / 0 = NaN. Single and multi-segment (an all-zero slice)."""
+    import torch
+
+    M, K, N = 128, 512, 512
+    rng = np.random.default_rng(7)
+    a = O.round_bf16(rng.uniform(-2, 2, (M, K)))
+    a[3, :256] = 0.0  # two leading zero tiles; with S = 2 slice 0 of row 3 is all zero
+    a[4, :128] = 0.0
+    w = rng.uniform(-1, 1, (K, N))
+    for S in (1, 2):
+        p = _gemm_plan("quant", M, K, N, S)
+        wp = p.pack_weight(torch.tensor(w, dtype=torch.float32).cuda())
+        amax, c = torch.empty(M, device="cuda"), torch.empty(M, N, device="cuda")
+        p.run([torch.tensor(a).bfloat16().cuda(), wp], [amax, c])
+        p.check_domain()
+        cc = c.cpu().numpy()
+        assert np.isfinite(cc).all()
+        w8 = wp.view(torch.float8_e4m3fn).double().cpu().numpy().T
+        if S == 1:
+            _, want = O.quant_gemm_e4m3(a, w8, 448.0, 128)
+            assert _err(cc, want) < 1e-3
+        _, creal = O.quant_gemm(a, w8)
+        assert np.sqrt(np.mean((cc - creal) ** 2) / np.mean(creal ** 2)) < 0.06
