@@ -126,6 +126,10 @@ typedef struct rf_desc {
   int32_t producer_len; /* MOE_ROUTER: hd, the reduce axis of the producer GEMM;
                            MLA_DECODE: the q / cache row width (576) (ABI v3;
                            was `reserved` in v2, same offset) */
+  int64_t stat_len;     /* RMSNORM / LAYERNORM: the K of the statistics' means
+                           d1/K, d2/K (0 = len). A host that zero-pads the reduce
+                           axis to the kernel's K tile passes the cascade's own
+                           L0 here (zeros add nothing to sum x, sum x^2). (ABI v4) */
 } rf_desc;
 
 /* Device buffers for one rf_run. Inputs by pattern:

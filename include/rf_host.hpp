@@ -1107,29 +1107,24 @@ inline std::vector<ExecReport> execute_batched(const Program& prog, const TreeCo
       const bool quant = prog.pattern == RF_PATTERN_QUANT_GEMM_E4M3;
       const bool ln = prog.pattern == RF_PATTERN_LAYERNORM_GEMM;
       // Pad to the kernel tiles: M to whole row tiles (copies of row 0: never
-      // an all-zero padding row), K with zeros (neutral for max|a| and sum
-      // x^2, zero contributions) — LayerNorm excepted: zeros would shift the
-      // mean d1/K — and N with zero weight columns.
-      // RMSNorm: the kernel normalises by the mean over its (padded) K,
-      // 1/sqrt(d1/Kp + eps'). With r = L0/Kp, eps' = eps*r and g' = g*sqrt(r):
-      //   g' / sqrt(d1/Kp + eps') = g sqrt(r) / (sqrt(r) sqrt(d1/L0 + eps))
-      // which is the cascade's g / sqrt(d1/L0 + eps) exactly (d1 is unchanged).
-      if (ln && L0 % 64) throw NotFusable("layernorm_gemm: reduce length must be a multiple of 64");
+      // an all-zero padding row), K with zeros — neutral for max|a|, sum x and
+      // sum x^2, zero contributions; the statistics' means keep the cascade's
+      // own L0 (rf_desc.stat_len) — and N with zero weight columns.
       const long long N = prog.free_len;
       const long long Kp = round_up(L0, quant ? 128 : 64), Np = round_up(N, quant ? 512 : 256);
       const long long M = round_up(R, ln ? 256 : 128);
-      const double ratio = static_cast<double>(L0) / static_cast<double>(Kp);
       rf_desc d = base_desc(prog.pattern, RF_BF16);
       d.rows = M;
       d.len = Kp;
       d.free_len = Np;
+      d.stat_len = quant ? 0 : L0;
       // run_multisegment: the kernels split K into S slices (split-K partials
       // + slice-ordered fold, gemm_fold.cu) when the reference's slices of
       // L0 / S are whole K tiles; otherwise one segment (equal in exact
       // arithmetic; the S | L0 contract was checked above)
       d.segments = L0 % (segments * (quant ? 128 : 64)) == 0 ? segments : 1;
       d.fmax = prog.fmax;
-      d.eps = quant || ln ? prog.eps : prog.eps * ratio;
+      d.eps = prog.eps;
       PlanHandle h(d);
       const double* W = shared_weight(prog.w);
       std::vector<float> wf(Kp * Np, 0.f), gf(Kp, 0.f);
@@ -1137,8 +1132,7 @@ inline std::vector<ExecReport> execute_batched(const Program& prog, const TreeCo
         for (long long f = 0; f < N; ++f) wf[l * Np + f] = static_cast<float>(W[l * N + f]);
       if (!quant) {
         const double* g = shared_weight(prog.g);
-        const double gs = ln ? 1.0 : std::sqrt(ratio);
-        for (long long l = 0; l < L0; ++l) gf[l] = static_cast<float>(g[l] * gs);
+        for (long long l = 0; l < L0; ++l) gf[l] = static_cast<float>(g[l]);
       }
       void* packed = nullptr;
       check(rf_pack_weight_host(h.p, wf.data(), quant ? nullptr : gf.data(), &packed));

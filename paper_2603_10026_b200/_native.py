@@ -62,6 +62,7 @@ class rf_desc(ctypes.Structure):
         ("tile_stream", ctypes.c_int32),
         ("device", ctypes.c_int32),
         ("producer_len", ctypes.c_int32),
+        ("stat_len", ctypes.c_int64),
     ]
 
 

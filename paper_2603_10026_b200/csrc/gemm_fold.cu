@@ -89,7 +89,7 @@ __global__ void gemm_fold_kernel(const float* __restrict__ ws, const float* __re
 cudaError_t launch_gemm_fold(int pattern, const GemmArgs& g, cudaStream_t st) {
   const int64_t work = g.m * (g.n / 8);
   const unsigned blocks = static_cast<unsigned>((work + 255) / 256);
-  const float inv_k = 1.f / static_cast<float>(g.k);
+  const float inv_k = 1.f / static_cast<float>(g.stat_len > 0 ? g.stat_len : g.k);
   switch (pattern) {
     case RF_PATTERN_QUANT_GEMM_E4M3:
       gemm_fold_kernel<RF_PATTERN_QUANT_GEMM_E4M3><<<blocks, 256, 0, st>>>(

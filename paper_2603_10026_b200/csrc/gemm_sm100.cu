@@ -1065,7 +1065,7 @@ static cudaError_t launch_rms_like(const GemmArgs& g, cudaStream_t st, bool ln) 
   }
   cudaError_t e;
   if (pair) {  // 2-SM path
-    rms::Params p{g.d1, g.k, 1.f / static_cast<float>(g.k), g.eps, static_cast<int>(g.m / (2 * BM)),
+    rms::Params p{g.d1, g.k, 1.f / static_cast<float>(g.stat_len > 0 ? g.stat_len : g.k), g.eps, static_cast<int>(g.m / (2 * BM)),
                   static_cast<int>(g.n / BN), group_param(8), g.d2, g.colsum, g.c4 != nullptr,
                   k_slice, g.ws_d1, g.ws_d2, g.ws_rows, S > 1};
     const size_t smem = sizeof(rms2::Smem) + 1024;
@@ -1076,7 +1076,7 @@ static cudaError_t launch_rms_like(const GemmArgs& g, cudaStream_t st, bool ln) 
     kern<<<grid, rms2::NT, smem, st>>>(ta, tb, ty, ty4, p);
   } else {
     if (ln) return cudaErrorNotSupported;  // layernorm: 2-SM tiles only (M % 256)
-    rms::Params p{g.d1, g.k, 1.f / static_cast<float>(g.k), g.eps, static_cast<int>(g.m / BM),
+    rms::Params p{g.d1, g.k, 1.f / static_cast<float>(g.stat_len > 0 ? g.stat_len : g.k), g.eps, static_cast<int>(g.m / BM),
                   static_cast<int>(g.n / BN), group_param(8), nullptr, nullptr, 0,
                   k_slice, g.ws_d1, nullptr, g.ws_rows, S > 1};
     const size_t smem = sizeof(rms::Smem) + 1024;

@@ -251,6 +251,7 @@ rf_status gemm_run(const rf_plan* p, const rf_io* io, int64_t m0, int64_t nm, cu
   g.m = nm;
   g.n = d.free_len;
   g.k = d.len;
+  g.stat_len = d.stat_len > 0 ? d.stat_len : d.len;
   g.fmax = static_cast<float>(d.fmax);
   g.eps = static_cast<float>(d.eps);
   g.segments = d.segments;
@@ -389,6 +390,7 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
   // ---- shape validation (check_shapes, simulator.cpp:235-245) ----
   if (d.rows < 0 || d.len < 1 || d.free_len < 0 || d.batch < 1 || d.heads < 1)
     return fail(RF_ERR_SHAPE, "non-positive extent in descriptor");
+  if (d.stat_len < 0 || d.stat_len > d.len) return fail(RF_ERR_SHAPE, "stat_len must be in [0, len]");
   if (d.segments < 1 || d.len % d.segments != 0)  // simulator.cpp:668-671
     return fail(RF_ERR_SEGMENTATION, std::to_string(d.segments) +
                                          " segments do not divide L0 = " + std::to_string(d.len));

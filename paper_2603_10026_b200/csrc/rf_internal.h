@@ -137,6 +137,7 @@ struct GemmArgs {
   const float* colsum; // [N] (layernorm: column sums of the packed g*w)
   int* domain_flag;    // device int, set to 1 on 0/0 at finalize
   int64_t m, n, k;
+  int64_t stat_len;    // rms / layernorm: K of the statistics' means (0 = k)
   float fmax, eps;
   // Multi-Segment (segments > 1): split-K slice partials + ordered fold
   int64_t segments;    // S (1 = single segment)

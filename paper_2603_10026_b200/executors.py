@@ -94,6 +94,7 @@ class Desc:
     offset: float = 0.0
     device: int = 0
     producer_len: int = 0  # MOE_ROUTER: hd (the router GEMM's reduce axis)
+    stat_len: int = 0  # RMSNORM / LAYERNORM: K of the statistics' means (0 = len)
 
     def to_c(self) -> N.rf_desc:
         d = N.rf_desc()
@@ -106,6 +107,7 @@ class Desc:
         d.tile_rows = d.tile_stream = 0
         d.device = self.device
         d.producer_len = self.producer_len
+        d.stat_len = self.stat_len
         return d
 
 
