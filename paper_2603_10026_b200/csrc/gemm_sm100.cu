@@ -36,6 +36,22 @@ namespace {
 
 using namespace sm100;
 
+#ifdef RF_QNT_TRACE
+// clock64 timeline of one CTA of the 2-SM quant kernel (probe build only,
+// tools/trace_quant.py): slot = event * 64 + K step.
+__device__ long long g_qnt_trace[4096];
+__device__ int g_qnt_trace_cta;
+#define QTRACE(ev, t)                                                                 \
+  do {                                                                               \
+    if (blockIdx.x == g_qnt_trace_cta && blockIdx.y == 0 && (t) < 64)                \
+      g_qnt_trace[(ev) * 64 + (t)] = clock64();                                      \
+  } while (0)
+#else
+#define QTRACE(ev, t) \
+  do {                \
+  } while (0)
+#endif
+
 constexpr int BM = 128;
 constexpr int BN = 256;
 
@@ -787,6 +803,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   const int m0 = mt * 2 * BM + static_cast<int>(rank) * BM;
   const int kt = static_cast<int>(p.k_slice / BK);
   const int k0 = static_cast<int>(blockIdx.y * p.k_slice);
+  if (threadIdx.x == 0) QTRACE(7, 2);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < SA; ++i) {
@@ -818,10 +835,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       for (int t = 0; t < kt; ++t) {
         const int sa = t % SA, sw = t % SW;
         mbar_wait(&s.abf_empty[sa], ((t / SA) & 1) ^ 1);
+        QTRACE(5, t);
         mbar_arrive_expect_tx(&s.abf_full[sa], ABF_BYTES);
         tma_load_2d(s.abf[sa], &ta, &s.abf_full[sa], k0 + t * BK, m0, kEvictFirst);
         tma_load_2d(s.abf[sa] + BM * 128, &ta, &s.abf_full[sa], k0 + t * BK + 64, m0, kEvictFirst);
         mbar_wait(&s.w_empty[sw], ((t / SW) & 1) ^ 1);
+        QTRACE(6, t);
         mbar_arrive_expect_tx(&s.w_full[sw], W_BYTES);
         for (int h = 0; h < 2; ++h)
           tma_load_2d(s.w[sw] + h * 128 * 128, &tw, &s.w_full[sw], k0 + t * BK,
@@ -835,7 +854,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       for (int t = 0; t < kt; ++t) {
         const int sw = t % SW, s8 = t % S8;
         mbar_wait(&s.w_full[sw], (t / SW) & 1);
+        if (el) QTRACE(0, t);
         mbar_wait(&s.a8_full[s8], (t / S8) & 1);  // own A8 + peer (W half + A8) relay
+        if (el) QTRACE(1, t);
         tc_fence_after();
         if (el) {
           const uint32_t a = smem_u32(s.a8[s8]), b = smem_u32(s.w[sw]);
@@ -866,6 +887,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     for (int t = 0; t < kt; ++t) {
       const int sa = t % SA, s8 = t % S8;
       mbar_wait(&s.abf_full[sa], (t / SA) & 1);
+      if (threadIdx.x == 0) QTRACE(2, t);
       uint32_t x[64];
 #pragma unroll
       for (int c = 0; c < 2; ++c)
@@ -918,6 +940,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       uint64_t sc2;
       asm("mov.b64 %0, {%1, %1};" : "=l"(sc2) : "f"(sc));
       mbar_wait(&s.a8_empty[s8], ((t / S8) & 1) ^ 1);
+      if (threadIdx.x == 0) QTRACE(3, t);
       const uint32_t dst = smem_u32(s.a8[s8]);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -932,6 +955,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       }
       fence_proxy_async_smem();
       __syncwarp();
+      if (threadIdx.x == 0) QTRACE(4, t);
       if ((threadIdx.x & 31) == 0) mbar_arrive(&s.a8_full[s8]);
     }
     const float fin = p.partial ? ref : ref / amax;
@@ -944,6 +968,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     const int crow = p.partial ? static_cast<int>(blockIdx.y * p.ws_rows) + m0 : m0;
     named_bar_sync(1, 128);
     mbar_wait(&s.acc_full, 0);
+    if (threadIdx.x == 0) QTRACE(7, 0);
     tc_fence_after();
     const uint32_t stage = smem_u32(s.abf[0]);  // abf + w: 160 KB drained, C half-tile = 128 KB
 #pragma unroll 1
@@ -974,6 +999,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       named_bar_sync(1, 128);
     }
     if (threadIdx.x == 0) bulk_wait0();
+    if (threadIdx.x == 0) QTRACE(7, 1);
   }
   tc_fence_before();
   cluster_sync();
