@@ -1056,7 +1056,7 @@ __device__ __forceinline__ void load_step(uint4 (&x)[16], const __nv_bfloat16* r
 
 __device__ __forceinline__ float bf16_abs_f(uint32_t h) { return __uint_as_float((h & 0x7fffu) << 16); }
 
-__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(200)
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(192)
     quant_gemm_2sm_kernel(const __nv_bfloat16* __restrict__ A, const __grid_constant__ CUtensorMap tw,
                           const __grid_constant__ CUtensorMap tc, const qnt::Params p) {
   extern __shared__ uint8_t smem_raw[];
