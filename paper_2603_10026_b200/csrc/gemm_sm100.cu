@@ -26,6 +26,7 @@
 // Tiles: BM = 128 rows (tokens) x BN = 256 (N) per CTA, UMMA M=128 N=256.
 #include <cuda_bf16.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "rf_internal.h"
@@ -1056,7 +1057,7 @@ __device__ __forceinline__ void load_step(uint4 (&x)[16], const __nv_bfloat16* r
 
 __device__ __forceinline__ float bf16_abs_f(uint32_t h) { return __uint_as_float((h & 0x7fffu) << 16); }
 
-__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(192)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     quant_gemm_2sm_kernel(const __nv_bfloat16* __restrict__ A, const __grid_constant__ CUtensorMap tw,
                           const __grid_constant__ CUtensorMap tc, const qnt::Params p) {
   extern __shared__ uint8_t smem_raw[];
@@ -1146,10 +1147,12 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(192)
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     const __nv_bfloat16* arow = A + static_cast<int64_t>(m0 + 32 * q + half) * p.k + k0 + 8 * c;
     float* pub = &s.run_amax[32 * q + 16 * half];  // this half's 16 rows, i-major
-    uint4 xa[16], xb[16];
-    if (par < kt) load_step(xa, arow, p.k, par * BK);
-    if (par + 2 < kt) load_step(xb, arow, p.k, (par + 2) * BK);
-    auto step = [&](uint4 (&x)[16], int t) {
+    // one K step of A in registers; each row's loads for this warp's next step
+    // (t + 2) are issued as soon as the row is quantised, so they are in
+    // flight for about two K steps
+    uint4 x[16];
+    if (par < kt) load_step(x, arow, p.k, par * BK);
+    for (int t = par; t < kt; t += 2) {
       if (lane == 0 && q == 0) QTRACE(2, t);
       // tile absmax per row: 8 elements per lane, then the half-warp (16 lanes
       // = the row's 128 K) in packed row pairs
@@ -1238,19 +1241,12 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(192)
         const uint32_t q2 = qnt::quant_pair(x[i].z, sc2), q3 = qnt::quant_pair(x[i].w, sc2);
         sts64(dst + sw128(32 * q + 2 * i + half, c >> 1), (q0 & 0xffffu) | (q1 << 16),
               (q2 & 0xffffu) | (q3 << 16));
+        if (t + 2 < kt) x[i] = ldg128_stream(arow + (2 * i) * p.k + (t + 2) * BK);
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0 && q == 0) QTRACE(4, t);
       if (lane == 0) mbar_arrive(&s.a8_full[s8]);
-    };
-    for (int t = par; t < kt; t += 4) {
-      step(xa, t);
-      if (t + 4 < kt) load_step(xa, arow, p.k, (t + 4) * BK);
-      if (t + 2 < kt) {
-        step(xb, t + 2);
-        if (t + 6 < kt) load_step(xb, arow, p.k, (t + 6) * BK);
-      }
     }
     // ---- finalize_root: retarget H'(ref) -> H(d1): c = acc * ref / d1 ----
     named_bar_sync(1, NQW * 32);  // the last step's running d1 is published
@@ -1465,6 +1461,13 @@ cudaError_t launch_quant_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     dim3 grid(static_cast<unsigned>(2 * (g.n / qnt::BNQ) * (g.m / (2 * BM))), static_cast<unsigned>(S));
     qnt3::quant_gemm_2sm_kernel<<<grid, qnt3::NT, smem, st>>>(static_cast<const __nv_bfloat16*>(g.a), tw, tc, p);
+    if (std::getenv("RF_DEBUG_LAUNCH")) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, qnt3::quant_gemm_2sm_kernel);
+      std::fprintf(stderr, "qnt3: regs %d maxThreads %d static smem %zu dyn %zu maxDyn %d local %zu err %s\n",
+                   fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, smem,
+                   fa.maxDynamicSharedSizeBytes, fa.localSizeBytes, cudaGetErrorString(cudaPeekAtLastError()));
+    }
   } else if (g.m % (2 * BM) == 0) {  // 2-SM path, TMA-staged A (RF_QNT_V=2)
     qnt::Params p{g.d1, g.domain_flag, g.k, g.fmax, static_cast<int>(g.m / (2 * BM)),
                   static_cast<int>(g.n / qnt::BNQ), group_param(4), k_slice, g.ws_d1, g.ws_rows, S > 1};
