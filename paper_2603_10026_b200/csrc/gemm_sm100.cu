@@ -1057,6 +1057,17 @@ __device__ __forceinline__ void load_step(uint4 (&x)[16], const __nv_bfloat16* r
 
 __device__ __forceinline__ float bf16_abs_f(uint32_t h) { return __uint_as_float((h & 0x7fffu) << 16); }
 
+// Branch-free H' reference of a non-negative float given by its bits: the
+// smallest power of two >= x (0 for 0), as bits.
+__device__ __forceinline__ uint32_t pow2_ceil_bits(uint32_t b) {
+  return (b & 0x007fffffu) ? (b & 0x7f800000u) + 0x00800000u : b;
+}
+
+// fmax / ref for a power-of-two ref (exact: 1/2^k has bits (254 << 23) - bits(2^k)); 0 for ref = 0.
+__device__ __forceinline__ float quant_scale(uint32_t ref_bits, float fmax) {
+  return ref_bits ? fmax * __uint_as_float((254u << 23) - ref_bits) : 0.f;
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     quant_gemm_2sm_kernel(const __nv_bfloat16* __restrict__ A, const __grid_constant__ CUtensorMap tw,
                           const __grid_constant__ CUtensorMap tc, const qnt::Params p) {
@@ -1194,7 +1205,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
         amax[2 * j + 1] = fmaxf(prev[2 * j + 1], bf16_abs_f(pk[j] >> 16));
       }
 #pragma unroll
-      for (int i = 0; i < 16; ++i) changed |= t > 0 && qnt::pow2_ceil(amax[i]) != qnt::pow2_ceil(prev[i]);
+      for (int i = 0; i < 16; ++i)
+        changed |= t > 0 && pow2_ceil_bits(__float_as_uint(amax[i])) != pow2_ceil_bits(__float_as_uint(prev[i]));
       // publish the running d1 for step t + 1 and release the other warp
       if (c == 0) {
         float4* dst = reinterpret_cast<float4*>(pub);
@@ -1233,8 +1245,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       const uint32_t dst = smem_u32(s.a8[s8]) + 8 * (c & 1);
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        const float ref = qnt::pow2_ceil(amax[i]);
-        const float sc = ref > 0.f ? p.fmax / ref : 0.f;  // see quant_gemm_kernel
+        // fmax / ref, 0 while d1 = 0 (see quant_gemm_kernel)
+        const float sc = quant_scale(pow2_ceil_bits(__float_as_uint(amax[i])), p.fmax);
         uint64_t sc2;
         asm("mov.b64 %0, {%1, %1};" : "=l"(sc2) : "f"(sc));
         const uint32_t q0 = qnt::quant_pair(x[i].x, sc2), q1 = qnt::quant_pair(x[i].y, sc2);
