@@ -1009,316 +1009,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
 
 }  // namespace qnt2
 
-// ------------------------------------- QUANT_GEMM, 2-SM, register-fed A --
-//
-// The bf16 activations never touch shared memory. Measured (tools/
-// trace_quant.py, profiles/r2_trace_quant.txt) the TMA-staged form spends
-// ~1730 cycles per K step against ~1024 of MMA work: the tensor core is never
-// starved of issued MMAs, it is slowed by the shared-memory port, which per K
-// step carries the bf16 A tile twice (TMA write 32 KB + quantiser read 32 KB)
-// on top of W (32 KB), A8 (16 KB) and the MMA operand reads (64 KB). Here
-// eight quantiser warps load A straight from global memory (coalesced: a
-// half-warp reads one row's 256 B of the K step), so the port carries 112 KB
-// per step instead of 176 KB.
-//
-// Warp w (0..7) owns TMEM lane quarter q = w & 3 (rows 32q..32q+31, the only
-// accumulator rows it may correct) and the K steps t = w >> 2 (mod 2): the two
-// warps of a quarter alternate steps, each with two steps of loads in flight.
-// The running absmax is sequential in t, so a warp publishes its rows' running
-// d1 to shared memory and releases the quarter's other warp with a named
-// barrier (bar.arrive / bar.sync, one barrier id per quarter and step parity)
-// before it quantises — the exchange is off the quantisation path.
-namespace qnt3 {
-
-using qnt::BK;   // 128
-using qnt::BNQ;  // 512
-constexpr int SW = 4, S8 = 4;
-constexpr int NQW = 8;                 // quantiser warps
-constexpr int WARP_TMA = NQW, WARP_MMA = NQW + 1;
-constexpr int NT = (NQW + 2) * 32;     // 320
-constexpr int W_BYTES = 2 * 128 * BK;  // 32 KB: this CTA's halves of the two 256-row W blocks
-constexpr int A8_BYTES = BM * BK;      // 16 KB
-
-struct Smem {
-  uint8_t w[SW][W_BYTES];    // 128 KB (C staging after the mainloop)
-  uint8_t a8[S8][A8_BYTES];  // 64 KB
-  float run_amax[BM];        // running d1 per row: index 32q + 16 (row & 1) + (row & 31) / 2
-  uint64_t w_full[SW], w_empty[SW], a8_full[S8], a8_empty[S8];
-  uint64_t acc_full;
-  uint32_t tmem_base;
-};
-
-// K step t of this lane's 16 rows: x[i] = row 32q + 2i + half, K chunk [8c, 8c + 8).
-__device__ __forceinline__ void load_step(uint4 (&x)[16], const __nv_bfloat16* row0, int64_t k,
-                                          int kofs) {
-#pragma unroll
-  for (int i = 0; i < 16; ++i) x[i] = ldg128_stream(row0 + (2 * i) * k + kofs);
-}
-
-__device__ __forceinline__ float bf16_abs_f(uint32_t h) { return __uint_as_float((h & 0x7fffu) << 16); }
-
-// Branch-free H' reference of a non-negative float given by its bits: the
-// smallest power of two >= x (0 for 0), as bits.
-__device__ __forceinline__ uint32_t pow2_ceil_bits(uint32_t b) {
-  return (b & 0x007fffffu) ? (b & 0x7f800000u) + 0x00800000u : b;
-}
-
-// fmax / ref for a power-of-two ref (exact: 1/2^k has bits (254 << 23) - bits(2^k)); 0 for ref = 0.
-__device__ __forceinline__ float quant_scale(uint32_t ref_bits, float fmax) {
-  return ref_bits ? fmax * __uint_as_float((254u << 23) - ref_bits) : 0.f;
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
-    quant_gemm_2sm_kernel(const __nv_bfloat16* __restrict__ A, const __grid_constant__ CUtensorMap tw,
-                          const __grid_constant__ CUtensorMap tc, const qnt::Params p) {
-  extern __shared__ uint8_t smem_raw[];
-  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int warp = warp_id();
-  const int lane = lane_id();
-  const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
-  int mt, nt;
-  tile_of(blockIdx.x >> 1, p.mt_count, p.nt_count, p.group_n, mt, nt);
-  const int n0 = nt * BNQ;
-  const int m0 = mt * 2 * BM + static_cast<int>(rank) * BM;
-  const int kt = static_cast<int>(p.k_slice / BK);
-  const int k0 = static_cast<int>(blockIdx.y * p.k_slice);
-  if (threadIdx.x == 0) QTRACE(7, 2);
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < SW; ++i) {
-      mbar_init(&s.w_full[i], 1);
-      mbar_init(&s.w_empty[i], 1);
-    }
-    for (int i = 0; i < S8; ++i) {
-      mbar_init(&s.a8_full[i], leader ? 4 + 1 : 4);  // the step's 4 quarter warps (+ peer relay)
-      mbar_init(&s.a8_empty[i], 1);
-    }
-    mbar_init(&s.acc_full, 1);
-    fence_barrier_init();
-  }
-  if (warp == WARP_MMA) tmem_alloc_2sm<512>(&s.tmem_base);
-  tc_fence_before();
-  cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem = s.tmem_base;
-
-  if (warp == WARP_TMA) {
-    if (elect_one()) {
-      prefetch_tmap(&tw);
-      prefetch_tmap(&tc);
-      for (int t = 0; t < kt; ++t) {
-        const int sw = t % SW;
-        mbar_wait(&s.w_empty[sw], ((t / SW) & 1) ^ 1);
-        QTRACE(6, t);
-        mbar_arrive_expect_tx(&s.w_full[sw], W_BYTES);
-        for (int h = 0; h < 2; ++h)
-          tma_load_2d(s.w[sw] + h * 128 * 128, &tw, &s.w_full[sw], k0 + t * BK,
-                      n0 + 256 * h + 128 * static_cast<int>(rank), kEvictLast);
-      }
-    }
-  } else if (warp == WARP_MMA) {
-    if (leader) {
-      const uint32_t idesc = idesc_f8(2 * BM, 256);
-      const bool el = elect_one();
-      for (int t = 0; t < kt; ++t) {
-        const int sw = t % SW, s8 = t % S8;
-        mbar_wait(&s.w_full[sw], (t / SW) & 1);
-        if (el) QTRACE(0, t);
-        mbar_wait(&s.a8_full[s8], (t / S8) & 1);  // own A8 + peer (W half + A8) relay
-        if (el) QTRACE(1, t);
-        tc_fence_after();
-        if (el) {
-          const uint32_t a = smem_u32(s.a8[s8]), b = smem_u32(s.w[sw]);
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int ks = 0; ks < BK / 32; ++ks)
-              mma_f8_ss_2sm(tmem + h * 256, sdesc_kmajor_sw128(a + ks * 32),
-                            sdesc_kmajor_sw128(b + h * 128 * 128 + ks * 32), idesc, (t | ks) != 0);
-          mma_commit_2sm(&s.w_empty[sw]);
-          mma_commit_2sm(&s.a8_empty[s8]);
-          if (t + 1 == kt) mma_commit_2sm(&s.acc_full);
-        }
-        __syncwarp();
-      }
-    } else if (elect_one()) {
-      // relay: this CTA's W half landed and its A8 rows are written -> leader
-      for (int t = 0; t < kt; ++t) {
-        const int sw = t % SW, s8 = t % S8;
-        mbar_wait(&s.w_full[sw], (t / SW) & 1);
-        mbar_wait(&s.a8_full[s8], (t / S8) & 1);
-        mbar_arrive_cluster(mapa_shared(smem_u32(&s.a8_full[s8]), 0));
-      }
-    }
-  } else {
-    // ---- quantiser warps: reduction 1 (running absmax) + e4m3 quantisation of A ----
-    const int q = warp & 3, par = warp >> 2;
-    const int half = lane >> 4, c = lane & 15;
-    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    const __nv_bfloat16* arow = A + static_cast<int64_t>(m0 + 32 * q + half) * p.k + k0 + 8 * c;
-    float* pub = &s.run_amax[32 * q + 16 * half];  // this half's 16 rows, i-major
-    // one K step of A in registers; each row's loads for this warp's next step
-    // (t + 2) are issued as soon as the row is quantised, so they are in
-    // flight for about two K steps
-    uint4 x[16];
-    if (par < kt) load_step(x, arow, p.k, par * BK);
-    for (int t = par; t < kt; t += 2) {
-      if (lane == 0 && q == 0) QTRACE(2, t);
-      // tile absmax per row: 8 elements per lane, then the half-warp (16 lanes
-      // = the row's 128 K) in packed row pairs
-      uint32_t pk[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        uint32_t m2[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const uint4 v = x[2 * j + e];
-          uint32_t m = qnt::absmax_bf16x2(qnt::absmax_bf16x2(v.x, v.y), qnt::absmax_bf16x2(v.z, v.w));
-          m2[e] = qnt::absmax_bf16x2(m, __byte_perm(m, 0, 0x1032));  // both halves = the max
-        }
-        pk[j] = __byte_perm(m2[0], m2[1], 0x5410);  // lo: row 2(2j) + half, hi: row 2(2j+1) + half
-      }
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) pk[j] = qnt::absmax_bf16x2(pk[j], __shfl_xor_sync(0xffffffffu, pk[j], o));
-      // previous running d1 (published by the quarter's other warp for step t - 1)
-      float prev[16];
-      if (t > 0) {
-        named_bar_sync(2 + 2 * q + (t & 1), 64);
-        const float4* src = reinterpret_cast<const float4*>(pub);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const float4 f = src[v];
-          prev[4 * v] = f.x; prev[4 * v + 1] = f.y; prev[4 * v + 2] = f.z; prev[4 * v + 3] = f.w;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) prev[i] = 0.f;
-      }
-      float amax[16];  // running d1 of rows 32q + 2i + half after step t
-      bool changed = false;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        amax[2 * j] = fmaxf(prev[2 * j], bf16_abs_f(pk[j]));
-        amax[2 * j + 1] = fmaxf(prev[2 * j + 1], bf16_abs_f(pk[j] >> 16));
-      }
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        changed |= t > 0 && pow2_ceil_bits(__float_as_uint(amax[i])) != pow2_ceil_bits(__float_as_uint(prev[i]));
-      // publish the running d1 for step t + 1 and release the other warp
-      if (c == 0) {
-        float4* dst = reinterpret_cast<float4*>(pub);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) dst[v] = make_float4(amax[4 * v], amax[4 * v + 1], amax[4 * v + 2], amax[4 * v + 3]);
-      }
-      if (t + 1 < kt) named_bar_arrive(2 + 2 * q + ((t + 1) & 1), 64);
-      if (__any_sync(0xffffffffu, changed)) {
-        // the accumulator rows of this quarter, once MMA(t - 1) has retired
-        float fr = 1.f;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          // Eq.17 correction ref'/ref (powers of two; 0 while d1' = 0)
-          const float fi = qnt::pow2_ceil(prev[i]) / qnt::pow2_ceil(amax[i]);
-          const float v = __shfl_sync(0xffffffffu, fi, (lane & 1) * 16);
-          if ((lane >> 1) == i) fr = v;
-        }
-        const int sp = (t - 1) % S8;
-        mbar_wait(&s.a8_empty[sp], ((t - 1) / S8) & 1);
-        tc_fence_after();
-#pragma unroll 1
-        for (int cc = 0; cc < 2 * 256 / 32; ++cc) {
-          uint32_t v[32];
-          tmem_ld32(tmem + lane_off + cc * 32, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * fr);
-          tmem_st32(tmem + lane_off + cc * 32, v);
-        }
-        tmem_st_wait();
-        tc_fence_before();
-      }
-      const int s8 = t % S8;
-      mbar_wait(&s.a8_empty[s8], ((t / S8) & 1) ^ 1);
-      if (lane == 0 && q == 0) QTRACE(3, t);
-      const uint32_t dst = smem_u32(s.a8[s8]) + 8 * (c & 1);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        // fmax / ref, 0 while d1 = 0 (see quant_gemm_kernel)
-        const float sc = quant_scale(pow2_ceil_bits(__float_as_uint(amax[i])), p.fmax);
-        uint64_t sc2;
-        asm("mov.b64 %0, {%1, %1};" : "=l"(sc2) : "f"(sc));
-        const uint32_t q0 = qnt::quant_pair(x[i].x, sc2), q1 = qnt::quant_pair(x[i].y, sc2);
-        const uint32_t q2 = qnt::quant_pair(x[i].z, sc2), q3 = qnt::quant_pair(x[i].w, sc2);
-        sts64(dst + sw128(32 * q + 2 * i + half, c >> 1), (q0 & 0xffffu) | (q1 << 16),
-              (q2 & 0xffffu) | (q3 << 16));
-        if (t + 2 < kt) x[i] = ldg128_stream(arow + (2 * i) * p.k + (t + 2) * BK);
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0 && q == 0) QTRACE(4, t);
-      if (lane == 0) mbar_arrive(&s.a8_full[s8]);
-    }
-    // ---- finalize_root: retarget H'(ref) -> H(d1): c = acc * ref / d1 ----
-    named_bar_sync(1, NQW * 32);  // the last step's running d1 is published
-    const int row = 32 * q + lane;
-    const float am = s.run_amax[32 * q + 16 * (lane & 1) + (lane >> 1)];
-    const float rf = qnt::pow2_ceil(am);
-    const float fin = p.partial ? rf : rf / am;  // 0/0 -> NaN for an all-zero row (DomainError)
-    if (par == 0) {
-      if (p.partial) {
-        if (nt == 0) p.ws_d1[blockIdx.y * p.ws_rows + m0 + row] = am;
-      } else {
-        if (!(am > 0.f)) atomicExch(p.domain_flag, 1);
-        if (nt == 0) p.d1[m0 + row] = am;
-      }
-    }
-    const int crow = p.partial ? static_cast<int>(blockIdx.y * p.ws_rows) + m0 : m0;
-    mbar_wait(&s.acc_full, 0);
-    if (threadIdx.x == 0) QTRACE(7, 0);
-    tc_fence_after();
-    // columns [256 par, 256 par + 256) of the 128 x 512 C tile, staged in this
-    // group's 64 KB of the drained W ring, 4 chunks of 32 columns per round
-    uint8_t* stage_ptr = s.w[0] + par * (4 * BM * 128);
-    const uint32_t stage = smem_u32(stage_ptr);
-#pragma unroll 1
-    for (int r0 = 0; r0 < 8; r0 += 4) {
-#pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {
-        uint32_t v[32];
-        tmem_ld32(tmem + lane_off + par * 256 + (r0 + cc) * 32, v);
-        tmem_ld_wait();
-        const uint32_t chunk = stage + cc * (BM * 128);
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          sts128(chunk + sw128(row, u),
-                 make_uint4(__float_as_uint(__uint_as_float(v[4 * u]) * fin),
-                            __float_as_uint(__uint_as_float(v[4 * u + 1]) * fin),
-                            __float_as_uint(__uint_as_float(v[4 * u + 2]) * fin),
-                            __float_as_uint(__uint_as_float(v[4 * u + 3]) * fin)));
-      }
-      fence_proxy_async_smem();
-      named_bar_sync(10 + par, 128);
-      if ((threadIdx.x & 127) == 0) {
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
-          tma_store_2d(&tc, stage_ptr + cc * (BM * 128), n0 + par * 256 + (r0 + cc) * 32, crow);
-        bulk_commit();
-        bulk_wait_read0();
-      }
-      named_bar_sync(10 + par, 128);
-    }
-    if ((threadIdx.x & 127) == 0) bulk_wait0();
-    if (threadIdx.x == 0) QTRACE(7, 1);
-  }
-  tc_fence_before();
-  cluster_sync();
-  if (warp == WARP_MMA) tmem_dealloc_2sm<512>(tmem);
-}
-
-}  // namespace qnt3
-
 // ============================================================== packing ====
 
 // w [K,N] f32 (reduce-axis major) -> out [N,K]: transposed, g folded (rms) or
@@ -1463,24 +1153,7 @@ cudaError_t launch_quant_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
       return cudaErrorInvalidValue;
   }
   cudaError_t e;
-  static const bool v2 = std::getenv("RF_QNT_V") && std::atoi(std::getenv("RF_QNT_V")) == 2;
-  if (g.m % (2 * BM) == 0 && !v2) {  // 2-SM path, register-fed A
-    qnt::Params p{g.d1, g.domain_flag, g.k, g.fmax, static_cast<int>(g.m / (2 * BM)),
-                  static_cast<int>(g.n / qnt::BNQ), group_param(4), k_slice, g.ws_d1, g.ws_rows, S > 1};
-    const size_t smem = sizeof(qnt3::Smem) + 1024;
-    e = cudaFuncSetAttribute(qnt3::quant_gemm_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    dim3 grid(static_cast<unsigned>(2 * (g.n / qnt::BNQ) * (g.m / (2 * BM))), static_cast<unsigned>(S));
-    qnt3::quant_gemm_2sm_kernel<<<grid, qnt3::NT, smem, st>>>(static_cast<const __nv_bfloat16*>(g.a), tw, tc, p);
-    if (std::getenv("RF_DEBUG_LAUNCH")) {
-      cudaFuncAttributes fa{};
-      cudaFuncGetAttributes(&fa, qnt3::quant_gemm_2sm_kernel);
-      std::fprintf(stderr, "qnt3: regs %d maxThreads %d static smem %zu dyn %zu maxDyn %d local %zu err %s\n",
-                   fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, smem,
-                   fa.maxDynamicSharedSizeBytes, fa.localSizeBytes, cudaGetErrorString(cudaPeekAtLastError()));
-    }
-  } else if (g.m % (2 * BM) == 0) {  // 2-SM path, TMA-staged A (RF_QNT_V=2)
+  if (g.m % (2 * BM) == 0) {  // 2-SM path
     qnt::Params p{g.d1, g.domain_flag, g.k, g.fmax, static_cast<int>(g.m / (2 * BM)),
                   static_cast<int>(g.n / qnt::BNQ), group_param(4), k_slice, g.ws_d1, g.ws_rows, S > 1};
     const size_t smem = sizeof(qnt2::Smem) + 1024;
