@@ -971,33 +971,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     mbar_wait(&s.acc_full, 0);
     if (threadIdx.x == 0) QTRACE(7, 0);
     tc_fence_after();
-    const uint32_t stage = smem_u32(s.abf[0]);  // abf + w: 160 KB drained, C half-tile = 128 KB
+    // C tile (128 rows x 512 fp32 columns = 16 chunks of 32 columns) through
+    // two 64 KB staging areas of the drained rings: round r (4 chunks) fills
+    // area r & 1 while the TMA store of round r - 1 drains the other, and the
+    // next chunk's TMEM load is in flight while the current one is staged.
+    uint8_t* const base = reinterpret_cast<uint8_t*>(&s);  // abf ring then w ring: 192 KB drained
+    uint8_t* const area[2] = {base, base + 4 * (BM * 128)};
+    uint32_t v[2][32];
+    tmem_ld32(tmem + lane_off, v[0]);
 #pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-#pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tmem + lane_off + h * 256 + c * 32, v);
+    for (int rnd = 0; rnd < 4; ++rnd) {
+      if (rnd >= 2) {  // round rnd - 2's store has finished reading this area
+        if (threadIdx.x == 0) bulk_wait_read1();
+        named_bar_sync(1, 128);
+      }
+      const uint32_t stage = smem_u32(area[rnd & 1]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int cc = 4 * rnd + c;
         tmem_ld_wait();
+        if (cc + 1 < 16) tmem_ld32(tmem + lane_off + (cc + 1) * 32, v[(c + 1) & 1]);
         const uint32_t chunk = stage + c * (BM * 128);
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           sts128(chunk + sw128(r, u),
-                 make_uint4(__float_as_uint(__uint_as_float(v[4 * u]) * fin),
-                            __float_as_uint(__uint_as_float(v[4 * u + 1]) * fin),
-                            __float_as_uint(__uint_as_float(v[4 * u + 2]) * fin),
-                            __float_as_uint(__uint_as_float(v[4 * u + 3]) * fin)));
+                 make_uint4(__float_as_uint(__uint_as_float(v[c & 1][4 * u]) * fin),
+                            __float_as_uint(__uint_as_float(v[c & 1][4 * u + 1]) * fin),
+                            __float_as_uint(__uint_as_float(v[c & 1][4 * u + 2]) * fin),
+                            __float_as_uint(__uint_as_float(v[c & 1][4 * u + 3]) * fin)));
       }
       fence_proxy_async_smem();
       named_bar_sync(1, 128);
       if (threadIdx.x == 0) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          tma_store_2d(&tc, s.abf[0] + c * (BM * 128), n0 + h * 256 + 32 * c, crow);
+        for (int c = 0; c < 4; ++c)
+          tma_store_2d(&tc, area[rnd & 1] + c * (BM * 128), n0 + 128 * rnd + 32 * c, crow);
         bulk_commit();
-        bulk_wait_read0();
       }
-      named_bar_sync(1, 128);
     }
     if (threadIdx.x == 0) bulk_wait0();
     if (threadIdx.x == 0) QTRACE(7, 1);
