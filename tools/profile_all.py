@@ -42,7 +42,7 @@ def raw(rep):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tag", default="r1")
-    ap.add_argument("--configs", default="0,1,2,3,4")
+    ap.add_argument("--configs", default="0,1,2,3,4,5,6,7")
     a = ap.parse_args()
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     summary, traffic = {}, {}
@@ -51,7 +51,7 @@ def main():
         cmd = ["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on",
                "-k", f"regex:{KERNELS[c]}", "-s", "3", "-c", "1", "-f", "-o", rep,
                sys.executable, os.path.join(ROOT, "bench.py"), "--config", str(c), "--steps", "2",
-               "--warmup", "3", "--no-cpu-baseline"]
+               "--warmup", "3", "--no-cpu-baseline", "--no-parity", "--also", ""]
         subprocess.run(cmd, capture_output=True, text=True, timeout=900)
         try:
             m = raw(rep + ".ncu-rep")
@@ -68,7 +68,7 @@ def main():
     subprocess.run(["ncu", "--metrics", "gpu__time_duration.sum", "--clock-control", "none",
                     "-c", "60", "--csv", "--log-file", lcsv, sys.executable,
                     os.path.join(ROOT, "bench.py"), "--steps", "5", "--warmup", "3",
-                    "--no-cpu-baseline"], capture_output=True, timeout=900)
+                    "--no-cpu-baseline", "--no-parity", "--also", ""], capture_output=True, timeout=900)
     json.dump(summary, open(os.path.join(ROOT, "gpurun_out", f"{a.tag}_ncu_summary.json"), "w"),
               indent=1)
     json.dump({k: int(v) for k, v in traffic.items()},
