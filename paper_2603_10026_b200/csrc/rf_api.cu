@@ -163,7 +163,6 @@ const char* kernel_name(rf::Kernel k) {
     case rf::Kernel::SoftmaxRows: return "softmax_rows (SIMT, single pass)";
     case rf::Kernel::AttentionF32: return "attention_f32 (SIMT, paper form)";
     case rf::Kernel::AttentionSm100: return "attention_sm100 (bf16 tcgen05/TMEM/TMA, ping-pong Q tiles)";
-    case rf::Kernel::AttentionQt: return "attention_sm100_qt (bf16 tcgen05, Q in TMEM, double-buffered S/TMA)";
     case rf::Kernel::AttentionDecode: return "attention_decode (bf16 split-KV, TMA bulk)";
     case rf::Kernel::QuantGemmSm100: return "quant_gemm_sm100 (e4m3 tcgen05 kind::f8f6f4)";
     case rf::Kernel::RmsGemmSm100: return "rmsnorm_gemm_sm100 (bf16 tcgen05 kind::f16)";
@@ -220,7 +219,6 @@ rf_status attention_run(const rf_plan* p, const rf_io* io, int64_t bh0, int64_t 
   cudaError_t e;
   switch (p->kernel) {
     case rf::Kernel::AttentionSm100: e = rf::launch_attention_sm100(a, st); break;
-    case rf::Kernel::AttentionQt: e = rf::launch_attention_qt(a, st); break;
     case rf::Kernel::AttentionDecode: e = rf::launch_attention_decode(a, st); break;
     default: e = rf::launch_attention_f32(a, st); break;
   }
@@ -448,9 +446,6 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
       } else if (d.rows == 1) {
         p->kernel = rf::Kernel::AttentionDecode;
         p->nsplit = pick_decode_splits(d.batch * d.heads, d.len, d.segments);
-      } else if (rf::attention_qt_supports(d.rows, d.len, d.free_len, d.segments) &&
-                 !(std::getenv("RF_ATTN_V") && std::string(std::getenv("RF_ATTN_V")) == "3")) {
-        p->kernel = rf::Kernel::AttentionQt;
       } else if (rf::attention_sm100_supports(d.rows, d.len, d.free_len, d.segments)) {
         p->kernel = rf::Kernel::AttentionSm100;
       } else {
@@ -769,7 +764,6 @@ rf_status rf_run_partials(const rf_plan* p, const rf_io* io, int64_t slice_begin
   cudaError_t e;
   switch (p->kernel) {
     case rf::Kernel::AttentionSm100: e = rf::launch_attention_sm100(a, as_stream(stream)); break;
-    case rf::Kernel::AttentionQt: e = rf::launch_attention_qt(a, as_stream(stream)); break;
     case rf::Kernel::AttentionDecode: e = rf::launch_attention_decode(a, as_stream(stream)); break;
     default: e = rf::launch_attention_f32(a, as_stream(stream)); break;
   }

@@ -27,7 +27,6 @@ enum class Kernel {
   SoftmaxRows,        // softmax.cu
   AttentionF32,       // attn_f32.cu   (SIMT, paper form, cfg1)
   AttentionSm100,     // attn_sm100.cu (bf16 tcgen05/TMEM/TMA prefill, ping-pong Q tiles)
-  AttentionQt,        // attn_sm100_qt.cu (bf16, Q in TMEM, double-buffered S; cfg2)
   AttentionDecode,    // attn_decode.cu (bf16 split-KV streaming, cfg3)
   QuantGemmSm100,     // gemm_sm100.cu (e4m3 kind::f8f6f4, cfg4)
   RmsGemmSm100,       // gemm_sm100.cu (bf16 kind::f16, cfg5)
@@ -114,6 +113,7 @@ cudaError_t launch_attention_decode(const AttnArgs& a, cudaStream_t st);
 // Returns cudaErrorNotSupported when the shape has no tcgen05 instantiation.
 cudaError_t launch_attention_sm100(const AttnArgs& a, cudaStream_t st);
 bool attention_sm100_supports(int64_t sq, int64_t skv, int64_t d, int64_t segments);
+// experimental/attn_sm100_qt.cu (not in librf_cuda: Q in TMEM, measured slower)
 cudaError_t launch_attention_qt(const AttnArgs& a, cudaStream_t st);
 bool attention_qt_supports(int64_t sq, int64_t skv, int64_t d, int64_t segments);
 // experimental/attn_sm100_2sm.cu (probe library only; not in librf_cuda)
