@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define RF_CUDA_ABI_VERSION 4
+#define RF_CUDA_ABI_VERSION 5
 
 typedef enum rf_status {
   RF_OK = 0,
@@ -130,6 +130,22 @@ typedef struct rf_desc {
                            d1/K, d2/K (0 = len). A host that zero-pads the reduce
                            axis to the kernel's K tile passes the cascade's own
                            L0 here (zeros add nothing to sum x, sum x^2). (ABI v4) */
+  /* Fusion at level k, the non-incremental executor run_fused(prog, cfg, k, store)
+   * (proj/src/simulator.cpp:485-559). 0 = the incremental
+   * executors above. k >= 1: the reduction tree is tree[0..tree_depth-1] =
+   * TreeConfig.levels[1..K] (L0 = len is implicit, tree[K-1] must be 1, every
+   * width divides the one below it, 1 <= k <= K). Each level-1 segment of
+   * len / tree[0] elements is buffered on chip and evaluated non-incrementally
+   * with its own dependency values (fused_level1_segment, :430-457); the
+   * segment partials are then corrected and folded in segment order (the
+   * group combines of levels 2..k, :461-481, and the bridge to the final
+   * dependency values, :510-536, are one closed-form fold — equal in exact
+   * arithmetic). A segment longer than the pattern's on-chip buffer is
+   * RF_ERR_UNSUPPORTED, as non-incremental fusion is only feasible for short
+   * segments. `segments` must be 1. (ABI v5) */
+  int32_t fuse_level;
+  int32_t tree_depth;   /* K, 1..8 */
+  int64_t tree[8];
 } rf_desc;
 
 /* Device buffers for one rf_run. Inputs by pattern:

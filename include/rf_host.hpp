@@ -903,16 +903,31 @@ inline long long round_up(long long x, long long m) { return (x + m - 1) / m * m
 // The fused loop's counters: every input element loaded once
 // (acceptance crit 6), root dependency reads once per corrected reduction at
 // finalize (crit 7, simulator.cpp:617), O(1) auxiliary state per level (crit 8).
-inline void fill_counters(const Program& prog, const TreeConfig& cfg, ExecReport& r) {
+// run_fused (fuse_level k >= 1, simulator.cpp:485-559): inputs are still
+// loaded once (the level-1 buffer), but every corrected reduction reads its
+// final dependencies once per level-k partial (the bridge, :522-525), the
+// level-1 buffer holds a segment's input lanes (:548-550) and levels 2..k keep
+// a group of child states (:551-556).
+inline void fill_counters(const Program& prog, const TreeConfig& cfg, ExecReport& r, int fuse_level = 0) {
   long long arity = 0;
   for (const auto& red : prog.spec.reductions) arity += red.op == "topk" ? 2LL * red.topk : red.free_len;
-  for (const auto& in : prog.spec.inputs) r.input_loads[in.name] = in.len * std::max(1LL, in.free_len);
+  long long lanes = 0;
+  for (const auto& in : prog.spec.inputs) {
+    r.input_loads[in.name] = in.len * std::max(1LL, in.free_len);
+    lanes += std::max(1LL, in.free_len);
+  }
+  const long long root_reads = fuse_level > 0 ? cfg.levels[static_cast<std::size_t>(fuse_level)] : 1;
   for (const auto& red : prog.spec.reductions) {
     std::set<int> ds;
     deps_of(red.body, ds);
-    for (int d : ds) r.dep_root_loads[d] += 1;
+    for (int d : ds) r.dep_root_loads[d] += root_reads;
   }
   for (int m = 1; m <= cfg.depth(); ++m) r.peak_aux_slots[m] = arity;
+  if (fuse_level > 0) {
+    r.peak_aux_slots[1] = cfg.levels[0] / cfg.levels[1] * lanes + arity;
+    for (int m = 2; m <= fuse_level; ++m)
+      r.peak_aux_slots[m] = (cfg.levels[static_cast<std::size_t>(m) - 1] / cfg.levels[static_cast<std::size_t>(m)] + 1) * arity;
+  }
 }
 
 // One host-side operand of a batched run: R rows of [len(, free)] values,
@@ -980,7 +995,8 @@ namespace detail {
 // sequence (rf_run_host), one ExecReport per row with the reference's field
 // meanings. Single-row run_incremental / run_multisegment are R = 1.
 inline std::vector<ExecReport> execute_batched(const Program& prog, const TreeConfig& cfg, long long segments,
-                                               const BatchedStore& st, const std::string& strategy) {
+                                               const BatchedStore& st, const std::string& strategy,
+                                               int fuse_level = 0) {
   // validate_tree (cascade.cpp:37-66) + store shapes (simulator.cpp:235-245)
   if (cfg.levels.size() < 2 || cfg.levels.front() != prog.L0 || cfg.levels.back() != 1)
     throw ShapeMismatch("BadTree: levels must run from L0 = " + std::to_string(prog.L0) + " to 1");
@@ -995,6 +1011,20 @@ inline std::vector<ExecReport> execute_batched(const Program& prog, const TreeCo
   if (segments < 1 || prog.L0 % segments != 0)  // simulator.cpp:668-671
     throw IncompatibleSegmentation(std::to_string(segments) + " segments do not divide L0 = " +
                                    std::to_string(prog.L0));
+  if (fuse_level != 0 && (fuse_level < 1 || fuse_level > cfg.depth()))  // simulator.cpp:491-493
+    throw std::out_of_range("fuse level out of range");
+  // run_fused: hand the tree to the plan (rf_desc.fuse_level / tree, ABI v5);
+  // the kernel evaluates each level-1 segment non-incrementally.
+  auto fuse = [&](rf_desc& d) {
+    if (fuse_level == 0) return;
+    if (d.len != prog.L0)
+      throw NotFusable("run_fused: the level-1 segments must be whole kernel K tiles (L0 = " +
+                       std::to_string(prog.L0) + ")");
+    d.segments = 1;
+    d.fuse_level = fuse_level;
+    d.tree_depth = cfg.depth();
+    for (int i = 0; i < cfg.depth() && i < 8; ++i) d.tree[i] = cfg.levels[static_cast<std::size_t>(i) + 1];
+  };
   const long long R = st.rows();
   std::vector<ExecReport> reps(R);
   for (auto& r : reps) r.strategy = strategy;
@@ -1033,6 +1063,7 @@ inline std::vector<ExecReport> execute_batched(const Program& prog, const TreeCo
       d.rows = R;
       d.len = L0;
       d.free_len = K;
+      fuse(d);
       PlanHandle h(d);
       std::vector<float> xf = rows_f(prog.x, R), m(R), t(R);
       std::vector<int32_t> rec(moe ? 2 * K * R : 0);
@@ -1073,6 +1104,7 @@ inline std::vector<ExecReport> execute_batched(const Program& prog, const TreeCo
       d.len = L0;
       d.free_len = D;
       d.segments = segments;
+      fuse(d);
       PlanHandle h(d);
       const auto& P = st.array(prog.x);
       const auto& V = st.array(prog.v);
@@ -1125,6 +1157,7 @@ inline std::vector<ExecReport> execute_batched(const Program& prog, const TreeCo
       d.segments = L0 % (segments * (quant ? 128 : 64)) == 0 ? segments : 1;
       d.fmax = prog.fmax;
       d.eps = prog.eps;
+      fuse(d);
       PlanHandle h(d);
       const double* W = shared_weight(prog.w);
       std::vector<float> wf(Kp * Np, 0.f), gf(Kp, 0.f);
@@ -1187,6 +1220,7 @@ inline std::vector<ExecReport> execute_batched(const Program& prog, const TreeCo
       d.segments = segments;
       d.eps = prog.eps;
       d.offset = prog.offset;
+      fuse(d);
       PlanHandle h(d);
       std::vector<float> xf = rows_f(prog.x, R), yf;
       if (prog.pattern != RF_PATTERN_VARIANCE) yf = rows_f(prog.v, R);
@@ -1207,18 +1241,18 @@ inline std::vector<ExecReport> execute_batched(const Program& prog, const TreeCo
     }
     default: throw NotFusable("unknown pattern");
   }
-  for (auto& r : reps) fill_counters(prog, cfg, r);
+  for (auto& r : reps) fill_counters(prog, cfg, r, fuse_level);
   return reps;
 }
 
 inline ExecReport execute(const Program& prog, const TreeConfig& cfg, long long segments,
-                          TensorStore& st, const std::string& strategy) {
+                          TensorStore& st, const std::string& strategy, int fuse_level = 0) {
   BatchedStore b;
   for (const auto& in : prog.spec.inputs) {
     const auto& a = st.array(in.name);  // ShapeMismatch if absent
     b.define_rows(in.name, 1, a.len, a.free_len, a.data);
   }
-  return execute_batched(prog, cfg, segments, b, strategy).front();
+  return execute_batched(prog, cfg, segments, b, strategy, fuse_level).front();
 }
 
 }  // namespace detail
@@ -1233,6 +1267,15 @@ inline ExecReport run_incremental(const Program& prog, const TreeConfig& cfg, Te
 inline ExecReport run_multisegment(const Program& prog, const TreeConfig& cfg, long long num_segments,
                                    TensorStore& store) {
   return detail::execute(prog, cfg, num_segments, store, "multi:" + std::to_string(num_segments));
+}
+
+// run_fused (simulator.hpp, simulator.cpp:485-559): fusion at level k, the
+// non-incremental executor. Each level-1 segment (L0 / levels[1] elements) is
+// buffered on chip and evaluated with its own dependency values, then the
+// segment states are corrected and folded in segment order. A segment longer
+// than the kernel's on-chip buffer raises NotFusable.
+inline ExecReport run_fused(const Program& prog, const TreeConfig& cfg, int fuse_level, TensorStore& store) {
+  return detail::execute(prog, cfg, 1, store, "fused:k=" + std::to_string(fuse_level), fuse_level);
 }
 
 // The batched executors: every row of the store in one run, one ExecReport

@@ -46,7 +46,7 @@ ExecReport to_reference(const rfcuda::ExecReport& r) {
 }
 
 ExecReport run(const FusedProgram& prog, const TreeConfig& cfg, long long segments,
-               TensorStore& store) {
+               TensorStore& store, int fuse_level = 0) {
   rfcuda::Program p = plan_checked(prog);
   rfcuda::TensorStore st;
   for (const auto& in : prog.spec.inputs) {
@@ -55,8 +55,9 @@ ExecReport run(const FusedProgram& prog, const TreeConfig& cfg, long long segmen
   }
   rfcuda::ExecReport r;
   try {
-    r = segments == 1 ? rfcuda::run_incremental(p, rfcuda::TreeConfig{cfg.levels}, st)
-                      : rfcuda::run_multisegment(p, rfcuda::TreeConfig{cfg.levels}, segments, st);
+    r = fuse_level > 0 ? rfcuda::run_fused(p, rfcuda::TreeConfig{cfg.levels}, fuse_level, st)
+        : segments == 1 ? rfcuda::run_incremental(p, rfcuda::TreeConfig{cfg.levels}, st)
+                        : rfcuda::run_multisegment(p, rfcuda::TreeConfig{cfg.levels}, segments, st);
   } catch (const rfcuda::ShapeMismatch& e) {
     throw ShapeMismatch(e.what());
   } catch (const rfcuda::IncompatibleSegmentation& e) {
@@ -138,6 +139,11 @@ ExecReport run_cuda(const FusedProgram& prog, const TreeConfig& cfg, TensorStore
 ExecReport run_cuda_multisegment(const FusedProgram& prog, const TreeConfig& cfg,
                                  long long num_segments, TensorStore& store) {
   return run(prog, cfg, num_segments, store);
+}
+
+ExecReport run_cuda_fused(const FusedProgram& prog, const TreeConfig& cfg, int fuse_level,
+                          TensorStore& store) {
+  return run(prog, cfg, 1, store, fuse_level);
 }
 
 }  // namespace redfuse

@@ -18,6 +18,12 @@ namespace redfuse {
 ExecReport run_cuda(const FusedProgram& prog, const TreeConfig& cfg, TensorStore& store);
 ExecReport run_cuda_multisegment(const FusedProgram& prog, const TreeConfig& cfg,
                                  long long num_segments, TensorStore& store);
+// Same contract as run_fused (simulator.cpp:485-559): fusion at level k, the
+// level-1 segments evaluated non-incrementally on chip. NotFusable when a
+// segment exceeds the kernel's on-chip buffer;
+// std::out_of_range for k outside 1..depth, as the reference.
+ExecReport run_cuda_fused(const FusedProgram& prog, const TreeConfig& cfg, int fuse_level,
+                          TensorStore& store);
 
 // Batched drop-in (the rows axis the reference only has as scalar_ir's
 // EmitStrategy.rows, scalar_ir.hpp:77): R cascade rows — one TensorStore

@@ -10,7 +10,7 @@
 //                  [--modes m1,m2,..] [--json] [--out PATH]
 //
 // Modes: unfused, fused@k, incremental, multi:S (the reference's executors)
-// and cuda, cuda-multi:S (librf_cuda through redfuse::run_cuda*). Every mode is
+// and cuda, cuda-multi:S, cuda-fused@k (librf_cuda through redfuse::run_cuda*). Every mode is
 // compared with the workload oracle by the reference's compare_reports.
 // The cuda gate: fp32 patterns use max scaled error <= max(tol, 1e-5) (the
 // north_star's fp32 bound); bf16/e4m3-operand patterns are compared against
@@ -159,6 +159,7 @@ struct Mode {
   std::string name;
   bool cuda = false;
   long long segments = 1;
+  int fuse = 0;  // cuda-fused@k: run_cuda_fused at level k
   double max_rel = 0.0, rms_rel = 0.0;
   bool pass = true;
   std::string worst, note;
@@ -211,6 +212,11 @@ int verify(const Args& a) {
     Mode md;
     md.name = m;
     if (m == "cuda") md.cuda = true;
+    else if (m.rfind("cuda-fused@", 0) == 0) {
+      md.cuda = true;
+      md.fuse = std::atoi(m.c_str() + 11);
+      if (md.fuse < 1 || md.fuse > tree.depth()) throw Usage("cuda-fused@k: k must lie in 1.." + std::to_string(tree.depth()));
+    }
     else if (m.rfind("cuda-multi:", 0) == 0) md.cuda = true, md.segments = segments_of(m, "cuda-multi:");
     else if (m.rfind("multi:", 0) == 0) md.segments = segments_of(m, "multi:");
     else if (m != "unfused" && m != "incremental" && m.rfind("fused@", 0) != 0)
@@ -245,12 +251,13 @@ int verify(const Args& a) {
       const auto t0 = std::chrono::steady_clock::now();
       if (md.cuda) {
         try {
-          got = md.segments > 1 ? run_cuda_multisegment(prog, tree, md.segments, st)
-                                : run_cuda(prog, tree, st);
+          got = md.fuse > 0 ? run_cuda_fused(prog, tree, md.fuse, st)
+                : md.segments > 1 ? run_cuda_multisegment(prog, tree, md.segments, st)
+                                  : run_cuda(prog, tree, st);
         } catch (const NotFusable& e) {
           md.pass = false;
           md.note = std::string("no librf_cuda kernel: ") + e.what();
-          no_kernel = e.what();
+          if (md.fuse == 0) no_kernel = e.what();  // a too-long fused segment is this mode's limit only
           continue;
         }
       } else if (md.name == "unfused") got = run_unfused(w.spec, tree, st);

@@ -63,6 +63,28 @@ static void check_workload(const std::string& name, const Workload& w, double to
   }
 }
 
+// run_fused (fusion at level k, simulator.cpp:485-559) against
+// redfuse::run_cuda_fused at every level of each tree (levels[1..K]).
+static void check_fused(const std::string& name, const Workload& w, double tol,
+                        std::initializer_list<std::vector<long long>> trees, int seeds) {
+  FusedProgram prog = derive_fused(w.spec);
+  const long long l0 = w.spec.axis_len();
+  for (int seed = 100; seed < 100 + seeds; ++seed)
+    for (const auto& t : trees) {
+      std::vector<long long> levels{l0};
+      std::string tag;
+      for (long long x : t) {
+        levels.push_back(x);
+        tag += "-" + std::to_string(x);
+      }
+      for (int k = 1; k <= static_cast<int>(t.size()); ++k) {
+        TensorStore a = w.generate(seed), b = w.generate(seed);
+        report(name + "/s" + std::to_string(seed) + "/tree" + tag, "fused@" + std::to_string(k),
+               run_fused(prog, TreeConfig{levels}, k, a), run_cuda_fused(prog, TreeConfig{levels}, k, b), tol);
+      }
+    }
+}
+
 // A DSL cascade with uniform(-1, 1) inputs (the reference CLI's generator).
 Workload dsl_workload(const std::string& name, const std::string& dsl) {
   CascadeSpec spec = parse_cascade(dsl);
@@ -121,6 +143,36 @@ int main() {
   check_workload("variance_8192", builtin("variance"), 1e-5, {2, 8}, 3);
   check_workload("sum_sum_1024", builtin("sum_sum"), 1e-5, {2, 8}, 3);
   check_workload("moment_of_inertia_1024", builtin("moment_of_inertia"), 1e-5, {2, 8}, 3);
+  // run_fused: level-1 segments evaluated non-incrementally on chip
+  check_fused("attention_256x64", make_attention(256, 64), 1e-5, {{4, 1}, {16, 4, 1}, {256, 1}}, 2);
+  check_fused("attention_128x128", make_attention(128, 128), 1e-5, {{2, 1}}, 1);
+  check_fused("safe_softmax_1024", make_safe_softmax(1024), 1e-5, {{32, 4, 1}, {8, 1}, {1}}, 2);
+  check_fused("variance_8192", builtin("variance"), 1e-5, {{16, 4, 1}, {64, 1}}, 2);
+  check_fused("sum_sum_1024", builtin("sum_sum"), 1e-5, {{4, 1}, {32, 8, 1}}, 2);
+  check_fused("quant_gemm_512x256", make_quant_gemm(512, 256), -0.06, {{4, 1}}, 1);
+  check_fused("rmsnorm_gemm_256x48",
+              dsl_workload("rmsnorm_gemm",
+                           "cascade rmsnorm_gemm\ninput x len 256\ninput g len 256\n"
+                           "input w len 256 free 48\nconst INVK = 0.00390625\nconst EPS = 1e-6\n"
+                           "reduce 1 op sum\n    x[l] * x[l]\nreduce 2 op sum free 48\n"
+                           "    x[l] * g[l] / sqrt(d1 * INVK + EPS) * w[l, f]\n"),
+              -0.02, {{4, 1}, {2, 1}}, 1);
+  // a level-1 segment longer than the on-chip buffer: NotFusable (non-incremental
+  // fusion is only feasible for short segments)
+  {
+    Workload w = make_attention(256, 64);
+    FusedProgram prog = derive_fused(w.spec);
+    bool threw = false;
+    try {
+      TensorStore st = w.generate(1);
+      run_cuda_fused(prog, TreeConfig{{256, 2, 1}}, 1, st);  // 128-key segments > the 64-key fp32 tile
+    } catch (const NotFusable&) {
+      threw = true;
+    }
+    if (!threw) ++failures;
+    std::printf("{\"case\": \"attention_256x64/tree-2-1\", \"mode\": \"fused-too-long\", \"not_fusable\": %s}\n",
+                threw ? "true" : "false");
+  }
   // a cascade with no kernel: NotFusable from the binding (no CPU fallback)
   {
     Workload w = dsl_workload("prod_chain", "cascade prod_chain\ninput x len 64\n"

@@ -168,9 +168,29 @@ std::string ln_dsl(long long k, long long n, double eps) {
   return os.str();
 }
 
+// run_fused (simulator.cpp:485-559) at every level k of each tree; a tree
+// lists TreeConfig.levels[1..K] (L0 is prepended). Report "fused_<w1>-..-<wK>_k<k>".
+template <class Gen>
+void add_fused(Case& c, const FusedProgram& prog, long long l0, Gen gen,
+               const std::vector<std::vector<long long>>& trees) {
+  for (const auto& t : trees) {
+    std::vector<long long> levels{l0};
+    std::string tag;
+    for (long long x : t) {
+      levels.push_back(x);
+      tag += (tag.empty() ? "" : "-") + std::to_string(x);
+    }
+    for (int k = 1; k <= static_cast<int>(t.size()); ++k) {
+      TensorStore s2 = gen();
+      add_report(c, "fused_" + tag + "_k" + std::to_string(k), run_fused(prog, TreeConfig{levels}, k, s2));
+    }
+  }
+}
+
 void golden_workload(const std::string& dir, const std::string& name,
                      const Workload& w, std::uint64_t seed,
-                     const std::vector<long long>& segs) {
+                     const std::vector<long long>& segs,
+                     const std::vector<std::vector<long long>>& trees = {}) {
   FusedProgram prog = derive_fused(w.spec);
   long long l0 = w.spec.axis_len();
   Case c;
@@ -190,26 +210,27 @@ void golden_workload(const std::string& dir, const std::string& name,
     add_report(c, "multi" + std::to_string(s),
                run_multisegment(prog, TreeConfig{{l0, 1}}, s, s2));
   }
+  add_fused(c, prog, l0, [&] { return w.generate(seed); }, trees);
   c.write(dir);
 }
 
 int cmd_golden(const std::string& dir) {
   for (std::uint64_t seed : {100ull, 101ull})
     golden_workload(dir, "attention_256x64_s" + std::to_string(seed),
-                    make_attention(256, 64), seed, {2, 4, 8});
-  golden_workload(dir, "attention_128x128_s7", make_attention(128, 128), 7, {2, 4});
+                    make_attention(256, 64), seed, {2, 4, 8}, {{4, 1}, {16, 4, 1}});
+  golden_workload(dir, "attention_128x128_s7", make_attention(128, 128), 7, {2, 4}, {{2, 1}});
   for (std::uint64_t seed = 100; seed < 105; ++seed)
     golden_workload(dir, "safe_softmax_1024_s" + std::to_string(seed),
-                    make_safe_softmax(1024), seed, {2, 4, 8});
+                    make_safe_softmax(1024), seed, {2, 4, 8}, {{32, 4, 1}, {8, 1}});
   golden_workload(dir, "quant_gemm_512x256_s100", make_quant_gemm(512, 256), 100,
-                  {2, 4, 8});
+                  {2, 4, 8}, {{4, 1}});
   for (std::uint64_t seed = 100; seed < 103; ++seed)
     golden_workload(dir, "quant_gemm_64x32_s" + std::to_string(seed),
                     make_quant_gemm(64, 32), seed, {2, 4, 8});
-  golden_workload(dir, "variance_8192_s100", make_variance(8192), 100, {2, 8});
-  golden_workload(dir, "sum_sum_1024_s100", make_sum_sum(1024), 100, {2, 8});
-  golden_workload(dir, "sum_sum_1024_s101", make_sum_sum(1024), 101, {2, 8});
-  golden_workload(dir, "variance_8192_s101", make_variance(8192), 101, {2, 8});
+  golden_workload(dir, "variance_8192_s100", make_variance(8192), 100, {2, 8}, {{16, 4, 1}});
+  golden_workload(dir, "sum_sum_1024_s100", make_sum_sum(1024), 100, {2, 8}, {{4, 1}, {32, 8, 1}});
+  golden_workload(dir, "sum_sum_1024_s101", make_sum_sum(1024), 101, {2, 8}, {{4, 1}});
+  golden_workload(dir, "variance_8192_s101", make_variance(8192), 101, {2, 8}, {{16, 4, 1}});
   golden_workload(dir, "moment_of_inertia_1024_s100", builtin("moment_of_inertia"), 100, {2, 8});
   golden_workload(dir, "moe_routing_128x8_s100", make_moe_routing(128, 8), 100, {2, 4});
 
@@ -252,6 +273,9 @@ int cmd_golden(const std::string& dir) {
       add_report(c, "multi" + std::to_string(s),
                  run_multisegment(prog, TreeConfig{{k, 1}}, s, s2));
     }
+    add_fused(c, prog, k, [&] { return dsl_inputs(spec, seed); },
+              k == 256 ? std::vector<std::vector<long long>>{{4, 1}, {2, 1}}
+                       : std::vector<std::vector<long long>>{{1}});
     c.write(dir);
   }
 

@@ -508,6 +508,102 @@ void rfo_moe_routing(const double* s, int64_t rows, int64_t experts, int64_t k,
 
 /* -------------------------------------------------------------- parity --- */
 
+/* ---------------------------------------------------------- run_fused --- */
+
+/* One partial state: d1, d2 scalars and d3 [hd] (attention). */
+typedef struct {
+  double d1, d2;
+  double* d3;
+} fstate;
+
+/* Correction of reduction idx (2 or 3) from the child's dependency values to
+ * the target's: retarget_factor (simulator.cpp:278-318) for each pattern's H. */
+static double fused_factor(int pattern, int idx, const fstate* from, double t1, double t2, double c,
+                           double eps) {
+  switch (pattern) {
+    case 1: return exp(from->d1 - t1);                                   /* e^(d1'-d1) */
+    case 2: return idx == 2 ? exp(from->d1 - t1) : exp(from->d1 - t1) * from->d2 / t2;
+    case 8: return sqrt(fmax(from->d1 - c, eps)) / sqrt(fmax(t1 - c, eps));
+    default: return 1.0; /* variance: no dependency */
+  }
+}
+
+int rfo_fused_row(int pattern, const double* a, const double* b, int64_t hd, const int64_t* levels,
+                  int depth, int k, double c, double eps, double* d1, double* d2, double* d3) {
+  if (depth < 1 || k < 1 || k > depth || levels[depth] != 1) return -1;
+  for (int m = 1; m <= depth; ++m)
+    if (levels[m] < 1 || levels[m - 1] % levels[m]) return -1;
+  const int64_t n1 = levels[1], seg = levels[0] / n1;
+  const int att = pattern == 2;
+  fstate* cur = calloc((size_t)n1, sizeof(fstate));
+  double* o1 = att ? calloc((size_t)(n1 * hd), sizeof(double)) : NULL;
+  /* level 1: buffered segments, reductions in dependency order */
+  for (int64_t j = 0; j < n1; ++j) {
+    const double* x = a + j * seg;
+    fstate* s = &cur[j];
+    s->d3 = att ? o1 + j * hd : NULL;
+    if (pattern == 1 || att) {
+      s->d1 = -INFINITY;
+      for (int64_t l = 0; l < seg; ++l) s->d1 = fmax(s->d1, x[l]);
+      for (int64_t l = 0; l < seg; ++l) s->d2 += exp(x[l] - s->d1);
+      if (att)
+        for (int64_t l = 0; l < seg; ++l) {
+          const double w = exp(x[l] - s->d1) / s->d2;
+          for (int64_t f = 0; f < hd; ++f) s->d3[f] += w * b[(j * seg + l) * hd + f];
+        }
+    } else if (pattern == 7) {
+      for (int64_t l = 0; l < seg; ++l) s->d1 += x[l];
+      for (int64_t l = 0; l < seg; ++l) s->d2 += x[l] * x[l];
+    } else {
+      for (int64_t l = 0; l < seg; ++l) s->d1 += x[l] * x[l];
+      const double h = sqrt(fmax(s->d1 - c, eps));
+      for (int64_t l = 0; l < seg; ++l) s->d2 += x[l] * b[j * seg + l] / h;
+    }
+  }
+  /* levels 2..k: group combines, children corrected to the group's values */
+  int64_t width = n1;
+  for (int m = 2; m <= k; ++m) {
+    const int64_t w2 = levels[m], group = width / w2;
+    for (int64_t j = 0; j < w2; ++j) {
+      fstate g = {(pattern == 1 || att) ? -INFINITY : 0.0, 0.0, NULL};
+      double og[hd > 0 ? hd : 1];
+      memset(og, 0, sizeof og);
+      for (int64_t q = 0; q < group; ++q) { /* reduction 1: plain */
+        const fstate* ch = &cur[j * group + q];
+        g.d1 = (pattern == 1 || att) ? fmax(g.d1, ch->d1) : g.d1 + ch->d1;
+      }
+      for (int64_t q = 0; q < group; ++q) /* reduction 2: corrected to g.d1 */
+        g.d2 += cur[j * group + q].d2 * fused_factor(pattern, 2, &cur[j * group + q], g.d1, 0, c, eps);
+      if (att)
+        for (int64_t q = 0; q < group; ++q) { /* reduction 3: corrected to (g.d1, g.d2) */
+          const fstate* ch = &cur[j * group + q];
+          const double f = fused_factor(pattern, 3, ch, g.d1, g.d2, c, eps);
+          for (int64_t e = 0; e < hd; ++e) og[e] += ch->d3[e] * f;
+        }
+      cur[j].d1 = g.d1;
+      cur[j].d2 = g.d2;
+      if (att) memcpy(cur[j].d3, og, sizeof(double) * (size_t)hd);
+    }
+    width = w2;
+  }
+  /* bridge + plain fold above level k, reduction by reduction */
+  double f1 = (pattern == 1 || att) ? -INFINITY : 0.0, f2 = 0.0;
+  for (int64_t j = 0; j < width; ++j) f1 = (pattern == 1 || att) ? fmax(f1, cur[j].d1) : f1 + cur[j].d1;
+  for (int64_t j = 0; j < width; ++j) f2 += cur[j].d2 * fused_factor(pattern, 2, &cur[j], f1, 0, c, eps);
+  *d1 = f1;
+  *d2 = f2;
+  if (att) {
+    for (int64_t e = 0; e < hd; ++e) d3[e] = 0.0;
+    for (int64_t j = 0; j < width; ++j) {
+      const double f = fused_factor(pattern, 3, &cur[j], f1, f2, c, eps);
+      for (int64_t e = 0; e < hd; ++e) d3[e] += cur[j].d3[e] * f;
+    }
+  }
+  free(o1);
+  free(cur);
+  return 0;
+}
+
 double rfo_scaled_max_err(const double* x, const double* y, int64_t n, int64_t* worst) {
   double mx = 0.0;
   int64_t wi = -1;

@@ -132,6 +132,19 @@ void rfo_moments(const double* mass, const double* pos, int64_t rows, int64_t n,
 void rfo_moe_routing(const double* s, int64_t rows, int64_t experts, int64_t k,
                      double* d1, double* d2, double* topk_val, int64_t* topk_idx);
 
+/* ---- run_fused: fusion at level k (simulator.cpp:485-559) ----------------
+ * The non-incremental executor on one row: the L0 elements are cut into
+ * levels[1] level-1 segments, each evaluated with its OWN dependency values
+ * (fused_level1_segment, :430-457); levels 2..k combine groups of children
+ * corrected to the group's dependency values (fused_combine_group, :461-481);
+ * the level-k partials are retargeted to the final values (the bridge,
+ * :510-536) and folded plainly over levels k+1..K. levels[0] = L0,
+ * levels[depth] = 1. pattern: 1 safe_softmax (a = x), 2 attention (a = P,
+ * b = V [L0, hd]; d3 [hd]), 7 variance (a = x), 8 sum_sum (a = x1, b = x2,
+ * c, eps). Returns -1 on a bad tree / level.                                  */
+int rfo_fused_row(int pattern, const double* a, const double* b, int64_t hd, const int64_t* levels,
+                  int depth, int k, double c, double eps, double* d1, double* d2, double* d3);
+
 /* ---- parity metric (compare_reports, simulator.cpp:691-752) --------------- */
 /* max over i of |x-y|/(1+max(|x|,|y|)); equal values (incl. matching infs)
  * count 0; NaN/inf mismatch is +inf. Returns the max, writes its index.     */

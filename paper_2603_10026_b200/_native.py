@@ -36,7 +36,7 @@ RF_PATTERN_MOMENTS = 9
 RF_PATTERN_MOE_ROUTER = 10
 RF_PATTERN_MLA_DECODE = 11
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 # rf_dtype
 RF_F32 = 0
@@ -63,6 +63,9 @@ class rf_desc(ctypes.Structure):
         ("device", ctypes.c_int32),
         ("producer_len", ctypes.c_int32),
         ("stat_len", ctypes.c_int64),
+        ("fuse_level", ctypes.c_int32),
+        ("tree_depth", ctypes.c_int32),
+        ("tree", ctypes.c_int64 * 8),
     ]
 
 

@@ -171,6 +171,7 @@ const char* kernel_name(rf::Kernel k) {
     case rf::Kernel::RowStats: return "rowstats (SIMT HBM streaming, fp64 accumulation)";
     case rf::Kernel::MoeRouter: return "moe_router (tcgen05 split-K router GEMM + routing cascade)";
     case rf::Kernel::MlaDecode: return "mla_decode (tcgen05, 128 heads x latent cache, split-KV)";
+    case rf::Kernel::FusedRows: return "fused_rows (run_fused: warp-buffered level-1 segments, SIMT)";
   }
   return "?";
 }
@@ -269,6 +270,16 @@ rf_status gemm_run(const rf_plan* p, const rf_io* io, int64_t m0, int64_t nm, cu
 }
 
 rf_status run_range(const rf_plan* p, const rf_io* io, int64_t u0, int64_t nu, cudaStream_t st) {
+  if (p->kernel == rf::Kernel::FusedRows) {  // run_fused on the row patterns
+    const rf_desc& d = p->d;
+    cudaError_t e = rf::launch_fused_rows(
+        d.pattern, static_cast<const float*>(io->in[0]) + u0 * d.len,
+        d.pattern == RF_PATTERN_SUM_SUM ? static_cast<const float*>(io->in[1]) + u0 * d.len : nullptr, nu,
+        d.len, d.tree[0], d.offset, d.eps, static_cast<float*>(io->d[0]) + u0,
+        static_cast<float*>(io->d[1]) + u0, st);
+    if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("fused_rows launch: ") + cudaGetErrorString(e));
+    return RF_OK;
+  }
   switch (p->d.pattern) {
     case RF_PATTERN_SAFE_SOFTMAX: {
       cudaError_t e = rf::launch_softmax_rows(
@@ -394,6 +405,23 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
   if (d.segments < 1 || d.len % d.segments != 0)  // simulator.cpp:668-671
     return fail(RF_ERR_SEGMENTATION, std::to_string(d.segments) +
                                          " segments do not divide L0 = " + std::to_string(d.len));
+  // run_fused: the reduction tree (validate_tree, cascade.cpp:37-66) and the
+  // fuse level (simulator.cpp:491-493)
+  int64_t fused_seg = 0;
+  if (d.fuse_level != 0) {
+    if (d.segments != 1) return fail(RF_ERR_ARG, "run_fused: segments must be 1 (the tree gives the segments)");
+    if (d.tree_depth < 1 || d.tree_depth > 8) return fail(RF_ERR_SHAPE, "BadTree: depth must be 1..8");
+    int64_t below = d.len;
+    for (int i = 0; i < d.tree_depth; ++i) {
+      if (d.tree[i] < 1 || below % d.tree[i] != 0)
+        return fail(RF_ERR_SHAPE, "BadTree: level widths must divide the level below");
+      below = d.tree[i];
+    }
+    if (below != 1) return fail(RF_ERR_SHAPE, "BadTree: the last level must be 1");
+    if (d.fuse_level < 1 || d.fuse_level > d.tree_depth)
+      return fail(RF_ERR_ARG, "fuse level out of range");
+    fused_seg = d.len / d.tree[0];
+  }
   rf_plan* p = new (std::nothrow) rf_plan();
   if (!p) return fail(RF_ERR_CUDA, "out of host memory");
   p->d = d;
@@ -418,6 +446,74 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
   DeviceGuard guard(d.device);
 
   // ---- kernel choice ----
+  if (fused_seg > 0) {
+    // run_fused: every level-1 segment must fit the pattern's on-chip buffer
+    // (non-incremental evaluation); the segments then run
+    // as the kernel's slices and fold in segment order.
+    const int64_t L1 = d.tree[0];
+    auto too_long = [&](int64_t cap, const char* what) {
+      return bail(RF_ERR_UNSUPPORTED, "run_fused: level-1 segment of " + std::to_string(fused_seg) +
+                                          " elements exceeds the on-chip buffer (" + what + ": " +
+                                          std::to_string(cap) + ")");
+    };
+    switch (d.pattern) {
+      case RF_PATTERN_SAFE_SOFTMAX:
+      case RF_PATTERN_VARIANCE:
+      case RF_PATTERN_SUM_SUM:
+        if (d.dtype != RF_F32) return bail(RF_ERR_UNSUPPORTED, "run_fused rows: f32 inputs");
+        if (d.pattern == RF_PATTERN_SUM_SUM && !(d.eps > 0.0))
+          return bail(RF_ERR_ARG, "sum_sum: eps must be > 0 (max(d1 - c, eps) is the H guard)");
+        if (fused_seg > rf::kSegMax) return too_long(rf::kSegMax, "one warp's registers");
+        if (L1 > rf::kFusedSegsMax)
+          return bail(RF_ERR_UNSUPPORTED, "run_fused rows: more than 8192 level-1 segments per row");
+        p->kernel = rf::Kernel::FusedRows;
+        p->rows_total = d.rows;
+        break;
+      case RF_PATTERN_ATTENTION:
+        // one KV tile per segment: the tile's row max is reduced before any
+        // exponential, so the segment is evaluated non-incrementally
+        if (d.dtype == RF_BF16 && d.rows > 1) {
+          if (fused_seg != 128 || !rf::attention_sm100_supports(d.rows, d.len, d.free_len, L1))
+            return bail(RF_ERR_UNSUPPORTED, "run_fused bf16 attention: segments of exactly one 128-key "
+                                            "tcgen05 tile, Sq % 256 == 0");
+          p->kernel = rf::Kernel::AttentionSm100;
+        } else if (d.dtype == RF_F32) {
+          if (fused_seg > 64) return too_long(64, "one 64-key fp32 tile");
+          if (d.free_len != 16 && d.free_len != 32 && d.free_len != 64 && d.free_len != 128)
+            return bail(RF_ERR_UNSUPPORTED, "attention: head_dim must be 16/32/64/128");
+          p->kernel = rf::Kernel::AttentionF32;
+        } else {
+          return bail(RF_ERR_UNSUPPORTED, "run_fused attention: f32, or bf16 prefill (Sq % 256 == 0)");
+        }
+        p->rows_total = d.batch * d.heads * d.rows;
+        p->nsplit = L1;
+        p->d.segments = L1;
+        break;
+      case RF_PATTERN_QUANT_GEMM_E4M3:
+      case RF_PATTERN_RMSNORM_GEMM:
+      case RF_PATTERN_LAYERNORM_GEMM: {
+        // quant: one 128-wide K tile per segment (its absmax is taken before
+        // any element is quantised); rms / layernorm: the accumulator carries
+        // H' = 1 and the segment's 1/sigma is applied once to the segment's
+        // sum, which is the non-incremental form for any segment length.
+        const bool quant = d.pattern == RF_PATTERN_QUANT_GEMM_E4M3;
+        if (d.dtype != RF_BF16) return bail(RF_ERR_UNSUPPORTED, "GEMM patterns take bf16 activations");
+        if (!rf::gemm_sm100_supports(d.pattern, d.rows, d.free_len, d.len))
+          return bail(RF_ERR_UNSUPPORTED, "GEMM shape has no tcgen05 tiling");
+        if (quant ? fused_seg != 128 : fused_seg % 64 != 0)
+          return bail(RF_ERR_UNSUPPORTED, quant ? "run_fused quant: segments of exactly one 128-wide K tile"
+                                                : "run_fused rms / layernorm: segments of whole 64-wide K tiles");
+        p->kernel = quant ? rf::Kernel::QuantGemmSm100
+                    : d.pattern == RF_PATTERN_LAYERNORM_GEMM ? rf::Kernel::LayerNormGemmSm100
+                                                             : rf::Kernel::RmsGemmSm100;
+        p->rows_total = d.rows;
+        p->d.segments = L1;
+        break;
+      }
+      default:
+        return bail(RF_ERR_UNSUPPORTED, "run_fused: no non-incremental kernel for this pattern");
+    }
+  } else
   switch (d.pattern) {
     case RF_PATTERN_SAFE_SOFTMAX:
       if (d.dtype != RF_F32) return bail(RF_ERR_UNSUPPORTED, "safe_softmax: f32 input only");
@@ -512,7 +608,7 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
     default:
       return bail(RF_ERR_UNSUPPORTED, "unknown pattern");
   }
-  if (is_gemm(p->d.pattern) && p->d.pattern != RF_PATTERN_MOE_ROUTER) p->nsplit = d.segments;
+  if (is_gemm(p->d.pattern) && p->d.pattern != RF_PATTERN_MOE_ROUTER) p->nsplit = p->d.segments;
   p->launches = (((p->d.pattern == RF_PATTERN_ATTENTION || p->d.pattern == RF_PATTERN_MLA_DECODE) &&
                   p->nsplit > 1) ||
                  p->d.pattern == RF_PATTERN_MOE_ROUTER ||
@@ -526,7 +622,7 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
     const size_t n = static_cast<size_t>(p->nsplit) * p->rows_total;
     if (cudaMalloc(&p->ws_m, n * sizeof(float)) != cudaSuccess ||
         cudaMalloc(&p->ws_l, n * sizeof(float)) != cudaSuccess ||
-        cudaMalloc(&p->ws_o, n * d.free_len * sizeof(float)) != cudaSuccess)
+        cudaMalloc(&p->ws_o, n * p->d.free_len * sizeof(float)) != cudaSuccess)
       return bail(RF_ERR_CUDA, "segment workspace allocation failed");
   }
   if (is_gemm(p->d.pattern) && p->d.pattern != RF_PATTERN_MOE_ROUTER && p->nsplit > 1) {
@@ -546,10 +642,10 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
   std::snprintf(buf, sizeof buf,
                 "{\"kernel\": \"%s\", \"pattern\": %d, \"dtype\": %d, \"rows_total\": %lld, "
                 "\"L0\": %lld, \"free\": %lld, \"segments\": %lld, \"slices_launched\": %lld, "
-                "\"launches_per_run\": %lld, \"device\": \"%s\"}",
+                "\"launches_per_run\": %lld, \"fuse_level\": %d, \"device\": \"%s\"}",
                 kernel_name(p->kernel), d.pattern, d.dtype, (long long)p->rows_total,
-                (long long)d.len, (long long)d.free_len, (long long)d.segments,
-                (long long)p->nsplit, (long long)p->launches, prop.name);
+                (long long)d.len, (long long)d.free_len, (long long)p->d.segments,
+                (long long)p->nsplit, (long long)p->launches, d.fuse_level, prop.name);
   p->describe = buf;
   *out = p;
   return RF_OK;

@@ -35,7 +35,16 @@ enum class Kernel {
   RowStats,           // rowstats.cu (variance / sum_sum / moments: HBM streaming)
   MoeRouter,          // router.cu (tcgen05 split-K router GEMM + routing cascade)
   MlaDecode,          // mla.cu (tcgen05 MLA decode, 128 heads share the latent cache)
+  FusedRows,          // fused_seg.cu (run_fused: non-incremental level-1 segments, row patterns)
 };
+
+// run_fused (fused_seg.cu): on-chip buffer of one level-1 segment (one warp's
+// registers) and the most segment partial states one CTA keeps in shared memory.
+constexpr int64_t kSegMax = 1024;
+constexpr int64_t kFusedSegsMax = 8192;
+cudaError_t launch_fused_rows(int pattern, const float* a, const float* b, int64_t rows, int64_t n,
+                              int64_t nseg, double c, double eps, float* d1, float* d2,
+                              cudaStream_t st);
 
 // MoE router (router.cu): scores = X W^T-packed, then the routing cascade.
 struct RouterArgs {

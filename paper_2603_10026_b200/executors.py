@@ -95,6 +95,10 @@ class Desc:
     device: int = 0
     producer_len: int = 0  # MOE_ROUTER: hd (the router GEMM's reduce axis)
     stat_len: int = 0  # RMSNORM / LAYERNORM: K of the statistics' means (0 = len)
+    # run_fused (simulator.cpp:485-559): fusion level k >= 1 over the tree
+    # levels[1..K] (L0 = len implicit); 0 = the incremental executors
+    fuse_level: int = 0
+    tree: tuple = ()
 
     def to_c(self) -> N.rf_desc:
         d = N.rf_desc()
@@ -108,6 +112,10 @@ class Desc:
         d.device = self.device
         d.producer_len = self.producer_len
         d.stat_len = self.stat_len
+        d.fuse_level = self.fuse_level
+        d.tree_depth = len(self.tree)
+        for i, w in enumerate(tuple(self.tree)[:8]):
+            d.tree[i] = int(w)
         return d
 
 
@@ -262,11 +270,14 @@ def _require(cond: bool, msg: str):
         raise ShapeMismatch(msg)
 
 
-def attention(q, k, v, segments: int = 1, softmax_scale: float = 1.0, stream=None):
+def attention(q, k, v, segments: int = 1, softmax_scale: float = 1.0, stream=None,
+              tree: tuple = (), fuse_level: int = 0):
     """Fused safe-softmax -> GEMM attention over every (b, h, query) row.
 
     q: [B,H,Sq,D], k/v: [B,H,Skv,D] (float32 or bfloat16, contiguous, cuda).
     Returns (d1 = m [B,H,Sq] f32, d2 = l [B,H,Sq] f32, d3 = O [B,H,Sq,D]).
+    fuse_level k >= 1 with tree = TreeConfig.levels[1..K]: run_fused
+    (simulator.cpp:485-559), each level-1 segment one on-chip KV tile.
     """
     import torch
 
@@ -279,7 +290,7 @@ def attention(q, k, v, segments: int = 1, softmax_scale: float = 1.0, stream=Non
         raise UnsupportedPattern(f"attention: dtype {q.dtype}")
     p = plan(Desc(N.RF_PATTERN_ATTENTION, dt, rows=Sq, len=k.shape[2], free_len=D, batch=B,
                   heads=H, segments=segments, softmax_scale=softmax_scale,
-                  device=q.device.index or 0), stream)
+                  device=q.device.index or 0, fuse_level=fuse_level, tree=tuple(tree)), stream)
     m = torch.empty((B, H, Sq), dtype=torch.float32, device=q.device)
     l = torch.empty_like(m)
     o = torch.empty_like(q)
@@ -287,13 +298,14 @@ def attention(q, k, v, segments: int = 1, softmax_scale: float = 1.0, stream=Non
     return m, l, o
 
 
-def safe_softmax(x, stream=None):
-    """d1 = max, d2 = sum exp(x - d1) per row of x [rows, n] (float32)."""
+def safe_softmax(x, stream=None, tree: tuple = (), fuse_level: int = 0):
+    """d1 = max, d2 = sum exp(x - d1) per row of x [rows, n] (float32).
+    fuse_level k >= 1 with tree = TreeConfig.levels[1..K]: run_fused."""
     import torch
 
     _require(x.dim() == 2 and x.dtype == torch.float32, "x must be float32 [rows, n]")
     p = plan(Desc(N.RF_PATTERN_SAFE_SOFTMAX, "f32", rows=x.shape[0], len=x.shape[1],
-                  device=x.device.index or 0), stream)
+                  device=x.device.index or 0, fuse_level=fuse_level, tree=tuple(tree)), stream)
     d1 = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
     d2 = torch.empty_like(d1)
     p.run([x.contiguous()], [d1, d2], stream)
@@ -453,28 +465,33 @@ def _rows_f32(name, *ts):
     return [t.contiguous() for t in ts]
 
 
-def variance(x, segments: int = 1, stream=None):
-    """make_variance per row: d1 = sum x, d2 = sum x^2. x: [rows, n] float32."""
+def variance(x, segments: int = 1, stream=None, tree: tuple = (), fuse_level: int = 0):
+    """make_variance per row: d1 = sum x, d2 = sum x^2. x: [rows, n] float32.
+    fuse_level k >= 1 with tree = TreeConfig.levels[1..K]: run_fused."""
     import torch
 
     _require(x.dim() == 2, "x must be [rows, n]")
     (x,) = _rows_f32("variance", x)
     p = plan(Desc(N.RF_PATTERN_VARIANCE, "f32", rows=x.shape[0], len=x.shape[1],
-                  segments=segments, device=x.device.index or 0), stream)
+                  segments=segments, device=x.device.index or 0, fuse_level=fuse_level,
+                  tree=tuple(tree)), stream)
     d1 = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
     d2 = torch.empty_like(d1)
     p.run([x], [d1, d2], stream)
     return d1, d2
 
 
-def sum_sum(x1, x2, offset: float = 10.0, eps: float = 1e-12, segments: int = 1, stream=None):
-    """make_sum_sum per row: d1 = sum x1^2, d2 = sum x1 x2 / sqrt(max(d1 - offset, eps))."""
+def sum_sum(x1, x2, offset: float = 10.0, eps: float = 1e-12, segments: int = 1, stream=None,
+            tree: tuple = (), fuse_level: int = 0):
+    """make_sum_sum per row: d1 = sum x1^2, d2 = sum x1 x2 / sqrt(max(d1 - offset, eps)).
+    fuse_level k >= 1 with tree = TreeConfig.levels[1..K]: run_fused."""
     import torch
 
     _require(x1.dim() == 2 and x1.shape == x2.shape, "x1, x2 must be [rows, n]")
     x1, x2 = _rows_f32("sum_sum", x1, x2)
     p = plan(Desc(N.RF_PATTERN_SUM_SUM, "f32", rows=x1.shape[0], len=x1.shape[1], eps=eps,
-                  offset=offset, segments=segments, device=x1.device.index or 0), stream)
+                  offset=offset, segments=segments, device=x1.device.index or 0,
+                  fuse_level=fuse_level, tree=tuple(tree)), stream)
     d1 = torch.empty(x1.shape[0], dtype=torch.float32, device=x1.device)
     d2 = torch.empty_like(d1)
     p.run([x1, x2], [d1, d2], stream)

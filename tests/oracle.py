@@ -48,6 +48,9 @@ def lib():
             "rfo_layernorm_gemm_incremental": (None, [D, D, D, I, I, ctypes.c_double, D, D, D, D]),
             "rfo_moe_routing": (None, [D, I, I, I, D, D, D, ctypes.POINTER(ctypes.c_int64)]),
             "rfo_scaled_max_err": (ctypes.c_double, [D, D, I, ctypes.POINTER(ctypes.c_int64)]),
+            "rfo_fused_row": (ctypes.c_int, [ctypes.c_int, D, D, I, ctypes.POINTER(ctypes.c_int64),
+                                             ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                             D, D, D]),
         }
         for n, (r, a) in sig.items():
             f = getattr(_lib, n)
@@ -270,6 +273,35 @@ def moe_routing(s, k):
     lib().rfo_moe_routing(_p(s), rows, e, k, _p(d1), _p(d2), _p(tv),
                           ti.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
     return d1, d2, tv, ti
+
+
+FUSED_PATTERNS = {"safe_softmax": 1, "attention": 2, "variance": 7, "sum_sum": 8}
+
+
+def fused(pattern, a, b=None, levels=(), k=1, c=10.0, eps=1e-12):
+    """run_fused (simulator.cpp:485-559) per row: a [rows, L0] (softmax x,
+    attention P, variance x, sum_sum x1), b = attention V [rows, L0, hd] or
+    sum_sum x2 [rows, L0]; levels = TreeConfig.levels (L0 first, 1 last).
+    Returns d1, d2 [rows] (+ d3 [rows, hd] for attention)."""
+    pat = FUSED_PATTERNS[pattern]
+    a = _f64(a)
+    rows, L0 = a.shape
+    lv = np.asarray(levels, dtype=np.int64)
+    assert lv[0] == L0
+    hd = b.shape[2] if pat == 2 else 0
+    b = _f64(b) if b is not None else np.zeros(1)
+    d1, d2 = np.empty(rows), np.empty(rows)
+    d3 = np.zeros((rows, max(hd, 1)))
+    for r in range(rows):
+        br = b[r] if pat in (2, 8) else b
+        o1, o2 = np.zeros(1), np.zeros(1)
+        rc = lib().rfo_fused_row(pat, _p(np.ascontiguousarray(a[r])), _p(np.ascontiguousarray(br)), hd,
+                                 lv.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), len(lv) - 1, k, c, eps,
+                                 _p(o1), _p(o2), _p(d3[r]))
+        if rc != 0:
+            raise ValueError("bad tree / fuse level")
+        d1[r], d2[r] = o1[0], o2[0]
+    return (d1, d2, d3) if pat == 2 else (d1, d2)
 
 
 def scaled_max_err(x, y):

@@ -76,3 +76,19 @@ def test_cli_verify_dsl_specs(tmp_path):
                  "reduce 2 op sum\n    x[l] / d1\n")
     rc, j, r = _verify(["--spec", str(f), "--modes", "incremental,cuda"])
     assert rc == 2 and j["modes"][1]["pass"] is False
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,levels", [("safe_softmax", "1024,32,4,1"), ("attention", "256,16,4,1"),
+                                         ("sum_sum", "1024,32,8,1"), ("variance", "8192,16,4,1"),
+                                         ("quant_gemm", "512,4,1")])
+def test_cli_verify_cuda_fused_mode(name, levels):
+    """The reference CLI's fused@k next to cuda-fused@k (run_fused on librf_cuda,
+    simulator.cpp:485-559) at every level k of a 3- or 2-level tree."""
+    depth = len(levels.split(",")) - 1
+    modes = ",".join([f"fused@{k}" for k in range(1, depth + 1)] +
+                     [f"cuda-fused@{k}" for k in range(1, depth + 1)])
+    rc, j, r = _verify(["--workload", name, "--levels", levels, "--modes", modes])
+    assert rc == 0, (r.stdout[-3000:], r.stderr[-2000:])
+    got = {m["mode"]: m for m in j["modes"]}
+    assert all(m["pass"] for m in j["modes"]) and set(got) == set(modes.split(","))

@@ -214,3 +214,60 @@ def test_moments_oracle_matches_reference():
         assert _err(d1, g[f"{tag}.d1"]) < TOL, tag
         assert _err(d2.ravel(), g[f"{tag}.d2"]) < TOL, tag
         assert _err(d3.ravel(), g[f"{tag}.d3"]) < TOL, tag
+
+
+# ---------------------------------------------------------------- run_fused --
+# Fusion at level k (simulator.cpp:485-559): the reference's own fused@k
+# reports (ref_driver golden: "fused_<levels[1..K]>_k<k>") against the C
+# restatement rfo_fused_row, and against the oracle (equal in exact arithmetic).
+
+def _fused_cases(prefix):
+    out = []
+    for name in O.golden_names(prefix):
+        g = O.load_golden(name)
+        for key in g:
+            if key.startswith("fused_") and key.endswith(".d1"):
+                tag, k = key[len("fused_"):-3].rsplit("_k", 1)
+                out.append((name, tag, int(k)))
+    return out
+
+
+FUSED = (_fused_cases("safe_softmax_") + _fused_cases("attention_") + _fused_cases("variance_")
+         + _fused_cases("sum_sum_"))
+
+
+def test_fused_goldens_exist():
+    assert len(FUSED) >= 30
+    assert {n.split("_")[0] for n, _, _ in FUSED} >= {"safe", "attention", "variance", "sum"}
+
+
+@pytest.mark.parametrize("name,tag,k", FUSED)
+def test_fused_restatement_matches_reference(name, tag, k):
+    g = O.load_golden(name)
+    pre = f"fused_{tag}_k{k}"
+    if name.startswith("attention_"):
+        p, v = g["in.P"], g["in.V"]
+        levels = [p.size] + [int(x) for x in tag.split("-")]
+        d1, d2, d3 = O.fused("attention", p.reshape(1, -1), v.reshape(1, *v.shape), levels, k)
+        assert _err(d3.ravel(), g[pre + ".d3"]) < TOL
+        assert _err(d3.ravel(), g["oracle.d3"]) < 1e-10
+    elif name.startswith("sum_sum_"):
+        x1, x2 = g["in.x1"], g["in.x2"]
+        levels = [x1.size] + [int(x) for x in tag.split("-")]
+        d1, d2 = O.fused("sum_sum", x1.reshape(1, -1), x2.reshape(1, -1), levels, k, 10.0, 1e-12)
+    else:
+        pat = "safe_softmax" if name.startswith("safe_softmax_") else "variance"
+        x = g["in.x"]
+        levels = [x.size] + [int(t) for t in tag.split("-")]
+        d1, d2 = O.fused(pat, x.reshape(1, -1), None, levels, k)
+    assert _err(d1, g[pre + ".d1"]) < TOL
+    assert _err(d2, g[pre + ".d2"]) < TOL
+    assert _err(d2, g["oracle.d2"]) < 1e-10
+
+
+def test_fused_restatement_rejects_bad_tree():
+    x = np.zeros((1, 8))
+    with pytest.raises(ValueError):
+        O.fused("safe_softmax", x, None, [8, 3, 1], 1)
+    with pytest.raises(ValueError):
+        O.fused("safe_softmax", x, None, [8, 2, 1], 3)
