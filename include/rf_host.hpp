@@ -1000,9 +1000,12 @@ inline std::vector<ExecReport> execute_batched(const Program& prog, const TreeCo
   // validate_tree (cascade.cpp:37-66) + store shapes (simulator.cpp:235-245)
   if (cfg.levels.size() < 2 || cfg.levels.front() != prog.L0 || cfg.levels.back() != 1)
     throw ShapeMismatch("BadTree: levels must run from L0 = " + std::to_string(prog.L0) + " to 1");
-  for (std::size_t k = 1; k < cfg.levels.size(); ++k)
-    if (cfg.levels[k] <= 0 || cfg.levels[k - 1] % cfg.levels[k] != 0)
-      throw ShapeMismatch("BadTree: level widths must divide");
+  for (std::size_t k = 1; k < cfg.levels.size(); ++k) {
+    if (cfg.levels[k] == 1 && cfg.levels[k - 1] == 1) continue;  // [1, 1]: a length-1 axis
+    if (cfg.levels[k] <= 0 || cfg.levels[k] >= cfg.levels[k - 1])
+      throw ShapeMismatch("NotDecreasing: levels must strictly decrease at index " + std::to_string(k));
+    if (cfg.levels[k - 1] % cfg.levels[k] != 0) throw ShapeMismatch("BadTree: level widths must divide");
+  }
   for (const auto& in : prog.spec.inputs) {
     const auto& a = st.array(in.name);
     if (a.len != in.len || a.free_len != in.free_len)

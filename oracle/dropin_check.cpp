@@ -144,7 +144,7 @@ int main() {
   check_workload("sum_sum_1024", builtin("sum_sum"), 1e-5, {2, 8}, 3);
   check_workload("moment_of_inertia_1024", builtin("moment_of_inertia"), 1e-5, {2, 8}, 3);
   // run_fused: level-1 segments evaluated non-incrementally on chip
-  check_fused("attention_256x64", make_attention(256, 64), 1e-5, {{4, 1}, {16, 4, 1}, {256, 1}}, 2);
+  check_fused("attention_256x64", make_attention(256, 64), 1e-5, {{4, 1}, {16, 4, 1}, {128, 1}}, 2);
   check_fused("attention_128x128", make_attention(128, 128), 1e-5, {{2, 1}}, 1);
   check_fused("safe_softmax_1024", make_safe_softmax(1024), 1e-5, {{32, 4, 1}, {8, 1}, {1}}, 2);
   check_fused("variance_8192", builtin("variance"), 1e-5, {{16, 4, 1}, {64, 1}}, 2);

@@ -413,8 +413,10 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
     if (d.tree_depth < 1 || d.tree_depth > 8) return fail(RF_ERR_SHAPE, "BadTree: depth must be 1..8");
     int64_t below = d.len;
     for (int i = 0; i < d.tree_depth; ++i) {
-      if (d.tree[i] < 1 || below % d.tree[i] != 0)
-        return fail(RF_ERR_SHAPE, "BadTree: level widths must divide the level below");
+      if (d.tree[i] < 1 || (d.tree[i] >= below && !(d.tree[i] == 1 && below == 1)))
+        return fail(RF_ERR_SHAPE, "NotDecreasing: levels must strictly decrease at index " + std::to_string(i + 1));
+      if (below % d.tree[i] != 0)
+        return fail(RF_ERR_SHAPE, "DivisibilityViolation: level widths must divide the level below");
       below = d.tree[i];
     }
     if (below != 1) return fail(RF_ERR_SHAPE, "BadTree: the last level must be 1");

@@ -83,6 +83,8 @@ def test_fused_tree_is_validated_before_device():
         Plan(mk((8, 2), 1))           # last level must be 1
     with pytest.raises(ShapeMismatch):
         Plan(mk((8, 3, 1), 1))        # 3 does not divide 8
+    with pytest.raises(ShapeMismatch):
+        Plan(mk((64, 1), 1))          # NotDecreasing: levels [64, 64, 1]
     with pytest.raises(ValueError):
         Plan(mk((8, 1), 3))           # k > depth
     with pytest.raises(ValueError):
