@@ -1103,7 +1103,7 @@ static cudaError_t launch_rms_like(const GemmArgs& g, cudaStream_t st, bool ln) 
   cudaError_t e;
   if (pair) {  // 2-SM path
     rms::Params p{g.d1, g.k, 1.f / static_cast<float>(g.stat_len > 0 ? g.stat_len : g.k), g.eps, static_cast<int>(g.m / (2 * BM)),
-                  static_cast<int>(g.n / BN), group_param(8), g.d2, g.colsum, g.c4 != nullptr,
+                  static_cast<int>(g.n / BN), group_param(16), g.d2, g.colsum, g.c4 != nullptr,
                   k_slice, g.ws_d1, g.ws_d2, g.ws_rows, S > 1};
     const size_t smem = sizeof(rms2::Smem) + 1024;
     auto kern = ln ? rms2::rms_gemm_2sm_kernel<true> : rms2::rms_gemm_2sm_kernel<false>;
@@ -1165,7 +1165,7 @@ cudaError_t launch_quant_gemm_sm100(const GemmArgs& g, cudaStream_t st) {
   cudaError_t e;
   if (g.m % (2 * BM) == 0) {  // 2-SM path
     qnt::Params p{g.d1, g.domain_flag, g.k, g.fmax, static_cast<int>(g.m / (2 * BM)),
-                  static_cast<int>(g.n / qnt::BNQ), group_param(4), k_slice, g.ws_d1, g.ws_rows, S > 1};
+                  static_cast<int>(g.n / qnt::BNQ), group_param(8), k_slice, g.ws_d1, g.ws_rows, S > 1};
     const size_t smem = sizeof(qnt2::Smem) + 1024;
     e = cudaFuncSetAttribute(qnt2::quant_gemm_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
