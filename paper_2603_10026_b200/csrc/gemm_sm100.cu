@@ -40,12 +40,12 @@ using namespace sm100;
 #ifdef RF_QNT_TRACE
 // clock64 timeline of one CTA of the 2-SM quant kernel (probe build only,
 // tools/trace_quant.py): slot = event * 64 + K step.
-__device__ long long g_qnt_trace[4096];
+__device__ long long g_qnt_trace[2 * 4096];  // [CTA rank in the traced pair][event * 64 + K step]
 __device__ int g_qnt_trace_cta;
 #define QTRACE(ev, t)                                                                 \
   do {                                                                               \
-    if (blockIdx.x == g_qnt_trace_cta && blockIdx.y == 0 && (t) < 64)                \
-      g_qnt_trace[(ev) * 64 + (t)] = clock64();                                      \
+    if ((blockIdx.x >> 1) == (g_qnt_trace_cta >> 1) && blockIdx.y == 0 && (t) < 64)  \
+      g_qnt_trace[(blockIdx.x & 1) * 4096 + (ev) * 64 + (t)] = clock64();            \
   } while (0)
 #else
 #define QTRACE(ev, t) \
@@ -827,6 +827,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = s.tmem_base;
+  if (threadIdx.x == 0) QTRACE(7, 3);  // common origin of the pair's clocks
 
   if (warp == 4) {
     if (elect_one()) {
@@ -1018,6 +1019,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
 }
 
 }  // namespace qnt2
+
 
 // ============================================================== packing ====
 

@@ -8,11 +8,11 @@ extern "C" int rf_probe_qnt_trace(const void* a, const void* w, float* d1, float
   rf::GemmArgs g{};
   g.a = a; g.b = w; g.d1 = d1; g.c = c; g.domain_flag = flag;
   g.m = m; g.n = n; g.k = k; g.stat_len = k; g.fmax = 448.f; g.segments = 1; g.ws_rows = m;
-  long long zero[4096] = {0};
+  static long long zero[2 * 4096] = {0};
   cudaMemcpyToSymbol(rf::g_qnt_trace, zero, sizeof zero);
   cudaMemcpyToSymbol(rf::g_qnt_trace_cta, &cta, sizeof cta);
   if (rf::launch_quant_gemm_sm100(g, 0) != cudaSuccess) return 1;
   if (cudaDeviceSynchronize() != cudaSuccess) return 2;
-  cudaMemcpyFromSymbol(out, rf::g_qnt_trace, sizeof(long long) * 4096);
+  cudaMemcpyFromSymbol(out, rf::g_qnt_trace, sizeof(long long) * 2 * 4096);
   return 0;
 }
