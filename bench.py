@@ -582,7 +582,13 @@ def measure(cfg, args, D, steps, warmup, want_cpu, cpu_budget):
         # fp32 SIMT FMA peak: 148 SMs x 128 lanes x 2 FLOP x max SM clock
         peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
         achieved = lflops / (kern_ms * 1e-3) / 1e12
-        unit, psrc, bound = "TFLOP/s", "fp32 SIMT FMA peak at max SM clock (no tensor cores on this path)", "compute"
+        unit, bound = "TFLOP/s", "compute"
+        if "tf32" in kernel:
+            psrc = ("fp32 SIMT FMA peak at max SM clock: the fp32 roofline of the SIMT form; this kernel runs "
+                    "fp32-accurate products as 3xTF32 tcgen05 MMAs, whose own ceiling (bf16 burst / 2 / 3) "
+                    "is roofline.tf32x3_peak")
+        else:
+            psrc = "fp32 SIMT FMA peak at max SM clock (no tensor cores on this path)"
     else:
         achieved = lflops / (kern_ms * 1e-3) / 1e12
         unit = "TFLOP/s"
@@ -631,7 +637,8 @@ def measure(cfg, args, D, steps, warmup, want_cpu, cpu_budget):
                      "unit": unit, "frac": round(achieved / peak, 4), "traffic": traffic,
                      "peak_source": psrc,
                      "algorithmic": {"flops": lflops, "bytes": lbytes,
-                                     "per": "rank 0's launch (its share of the config)"}},
+                                     "per": "rank 0's launch (its share of the config)"},
+                     **({"tf32x3_peak": round(pk["bf16_tflops"] / 6, 1)} if "tf32" in kernel else {})},
         "e2e": {"value": round(job_flops * e2e_steps / e2e_s / 1e12, 3), "unit": "TFLOP/s",
                 "h2d_bytes_per_step": h2d * D.world, "d2h_bytes_per_step": d2h * D.world,
                 "path": ("split_kv_decode between pinned-host copies (partials + all-gather + merge)"

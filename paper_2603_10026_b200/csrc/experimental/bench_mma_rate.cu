@@ -90,12 +90,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
   if (threadIdx.x < 32) tmem_dealloc_2sm<512>(tmem);
 }
 
+// 1-SM forms (the attention kernel's S = Q K^T (SS, K-major B) and O += P V
+// (TS, V MN-major)): one CTA per SM, M = 128.
+__global__ void __launch_bounds__(128, 1)
+    rate1_kernel(int ts, int mn_b, int n, int reps, long long* out) {
+  extern __shared__ uint8_t raw[];
+  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  for (int i = threadIdx.x; i < 16384 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(s.a)[i] = 0x3c3a3836u ^ (i * 2654435761u);
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(s.b)[i] = 0x3a383634u ^ (i * 2246822519u);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(&s.done, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s.tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+  if (threadIdx.x < 32) {
+    const bool el = elect_one();
+    const uint32_t id = idesc_f16(128, n, kFmtBF16, false, mn_b != 0);
+    long long t0 = clock64();
+    if (el) {
+      for (int r = 0; r < reps; ++r) {
+        const uint32_t a = smem_u32(s.a), b = smem_u32(s.b[r & 1]);
+        for (int ks = 0; ks < 8; ++ks) {  // K = 128 per group: 8 x K16
+          // K-major B: 128 B rows, K16 = 32 B step inside the row, 2 row chunks of 64 K;
+          // MN-major B (V): K16 = 16 rows of 128 B MN-chunks = 2048 B step
+          const uint64_t bd = mn_b ? sdesc_mnmajor_sw128(b + ks * 2048, n * 128)
+                                   : sdesc_kmajor_sw128(b + (ks >> 2) * (n * 128) + (ks & 3) * 32);
+          if (ts)
+            mma_f16_ts(tmem + 256, tmem + ks * 8, bd, id, r | ks);
+          else
+            mma_f16_ss(tmem + 256, sdesc_kmajor_sw128(a + (ks >> 2) * 16384 + (ks & 3) * 32), bd, id, r | ks);
+        }
+      }
+      mma_commit(&s.done);
+    }
+    __syncwarp();
+    mbar_wait(&s.done, 0);
+    const long long t1 = clock64();
+    if (el) out[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc<512>(tmem);
+}
+
 int main() {
   const Mode modes[] = {
       {"f8 SS N=256 x2 (qnt2)", 0, 0, 256, 2}, {"f8 TS N=224 x2 (qnt3)", 0, 1, 224, 2},
       {"f8 SS N=224 x2", 0, 0, 224, 2},        {"f8 TS N=256 x1", 0, 1, 256, 1},
       {"f8 SS N=256 x1", 0, 0, 256, 1},        {"f8 TS N=128 x2", 0, 1, 128, 2},
       {"bf16 SS N=256 x2", 1, 0, 256, 2},      {"bf16 TS N=224 x2", 1, 1, 224, 2},
+      {"bf16 SS N=128 x1 (M=256)", 1, 0, 128, 1}, {"bf16 TS N=128 x1 (M=256)", 1, 1, 128, 1},
+      {"bf16 SS N=256 x1 (M=256)", 1, 0, 256, 1}, {"bf16 SS N=128 x2 (M=256)", 1, 0, 128, 2},
   };
   const int pairs = 74, reps = 512;
   long long* out;
@@ -122,6 +177,38 @@ int main() {
     const double per = static_cast<double>(sum) / 74 / reps;
     printf("%-26s cycles per K tile: %7.1f (floor %6.1f) -> %.3f of peak (max-pair %.1f)\n", m.name, per,
            floor_cyc, floor_cyc / per, static_cast<double>(mx) / reps);
+  }
+  {
+    struct M1 {
+      const char* name;
+      int ts, mn_b, n;
+    } m1[] = {{"bf16 1-SM SS N=128 (S=QK^T)", 0, 0, 128},
+              {"bf16 1-SM TS N=128 MN-major B (PV)", 1, 1, 128},
+              {"bf16 1-SM TS N=128 K-major B", 1, 0, 128},
+              {"bf16 1-SM SS N=256", 0, 0, 256},
+              {"bf16 1-SM TS N=64 K-major B", 1, 0, 64},
+              {"bf16 1-SM SS N=64", 0, 0, 64},
+              {"bf16 1-SM TS N=256 K-major B", 1, 0, 256},
+              {"bf16 1-SM TS N=192 K-major B", 1, 0, 192}};
+    long long* out1;
+    cudaMalloc(&out1, 148 * sizeof(long long));
+    const size_t smem1 = 160 * 1024;  // descriptors of the N = 256 / K = 128 case reach past Smem
+    cudaFuncSetAttribute(rate1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1));
+    for (const M1& m : m1) {
+      for (int it = 0; it < 2; ++it) rate1_kernel<<<148, 128, smem1>>>(m.ts, m.mn_b, m.n, reps, out1);
+      if (cudaDeviceSynchronize() != cudaSuccess) {
+        printf("%s failed\n", m.name);
+        return 1;
+      }
+      long long h[148];
+      cudaMemcpy(h, out1, sizeof h, cudaMemcpyDeviceToHost);
+      double sum = 0;
+      for (long long v : h) sum += v;
+      const double floor_cyc = 128.0 * m.n * 128.0 / 4096.0;
+      const double per = sum / 148 / reps;
+      printf("%-36s cycles per K=128: %7.1f (floor %6.1f) -> %.3f of peak\n", m.name, per, floor_cyc,
+             floor_cyc / per);
+    }
   }
   return 0;
 }

@@ -162,6 +162,7 @@ const char* kernel_name(rf::Kernel k) {
   switch (k) {
     case rf::Kernel::SoftmaxRows: return "softmax_rows (SIMT, single pass)";
     case rf::Kernel::AttentionF32: return "attention_f32 (SIMT, paper form)";
+    case rf::Kernel::AttentionTf32: return "attention_tf32 (fp32 as 3xTF32 tcgen05, in-cluster slice fold)";
     case rf::Kernel::AttentionSm100: return "attention_sm100 (bf16 tcgen05/TMEM/TMA, ping-pong Q tiles)";
     case rf::Kernel::AttentionDecode: return "attention_decode (bf16 split-KV, TMA bulk)";
     case rf::Kernel::QuantGemmSm100: return "quant_gemm_sm100 (e4m3 tcgen05 kind::f8f6f4)";
@@ -221,10 +222,11 @@ rf_status attention_run(const rf_plan* p, const rf_io* io, int64_t bh0, int64_t 
   switch (p->kernel) {
     case rf::Kernel::AttentionSm100: e = rf::launch_attention_sm100(a, st); break;
     case rf::Kernel::AttentionDecode: e = rf::launch_attention_decode(a, st); break;
+    case rf::Kernel::AttentionTf32: e = rf::launch_attention_tf32(a, st); break;
     default: e = rf::launch_attention_f32(a, st); break;
   }
   if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
-  if (p->nsplit > 1) {
+  if (p->nsplit > 1 && p->kernel != rf::Kernel::AttentionTf32) {  // tf32: folded in-kernel
     e = rf::launch_attention_merge(a.part_m, a.part_l, a.part_o, p->nsplit, nbh * d.rows,
                                    p->rows_total, d.free_len, a.m, a.l, a.o, d.dtype, st);
     if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("merge launch: ") + cudaGetErrorString(e));
@@ -530,7 +532,18 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
         return bail(RF_ERR_UNSUPPORTED, "attention: head_dim must be 16/32/64/128");
       p->rows_total = d.batch * d.heads * d.rows;
       p->nsplit = d.segments;
-      if (d.dtype == RF_F32) {
+      if (d.dtype == RF_F32 && d.segments <= 8 &&
+          rf::attention_tf32_supports(d.rows, d.len, d.free_len, d.segments) && !std::getenv("RF_ATTN_F32_SIMT")) {
+        // tcgen05 (3xTF32): cut the reference slices into up to 8 sub-slices of
+        // >= 128 keys (one cluster per 128-row tile) while the grid is below
+        // one CTA per SM; the in-kernel fold is the same closed-form sum over
+        // the finer slices. RF_ATTN_F32_SIMT=1 keeps the SIMT kernel (A/B only).
+        p->kernel = rf::Kernel::AttentionTf32;
+        const int64_t tiles = d.batch * d.heads * (d.rows / 128);
+        while (p->nsplit * 2 <= 8 && tiles * p->nsplit < 148 &&
+               rf::attention_tf32_supports(d.rows, d.len, d.free_len, p->nsplit * 2))
+          p->nsplit *= 2;
+      } else if (d.dtype == RF_F32) {
         p->kernel = rf::Kernel::AttentionF32;
         // A grid too small to fill the GPU (cfg1: 16 row tiles x 8 slices):
         // cut every reference slice into c sub-slices of >= 64 keys, up to
@@ -612,7 +625,7 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
   }
   if (is_gemm(p->d.pattern) && p->d.pattern != RF_PATTERN_MOE_ROUTER) p->nsplit = p->d.segments;
   p->launches = (((p->d.pattern == RF_PATTERN_ATTENTION || p->d.pattern == RF_PATTERN_MLA_DECODE) &&
-                  p->nsplit > 1) ||
+                  p->nsplit > 1 && p->kernel != rf::Kernel::AttentionTf32) ||
                  p->d.pattern == RF_PATTERN_MOE_ROUTER ||
                  (is_gemm(p->d.pattern) && p->nsplit > 1)) ? 2 : 1;
 

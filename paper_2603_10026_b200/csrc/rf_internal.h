@@ -25,7 +25,8 @@ void set_error(const std::string& msg);
 
 enum class Kernel {
   SoftmaxRows,        // softmax.cu
-  AttentionF32,       // attn_f32.cu   (SIMT, paper form, cfg1)
+  AttentionF32,       // attn_f32.cu   (SIMT, paper form; partials, odd shapes)
+  AttentionTf32,      // attn_tf32.cu  (3xTF32 tcgen05, in-cluster slice fold, cfg1)
   AttentionSm100,     // attn_sm100.cu (bf16 tcgen05/TMEM/TMA prefill, ping-pong Q tiles)
   AttentionDecode,    // attn_decode.cu (bf16 split-KV streaming, cfg3)
   QuantGemmSm100,     // gemm_sm100.cu (e4m3 kind::f8f6f4, cfg4)
@@ -118,6 +119,9 @@ struct AttnArgs {
   int dtype;
 };
 cudaError_t launch_attention_f32(const AttnArgs& a, cudaStream_t st);
+// fp32 on tcgen05 (3xTF32) with the slice fold inside the kernel (one launch).
+cudaError_t launch_attention_tf32(const AttnArgs& a, cudaStream_t st);
+bool attention_tf32_supports(int64_t sq, int64_t skv, int64_t d, int64_t nslices);
 cudaError_t launch_attention_decode(const AttnArgs& a, cudaStream_t st);
 // Returns cudaErrorNotSupported when the shape has no tcgen05 instantiation.
 cudaError_t launch_attention_sm100(const AttnArgs& a, cudaStream_t st);

@@ -179,3 +179,57 @@ def test_safe_softmax_vs_goldens_and_oracle():
     d1, d2 = safe_softmax(torch.tensor([[1.0, 2.0, 3.0]], device="cuda"))
     assert d1.item() == 3.0
     assert abs(d2.item() - (np.exp(-2) + np.exp(-1) + 1)) < 1e-6
+
+
+def _plan_run(shape, segments, seed, simt=False):
+    import os
+
+    import torch
+    from paper_2603_10026_b200 import Desc, Plan
+    from paper_2603_10026_b200 import _native as N
+
+    B, H, Sq, Skv, D = shape
+    q, k, v = _inputs(B, H, Sq, Skv, D, seed, torch.float32)
+    if simt:
+        os.environ["RF_ATTN_F32_SIMT"] = "1"
+    try:
+        plan = Plan(Desc(N.RF_PATTERN_ATTENTION, "f32", rows=Sq, len=Skv, free_len=D, batch=B,
+                         heads=H, segments=segments))
+    finally:
+        os.environ.pop("RF_ATTN_F32_SIMT", None)
+    m = torch.empty(B, H, Sq, device="cuda")
+    l, o = torch.empty_like(m), torch.empty(B, H, Sq, D, device="cuda")
+    plan.run([q.cuda(), k.cuda(), v.cuda()], [m, l, o])
+    torch.cuda.synchronize()
+    return plan, (q, k, v), (m, l, o)
+
+
+@pytest.mark.parametrize("shape,segments,nsplit", [
+    ((1, 1, 1024, 1024, 64), 8, 8),    # cfg1: one 128-key tile per CTA, cluster of 8
+    ((1, 1, 1024, 1024, 64), 1, 8),    # run_incremental cut into 8 sub-slices
+    ((1, 1, 256, 2048, 64), 2, 8),     # 256-key slices: two tiles per CTA (running-max rescale of O in TMEM)
+    ((2, 3, 128, 1024, 64), 1, 8),     # several (b, h)
+    ((5, 8, 128, 512, 64), 1, 4),      # a 4-CTA cluster (the grid fills the GPU at 4 sub-slices)
+    ((4, 37, 128, 256, 64), 1, 1),     # grid already fills the GPU: one slice, no fold
+])
+def test_fp32_tcgen05_tf32x3(shape, segments, nsplit):
+    """The fp32 path on tcgen05 (3xTF32, attn_tf32.cu) with the slice fold in
+    the kernel's cluster: plan choice, sub-slicing and <= 1e-5 against the
+    oracle, on shapes with one and several KV tiles per slice."""
+    plan, (q, k, v), (m, l, o) = _plan_run(shape, segments, 23)
+    assert "tf32" in plan.info["kernel"] and plan.info["segments"] == segments
+    assert plan.info["slices_launched"] == nsplit and plan.info["launches_per_run"] == 1
+    _check(q, k, v, m, l, o, 1e-5)
+
+
+def test_fp32_tcgen05_matches_simt_path():
+    """Same inputs through the tcgen05 kernel and the SIMT paper-form kernel
+    (+ merge): both within the fp32 gate of the oracle and of each other."""
+    shape = (1, 1, 1024, 1024, 64)
+    p1, inp, out_t = _plan_run(shape, 8, 5)
+    p2, _, out_s = _plan_run(shape, 8, 5, simt=True)
+    assert "tf32" in p1.info["kernel"] and "SIMT" in p2.info["kernel"]
+    for a, b in zip(out_t, out_s):
+        e = O.scaled_max_err(a.double().cpu().numpy().ravel(), b.double().cpu().numpy().ravel())[0]
+        assert e <= 2e-6, e
+    _check(*inp, *out_t, 1e-5)
