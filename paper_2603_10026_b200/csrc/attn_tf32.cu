@@ -67,8 +67,7 @@ struct Smem {
   uint8_t k[2][D / 32][CH];             // rows = keys
   uint8_t vt[2][BN / 32][D * 128];      // [hi/lo][key chunk]: rows = d, 32 keys each
   float xchg[2][2][BM];                 // [max / sum][column half][row]
-  float st_m[BM], st_l[BM];             // slice state (m, l) for the in-cluster fold
-  uint64_t q_bar, ld_bar, mma_done;
+  uint64_t q_bar, ld_bar, mma_done, recv_bar;
   uint32_t tmem_base;
 };
 
@@ -146,6 +145,14 @@ __device__ __forceinline__ void split_vt(const float4 (&xv)[8], Smem& s, int kr,
   }
 }
 
+// Bulk copy of `bytes` from this CTA's shared memory to a shared::cluster
+// address, completing on a shared::cluster mbarrier (the receiver's).
+__device__ __forceinline__ void bulk_s2c(uint32_t dst_cluster, uint32_t src, uint32_t bytes, uint32_t bar_cluster) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst_cluster), "r"(src), "r"(bytes), "r"(bar_cluster)
+               : "memory");
+}
+
 // TMA of one 128-key tile: K (2 D halves) into the K hi tiles, V into the K
 // lo tiles (staging; V^T is built from there before K is split).
 __device__ __forceinline__ void load_kv(Smem& s, const CUtensorMap* tk, const CUtensorMap* tv, int64_t key0) {
@@ -174,6 +181,7 @@ __global__ void __launch_bounds__(NT, 1)
     mbar_init(&s.q_bar, 1);
     mbar_init(&s.ld_bar, 1);
     mbar_init(&s.mma_done, 1);
+    mbar_init(&s.recv_bar, 1);
     fence_barrier_init();
     // Q and the first K / V tile, all in flight at once
     mbar_arrive_expect_tx(&s.q_bar, 2 * CH);
@@ -333,9 +341,11 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
   } else {
-    // stage the state in this CTA's shared memory (the drained Q tiles):
-    // row-major [128][D] with the 16-byte units of row r XOR-swizzled by r
-    float* so = reinterpret_cast<float*>(s.q);
+    // Stage the state for the bulk push: row-major [128][D] in the drained K
+    // tiles (16-byte units of row r XOR-swizzled by r & 15: conflict-free
+    // here, undone by the reader), then m[128], l[128]. The rows of each
+    // owner (16 / 32 / 64 consecutive rows) are one contiguous block.
+    float* so = reinterpret_cast<float*>(s.k);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int u = (D / 8) * h + j;  // 16-byte unit of the row
@@ -344,9 +354,10 @@ __global__ void __launch_bounds__(NT, 1)
                       __uint_as_float(o[4 * j + 2]) * inv, __uint_as_float(o[4 * j + 3]) * inv);
     }
     if (h == 0) {
-      s.st_m[r] = m;
-      s.st_l[r] = l;
+      so[BM * D + r] = m;
+      so[BM * D + BM + r] = l;
     }
+    fence_proxy_async_smem();  // generic stores -> the bulk copies' reads
   }
   tc_fence_before();
   __syncthreads();
@@ -355,51 +366,54 @@ __global__ void __launch_bounds__(NT, 1)
   }
   TTRACE(6);
   if (!fold) return;
-  // Every slice's state sits in its CTA's shared memory: after the cluster
-  // barrier, CTA z folds rows [z * 128 / S, (z + 1) * 128 / S) of the tile
-  // over all S slices, reading them through distributed shared memory
-  // (coalesced 16-byte units), in slice order with fold.cuh's arithmetic.
+  // In-cluster fold. CTA z owns rows [z * per, (z + 1) * per) of the tile.
+  // After a cluster barrier (every CTA is past its MMAs, so every Q region is
+  // free), each CTA pushes the owners' blocks of its slice state into their Q
+  // region with bulk shared::cta -> shared::cluster copies that complete on
+  // the owner's recv_bar; each owner then folds its rows locally, over all
+  // slices in slice order with fold.cuh's arithmetic.
+  const int ns = static_cast<int>(a.nslices);
+  const int per = BM / ns;
+  const uint32_t blk = static_cast<uint32_t>(per * D * 4), mlb = static_cast<uint32_t>(per * 4);
+  const uint32_t recv = smem_u32(s.q), stage = smem_u32(s.k);
+  if (tid == 0) mbar_arrive_expect_tx(&s.recv_bar, static_cast<uint32_t>(ns) * (blk + 2 * mlb));
   cluster_sync();
   TTRACE(7);
-  const int per = BM / static_cast<int>(a.nslices);
-  const int ns = static_cast<int>(a.nslices);
-  const uint32_t so_base = smem_u32(s.q), sm_base = smem_u32(s.st_m), sl_base = smem_u32(s.st_l);
-  for (int i = tid; i < per * (D / 4); i += NT) {
-    const int rr = static_cast<int>(slice) * per + i / (D / 4), c4 = i % (D / 4);
-    // one round of remote loads: every slice's (m, l) and O unit together
-    // (an empty slice, l = 0, contributes nothing whatever its staged O)
-    float ms[8], ls[8];
-    float4 os[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      ms[j] = -INFINITY;
-      ls[j] = 0.f;
-      os[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (j < ns) {
-        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(ms[j]) : "r"(mapa_shared(sm_base + 4 * rr, j)));
-        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(ls[j]) : "r"(mapa_shared(sl_base + 4 * rr, j)));
-        asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-                     : "=f"(os[j].x), "=f"(os[j].y), "=f"(os[j].z), "=f"(os[j].w)
-                     : "r"(mapa_shared(so_base + 4 * (rr * D + 4 * (c4 ^ (rr & 15))), j)));
-      }
+  if (tid == 0) {
+    const uint32_t me = static_cast<uint32_t>(slice);
+    for (int z = 0; z < ns; ++z) {
+      const uint32_t bar = mapa_shared(smem_u32(&s.recv_bar), z);
+      const uint32_t dst = mapa_shared(recv, z);
+      // [slot][per rows][D] O, then m[slot][per], then l[slot][per]
+      bulk_s2c(dst + me * blk, stage + z * blk, blk, bar);
+      bulk_s2c(dst + ns * blk + me * mlb, stage + BM * D * 4 + z * mlb, mlb, bar);
+      bulk_s2c(dst + ns * blk + ns * mlb + me * mlb, stage + BM * D * 4 + BM * 4 + z * mlb, mlb, bar);
     }
+    bulk_commit();
+  }
+  mbar_wait(&s.recv_bar, 0);
+  const float* ro = reinterpret_cast<const float*>(s.q);
+  const float* rm = ro + ns * per * D;
+  const float* rl = rm + ns * per;
+  for (int i = tid; i < per * (D / 4); i += NT) {
+    const int lr = i / (D / 4), c4 = i % (D / 4);
     float mm = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) mm = fmaxf(mm, ms[j]);
+    for (int j = 0; j < ns; ++j) mm = fmaxf(mm, rm[j * per + lr]);
     float ll = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (ls[j] != 0.f) {
-        const float w = ls[j] * __expf(ms[j] - mm);
+    for (int j = 0; j < ns; ++j) {
+      const float lj = rl[j * per + lr];
+      if (lj != 0.f) {  // an empty slice contributes nothing whatever its staged O
+        const float4 oj = *reinterpret_cast<const float4*>(ro + (j * per + lr) * D + 4 * (c4 ^ (lr & 15)));
+        const float w = lj * __expf(rm[j * per + lr] - mm);
         ll += w;
-        acc.x = fmaf(os[j].x, w, acc.x);
-        acc.y = fmaf(os[j].y, w, acc.y);
-        acc.z = fmaf(os[j].z, w, acc.z);
-        acc.w = fmaf(os[j].w, w, acc.w);
+        acc.x = fmaf(oj.x, w, acc.x);
+        acc.y = fmaf(oj.y, w, acc.y);
+        acc.z = fmaf(oj.z, w, acc.z);
+        acc.w = fmaf(oj.w, w, acc.w);
       }
     }
-    const int64_t grow = row0 + rr;
+    const int64_t grow = row0 + static_cast<int64_t>(slice) * per + lr;
     if (grow < a.sq) {
       const int64_t row = bh * a.sq + grow;
       const float iv = 1.f / ll;
@@ -412,7 +426,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
   }
   TTRACE(8);
-  cluster_sync();  // no CTA leaves while its shared memory may still be read
+  if (tid == 0) bulk_wait_read0();  // our outgoing copies have read the staging before we leave
 }
 
 }  // namespace
