@@ -192,6 +192,9 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == 0) tmem_alloc<512>(&s.tmem_base);
   const int r = tid & (BM - 1), h = tid >> 7;  // thread (row / key r, D half h)
   uint32_t ld_phase = 0;
+  tc_fence_before();
+  __syncthreads();  // barriers initialised (and the TMEM base written) before anyone waits
+  tc_fence_after();
   mbar_wait(&s.q_bar, 0);
   {
     float4 x[8];
@@ -376,12 +379,15 @@ __global__ void __launch_bounds__(NT, 1)
   const int per = BM / ns;
   const uint32_t blk = static_cast<uint32_t>(per * D * 4), mlb = static_cast<uint32_t>(per * 4);
   const uint32_t recv = smem_u32(s.q), stage = smem_u32(s.k);
-  if (tid == 0) mbar_arrive_expect_tx(&s.recv_bar, static_cast<uint32_t>(ns) * (blk + 2 * mlb));
+  // the own slice's block is read from the staging area in place (a bulk
+  // copy to a shared::cluster address of the executing CTA is not allowed)
+  if (tid == 0) mbar_arrive_expect_tx(&s.recv_bar, static_cast<uint32_t>(ns - 1) * (blk + 2 * mlb));
   cluster_sync();
   TTRACE(7);
   if (tid == 0) {
     const uint32_t me = static_cast<uint32_t>(slice);
     for (int z = 0; z < ns; ++z) {
+      if (z == static_cast<int>(me)) continue;
       const uint32_t bar = mapa_shared(smem_u32(&s.recv_bar), z);
       const uint32_t dst = mapa_shared(recv, z);
       // [slot][per rows][D] O, then m[slot][per], then l[slot][per]
@@ -395,17 +401,22 @@ __global__ void __launch_bounds__(NT, 1)
   const float* ro = reinterpret_cast<const float*>(s.q);
   const float* rm = ro + ns * per * D;
   const float* rl = rm + ns * per;
+  const float* own = reinterpret_cast<const float*>(s.k);  // staging: [128][D], m[128], l[128]
+  const int me = static_cast<int>(slice);
   for (int i = tid; i < per * (D / 4); i += NT) {
     const int lr = i / (D / 4), c4 = i % (D / 4);
+    const int orow = me * per + lr;  // the own slice's row in the staging area
     float mm = -INFINITY;
-    for (int j = 0; j < ns; ++j) mm = fmaxf(mm, rm[j * per + lr]);
+    for (int j = 0; j < ns; ++j) mm = fmaxf(mm, j == me ? own[BM * D + orow] : rm[j * per + lr]);
     float ll = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int j = 0; j < ns; ++j) {
-      const float lj = rl[j * per + lr];
+      const float lj = j == me ? own[BM * D + BM + orow] : rl[j * per + lr];
+      const float mj = j == me ? own[BM * D + orow] : rm[j * per + lr];
       if (lj != 0.f) {  // an empty slice contributes nothing whatever its staged O
-        const float4 oj = *reinterpret_cast<const float4*>(ro + (j * per + lr) * D + 4 * (c4 ^ (lr & 15)));
-        const float w = lj * __expf(rm[j * per + lr] - mm);
+        const float* src = j == me ? own + orow * D : ro + (j * per + lr) * D;
+        const float4 oj = *reinterpret_cast<const float4*>(src + 4 * (c4 ^ (lr & 15)));
+        const float w = lj * __expf(mj - mm);
         ll += w;
         acc.x = fmaf(oj.x, w, acc.x);
         acc.y = fmaf(oj.y, w, acc.y);

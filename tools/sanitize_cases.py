@@ -38,6 +38,14 @@ def attn_f32():
     return _close(o, _attn_ref(q, k, v), 1e-4)
 
 
+def attn_tf32():
+    """fp32 on tcgen05 (3xTF32), a 4-CTA cluster with the in-cluster fold."""
+    q = (torch.rand(1, 1, 128, 64, device="cuda") * 2 - 1) / 8
+    k, v = (torch.rand(2, 1, 1, 512, 64, device="cuda") * 2 - 1)
+    _, _, o = attention(q, k, v, segments=4)
+    return _close(o, _attn_ref(q, k, v), 1e-5)
+
+
 def attn_bf16():
     q = ((torch.rand(1, 2, 256, 128, device="cuda") * 2 - 1) / 11).bfloat16()
     k, v = (torch.rand(2, 1, 2, 256, 128, device="cuda") * 2 - 1).bfloat16()
@@ -142,7 +150,7 @@ def rowstats():
     return _close(m2, (mass[..., None] * pos).sum(1), 1e-4)
 
 
-CASES = [attn_f32, attn_bf16, decode, softmax, quant, quant_2sm, rms, rms_2sm, layernorm, routing, router,
+CASES = [attn_f32, attn_tf32, attn_bf16, decode, softmax, quant, quant_2sm, rms, rms_2sm, layernorm, routing, router,
          mla, rowstats]
 
 
