@@ -93,7 +93,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
 // 1-SM forms (the attention kernel's S = Q K^T (SS, K-major B) and O += P V
 // (TS, V MN-major)): one CTA per SM, M = 128.
 __global__ void __launch_bounds__(128, 1)
-    rate1_kernel(int ts, int mn_b, int n, int reps, long long* out) {
+    rate1_kernel(int ts, int mn_b, int n, int reps, long long* out, int mn_a = 0) {
   extern __shared__ uint8_t raw[];
   Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   for (int i = threadIdx.x; i < 16384 / 4; i += blockDim.x)
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t tmem = s.tmem_base;
   if (threadIdx.x < 32) {
     const bool el = elect_one();
-    const uint32_t id = idesc_f16(128, n, kFmtBF16, false, mn_b != 0);
+    const uint32_t id = idesc_f16(128, n, kFmtBF16, mn_a != 0, mn_b != 0);
     long long t0 = clock64();
     if (el) {
       for (int r = 0; r < reps; ++r) {
@@ -128,7 +128,10 @@ __global__ void __launch_bounds__(128, 1)
           if (ts)
             mma_f16_ts(tmem + 256, tmem + ks * 8, bd, id, r | ks);
           else
-            mma_f16_ss(tmem + 256, sdesc_kmajor_sw128(a + (ks >> 2) * 16384 + (ks & 3) * 32), bd, id, r | ks);
+            mma_f16_ss(tmem + 256,
+                       mn_a ? sdesc_mnmajor_sw128(a + ks * 2048, 128 * 128)
+                            : sdesc_kmajor_sw128(a + (ks >> 2) * 16384 + (ks & 3) * 32),
+                       bd, id, r | ks);
         }
       }
       mma_commit(&s.done);
@@ -181,8 +184,10 @@ int main() {
   {
     struct M1 {
       const char* name;
-      int ts, mn_b, n;
-    } m1[] = {{"bf16 1-SM SS N=128 (S=QK^T)", 0, 0, 128},
+      int ts, mn_b, n, mn_a;
+    } m1[] = {{"bf16 1-SM SS N=128 A MN-major", 0, 0, 128, 1},
+              {"bf16 1-SM SS N=128 B MN-major", 0, 1, 128, 0},
+              {"bf16 1-SM SS N=128 A,B MN-major", 0, 1, 128, 1},{"bf16 1-SM SS N=128 (S=QK^T)", 0, 0, 128},
               {"bf16 1-SM TS N=128 MN-major B (PV)", 1, 1, 128},
               {"bf16 1-SM TS N=128 K-major B", 1, 0, 128},
               {"bf16 1-SM SS N=256", 0, 0, 256},
@@ -195,7 +200,7 @@ int main() {
     const size_t smem1 = 160 * 1024;  // descriptors of the N = 256 / K = 128 case reach past Smem
     cudaFuncSetAttribute(rate1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1));
     for (const M1& m : m1) {
-      for (int it = 0; it < 2; ++it) rate1_kernel<<<148, 128, smem1>>>(m.ts, m.mn_b, m.n, reps, out1);
+      for (int it = 0; it < 2; ++it) rate1_kernel<<<148, 128, smem1>>>(m.ts, m.mn_b, m.n, reps, out1, m.mn_a);
       if (cudaDeviceSynchronize() != cudaSuccess) {
         printf("%s failed\n", m.name);
         return 1;
