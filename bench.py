@@ -583,12 +583,14 @@ def measure(cfg, args, D, steps, warmup, want_cpu, cpu_budget):
         peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
         achieved = lflops / (kern_ms * 1e-3) / 1e12
         unit, bound = "TFLOP/s", "compute"
+        psrc = "fp32 SIMT FMA peak at max SM clock (no tensor cores on this path)"
         if "tf32" in kernel:
-            psrc = ("fp32 SIMT FMA peak at max SM clock: the fp32 roofline of the SIMT form; this kernel runs "
-                    "fp32-accurate products as 3xTF32 tcgen05 MMAs, whose own ceiling (bf16 burst / 2 / 3) "
-                    "is roofline.tf32x3_peak")
-        else:
-            psrc = "fp32 SIMT FMA peak at max SM clock (no tensor cores on this path)"
+            # fp32-accurate products as 3xTF32 tcgen05 MMAs: the tensor rate for
+            # tf32 is half the bf16 rate, and every product costs three MMAs
+            simt_peak, peak, bound = peak, pk["bf16_tflops"] / 6, "tensor"
+            psrc = (f"{pk_src} bf16 burst / 2 (tf32 rate) / 3 (3xTF32 passes); the fp32 SIMT FMA peak "
+                    f"{simt_peak:.1f} TFLOP/s is roofline.fp32_simt_peak. Latency-bound at this size "
+                    "(1 MB problem, L2 flushed): neither peak is approachable")
     else:
         achieved = lflops / (kern_ms * 1e-3) / 1e12
         unit = "TFLOP/s"
@@ -638,7 +640,8 @@ def measure(cfg, args, D, steps, warmup, want_cpu, cpu_budget):
                      "peak_source": psrc,
                      "algorithmic": {"flops": lflops, "bytes": lbytes,
                                      "per": "rank 0's launch (its share of the config)"},
-                     **({"tf32x3_peak": round(pk["bf16_tflops"] / 6, 1)} if "tf32" in kernel else {})},
+                     **({"fp32_simt_peak": round(simt_peak, 1), "frac_vs_fp32_simt": round(achieved / simt_peak, 4)}
+                        if cfg["dtype"] == "f32" and "tf32" in kernel else {})},
         "e2e": {"value": round(job_flops * e2e_steps / e2e_s / 1e12, 3), "unit": "TFLOP/s",
                 "h2d_bytes_per_step": h2d * D.world, "d2h_bytes_per_step": d2h * D.world,
                 "path": ("split_kv_decode between pinned-host copies (partials + all-gather + merge)"
