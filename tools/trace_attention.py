@@ -9,7 +9,7 @@ import sys
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-h = ctypes.CDLL(os.path.join(ROOT, "paper_2603_10026_b200", "librf_probe.so"))
+h = ctypes.CDLL(os.path.join(ROOT, "paper_2603_10026_b200", os.environ.get("RF_PROBE_LIB", "librf_probe.so")))
 h.rf_probe_attn_trace.restype = ctypes.c_int
 B, H, S, D = 8, 32, 4096, 128
 q = ((torch.rand(B, H, S, D, device="cuda") * 2 - 1) / D ** 0.5).bfloat16()
