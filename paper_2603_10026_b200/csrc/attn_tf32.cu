@@ -185,7 +185,9 @@ __global__ void __launch_bounds__(NT, 1)
     mbar_init(&s.mma_done, 1);
     mbar_init(&s.recv_bar, 1);
     fence_barrier_init();
-    // Q and the first K / V tile, all in flight at once
+    // Q and the first K / V tile, all in flight at once. A ragged last row
+    // tile (Sq % 128 != 0) reads the next head's rows or TMA zero fill past
+    // the tensor: those rows are computed and never stored.
     mbar_arrive_expect_tx(&s.q_bar, 2 * CH);
     for (int hh = 0; hh < 2; ++hh)
       tma_load_2d(s.q[0][hh], &tq, &s.q_bar, 32 * hh, static_cast<int32_t>(bh * a.sq + row0), kEvictFirst);
@@ -445,7 +447,7 @@ __global__ void __launch_bounds__(NT, 1)
 }  // namespace
 
 bool attention_tf32_supports(int64_t sq, int64_t skv, int64_t d, int64_t nslices) {
-  return d == D && sq % BM == 0 && nslices >= 1 && nslices <= 8 && (BM % nslices) == 0 &&
+  return d == D && sq >= 1 && nslices >= 1 && nslices <= 8 && (BM % nslices) == 0 &&
          skv % nslices == 0 && (skv / nslices) % BN == 0;
 }
 
@@ -472,7 +474,7 @@ cudaError_t launch_attention_tf32(const AttnArgs& a, cudaStream_t st) {
     attr_set.fetch_or(bit);
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(a.sq / BM), static_cast<unsigned>(a.bh),
+  cfg.gridDim = dim3(static_cast<unsigned>((a.sq + BM - 1) / BM), static_cast<unsigned>(a.bh),
                      static_cast<unsigned>(a.nslices));
   cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;

@@ -532,14 +532,14 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
         return bail(RF_ERR_UNSUPPORTED, "attention: head_dim must be 16/32/64/128");
       p->rows_total = d.batch * d.heads * d.rows;
       p->nsplit = d.segments;
-      if (d.dtype == RF_F32 && d.segments <= 8 &&
+      if (d.dtype == RF_F32 && d.segments <= 8 && d.rows >= 128 &&
           rf::attention_tf32_supports(d.rows, d.len, d.free_len, d.segments) && !std::getenv("RF_ATTN_F32_SIMT")) {
         // tcgen05 (3xTF32): cut the reference slices into up to 8 sub-slices of
         // >= 128 keys (one cluster per 128-row tile) while the grid is below
         // one CTA per SM; the in-kernel fold is the same closed-form sum over
         // the finer slices. RF_ATTN_F32_SIMT=1 keeps the SIMT kernel (A/B only).
         p->kernel = rf::Kernel::AttentionTf32;
-        const int64_t tiles = d.batch * d.heads * (d.rows / 128);
+        const int64_t tiles = d.batch * d.heads * ((d.rows + 127) / 128);
         while (p->nsplit * 2 <= 8 && tiles * p->nsplit < 148 &&
                rf::attention_tf32_supports(d.rows, d.len, d.free_len, p->nsplit * 2))
           p->nsplit *= 2;

@@ -211,6 +211,8 @@ def _plan_run(shape, segments, seed, simt=False):
     ((2, 3, 128, 1024, 64), 1, 8),     # several (b, h)
     ((5, 8, 128, 512, 64), 1, 4),      # a 4-CTA cluster (the grid fills the GPU at 4 sub-slices)
     ((4, 37, 128, 256, 64), 1, 1),     # grid already fills the GPU: one slice, no fold
+    ((2, 3, 200, 512, 64), 1, 4),      # ragged row tiles (Sq % 128 != 0) across heads
+    ((1, 1, 1000, 1024, 64), 8, 8),    # ragged cfg1-like shape
 ])
 def test_fp32_tcgen05_tf32x3(shape, segments, nsplit):
     """The fp32 path on tcgen05 (3xTF32, attn_tf32.cu) with the slice fold in
