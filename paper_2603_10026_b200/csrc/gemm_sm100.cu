@@ -463,7 +463,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 2)
     named_bar_sync(1, 128);
     if (threadIdx.x == 0) {
 #pragma unroll
-      for (int c = 0; c < BN / 64; ++c) tma_store_2d(&ty, s.a[0] + c * (BM * 128), n0 + 64 * c, m0);
+      for (int c = 0; c < BN / 64; ++c) tma_store_2d_hint(&ty, s.a[0] + c * (BM * 128), n0 + 64 * c, m0, kEvictFirst);
       bulk_commit();
       bulk_wait_read0();
     }
@@ -491,7 +491,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 2)
       named_bar_sync(1, 128);
       if (threadIdx.x == 0) {
 #pragma unroll
-        for (int c = 0; c < BN / 64; ++c) tma_store_2d(&ty4, s.a[0] + c * (BM * 128), n0 + 64 * c, m0);
+        for (int c = 0; c < BN / 64; ++c) tma_store_2d_hint(&ty4, s.a[0] + c * (BM * 128), n0 + 64 * c, m0, kEvictFirst);
         bulk_commit();
       }
     }
@@ -1006,7 +1006,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       if (threadIdx.x == 0) {
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-          tma_store_2d(&tc, area[rnd & 1] + c * (BM * 128), n0 + 128 * rnd + 32 * c, crow);
+          tma_store_2d_hint(&tc, area[rnd & 1] + c * (BM * 128), n0 + 128 * rnd + 32 * c, crow, kEvictFirst);
         bulk_commit();
       }
     }
