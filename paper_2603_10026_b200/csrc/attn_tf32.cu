@@ -8,9 +8,12 @@
 // (incr_ingest_element, :566-589) from fresh state over its keys in tiles of
 // 128 (tests/golden/flash_attention_tile.txt's RT = ST = 128), and the slice
 // states fold in slice order (incr_push_child, :592-608; closed form and
-// order in fold.cuh). The SIMT kernel (attn_f32.cu) spends most of cfg1 on
-// shared-memory latency and a second (merge) launch; here both contractions
-// are tcgen05 MMAs and the fold follows a cluster barrier.
+// order in fold.cuh's arithmetic). The SIMT kernel (attn_f32.cu) spends most
+// of cfg1 on shared-memory latency and a second (merge) launch; here both
+// contractions are tcgen05 MMAs and the fold runs inside the cluster: after a
+// cluster barrier every CTA bulk-copies each owner's block of its state into
+// the owner's drained Q tiles (cp.async.bulk shared::cta -> shared::cluster,
+// completing on the owner's mbarrier) and each owner folds its rows locally.
 //
 // fp32 accuracy (<= 1e-5 scaled error, north_star) with kind::tf32 MMAs: each
 // operand x is split as x = hi + lo, hi = tf32(x) (cvt.rna), lo = x - hi
@@ -22,9 +25,11 @@
 //                K-major: transposed while splitting), M=128 N=D K=128
 // TMEM: S / P_hi [0,128), P_lo [128,256), O [256, 256 + D).
 // Two threads per query row (TMEM lane, one per half of the columns) run the
-// online softmax; O is kept
-// unnormalised with the running max and rescaled in TMEM when it grows, and
-// the slice state is (m, l, O / l) — the paper form the fold expects.
+// online softmax; O is kept unnormalised with the running max and rescaled in
+// TMEM when it grows, and the slice state is (m, l, O / l) — the paper form
+// the fold expects. Q and the first K / V tile land by TMA (K raw into the K
+// hi tiles, V staged in the K lo tiles until it is transposed), then every
+// thread splits its own row in place.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
