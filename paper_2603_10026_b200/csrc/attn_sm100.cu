@@ -43,7 +43,22 @@
 __device__ long long g_attn_trace[4096];
 #define RF_TRACE(idx) \
   do { if ((blockIdx.x | blockIdx.y | blockIdx.z) == 0) g_attn_trace[(idx)] = clock64(); } while (0)
+// effective SM clock of CTA 0 per launch: (clock64, globaltimer) at its start and end
+__device__ long long g_attn_clk[64][4];
+__device__ int g_attn_launch;
+#define RF_CLK(slot)                                                                 \
+  do {                                                                               \
+    if ((blockIdx.x | blockIdx.y | blockIdx.z) == 0 && threadIdx.x == 0) {            \
+      long long g_;                                                                  \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));                         \
+      const int l_ = g_attn_launch & 63;                                             \
+      g_attn_clk[l_][2 * (slot)] = clock64();                                        \
+      g_attn_clk[l_][2 * (slot) + 1] = g_;                                           \
+      if ((slot) == 1) g_attn_launch = g_attn_launch + 1;                            \
+    }                                                                                \
+  } while (0)
 #else
+#define RF_CLK(slot) do {} while (0)
 #define RF_TRACE(idx) do {} while (0)
 #endif
 
@@ -99,6 +114,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   Smem<D>& s = *reinterpret_cast<Smem<D>*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  RF_CLK(0);
   const int warp = warp_id();
   const int n_tiles = static_cast<int>(p.slice_len / BN);
   auto unit_of = [&](int u, int& bh, int64_t& q_row0, int64_t& slice) {
@@ -385,6 +401,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 9) tmem_dealloc<512>(tmem);
+  RF_CLK(1);
 }
 
 template <int D>
