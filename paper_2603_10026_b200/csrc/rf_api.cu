@@ -41,7 +41,10 @@ struct rf_plan {
   bool staged = false;
   void* dev_in[4] = {nullptr, nullptr, nullptr, nullptr};
   void* dev_out[4] = {nullptr, nullptr, nullptr, nullptr};
-  cudaStream_t streams[2] = {nullptr, nullptr};
+  // rf_run_host: H2D, compute and D2H streams, and per-chunk events linking them
+  static constexpr int kChunks = 16;
+  cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_in[kChunks] = {}, ev_done[kChunks] = {};
   std::string describe;
 };
 
@@ -676,6 +679,10 @@ void rf_plan_destroy(rf_plan* p) {
   for (void* b : p->dev_out) cudaFree(b);
   for (cudaStream_t s : p->streams)
     if (s) cudaStreamDestroy(s);
+  for (int c = 0; c < rf_plan::kChunks; ++c) {
+    if (p->ev_in[c]) cudaEventDestroy(p->ev_in[c]);
+    if (p->ev_done[c]) cudaEventDestroy(p->ev_done[c]);
+  }
   delete p;
 }
 
@@ -793,11 +800,14 @@ rf_status rf_run_host(rf_plan* p, const rf_host_io* io) {
     for (int i = 0; i < 4; ++i)
       if (out[i]) RF_CUDA_TRY(cudaMalloc(&p->dev_out[i], out[i]));
     for (auto& s : p->streams) RF_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    for (int c = 0; c < rf_plan::kChunks; ++c) {
+      RF_CUDA_TRY(cudaEventCreateWithFlags(&p->ev_in[c], cudaEventDisableTiming));
+      RF_CUDA_TRY(cudaEventCreateWithFlags(&p->ev_done[c], cudaEventDisableTiming));
+    }
     p->staged = true;
   }
   auto drain = [&](rf_status s) {
-    cudaStreamSynchronize(p->streams[0]);
-    cudaStreamSynchronize(p->streams[1]);
+    for (cudaStream_t st : p->streams) cudaStreamSynchronize(st);
     return s;
   };
   for (int i = 0; i < 4; ++i)
@@ -811,16 +821,20 @@ rf_status rf_run_host(rf_plan* p, const rf_host_io* io) {
   if (gemm) dio.in[1] = io->in[1];  // packed weight: plan-time resident device buffer
   const int64_t units = units_of(p);
   if (units == 0 || p->d.rows == 0) return RF_OK;  // empty batch
-  // Chunking: 8 chunks over independent units, alternating two streams, so
-  // the H2D of chunk c+1 and the D2H of chunk c-1 overlap chunk c's kernels.
-  // GEMM chunks are whole 128-row tiles.
+  // Chunking: up to 16 chunks over independent units. The H2D copies run back
+  // to back on their own stream (the link's host-to-device direction never
+  // waits on a download), each chunk's kernels on the compute stream once its
+  // inputs landed (event), and its D2H on a third stream once they finished
+  // (event): PCIe both ways and the kernels overlap. GEMM chunks are whole
+  // 128-row tiles.
   const int64_t gran = p->d.pattern == RF_PATTERN_LAYERNORM_GEMM ? 256 : gemm ? 128 : 1;
-  const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(8, units / gran));
+  const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(rf_plan::kChunks, units / gran));
   const int64_t per = ((units + nchunk - 1) / nchunk + gran - 1) / gran * gran;
+  cudaStream_t s_in = p->streams[0], s_run = p->streams[1], s_out = p->streams[2];
   for (int64_t c = 0; c < nchunk; ++c) {
     const int64_t u0 = c * per, nu = std::min(per, units - u0);
     if (nu <= 0) break;
-    cudaStream_t st = p->streams[c & 1];
+    cudaStream_t st = s_in;
     for (int i = 0; i < 4; ++i) {
       if (!in[i] || (gemm && i == 1)) continue;
       const size_t chunk = in[i] / units * nu, off = in[i] / units * u0;
@@ -829,20 +843,23 @@ rf_status rf_run_host(rf_plan* p, const rf_host_io* io) {
                                             cudaMemcpyHostToDevice, st);
       if (e != cudaSuccess) return drain(fail(RF_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(e)));
     }
-    rf_status s = run_range(p, &dio, u0, nu, st);
+    RF_CUDA_TRY(cudaEventRecord(p->ev_in[c], s_in));
+    RF_CUDA_TRY(cudaStreamWaitEvent(s_run, p->ev_in[c], 0));
+    rf_status s = run_range(p, &dio, u0, nu, s_run);
     // an early return must not leave copies into the caller's host buffers in flight
     if (s != RF_OK) return drain(s);
+    RF_CUDA_TRY(cudaEventRecord(p->ev_done[c], s_run));
+    RF_CUDA_TRY(cudaStreamWaitEvent(s_out, p->ev_done[c], 0));
     for (int i = 0; i < 4; ++i) {
       if (!out[i] || !io->d[i]) continue;
       const size_t chunk = out[i] / units * nu, off = out[i] / units * u0;
       const cudaError_t e = cudaMemcpyAsync(static_cast<char*>(io->d[i]) + off,
                                             static_cast<char*>(p->dev_out[i]) + off, chunk,
-                                            cudaMemcpyDeviceToHost, st);
+                                            cudaMemcpyDeviceToHost, s_out);
       if (e != cudaSuccess) return drain(fail(RF_ERR_CUDA, std::string("D2H: ") + cudaGetErrorString(e)));
     }
   }
-  RF_CUDA_TRY(cudaStreamSynchronize(p->streams[0]));
-  RF_CUDA_TRY(cudaStreamSynchronize(p->streams[1]));
+  for (cudaStream_t st : p->streams) RF_CUDA_TRY(cudaStreamSynchronize(st));
   return RF_OK;
 }
 
