@@ -272,6 +272,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_wait(&s.s_full[k], g & 1);
         tc_fence_after();
         if ((threadIdx.x & 127) == 0 && uc == 0) RF_TRACE(512 * k + 4 * i + 0);
+        if (threadIdx.x == 0 && i == 0 && uc < 32) RF_TRACE(2048 + 2 * uc);  // unit start (softmax 0, S_0 ready)
         float tmax;
         {
           // pass 1 (reduction 1): d1 = max(d1, max_tile) over the 4 chunks in flight
@@ -351,6 +352,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc_fence_before();
         __syncwarp();
         if ((threadIdx.x & 127) == 0 && uc == 0) RF_TRACE(512 * k + 4 * i + 2);
+        if (threadIdx.x == 0 && i + 1 == n_tiles && uc < 32) RF_TRACE(2048 + 2 * uc + 1);  // unit's last P released
         if ((threadIdx.x & 31) == 0) mbar_arrive(&s.p_full[k]);
       }
       // ---- finalize (finalize_root): d2 re-based to the true d1, d3 = O / d2 ----

@@ -36,6 +36,12 @@ per = [(t[4 * (i + 1)] - t[4 * i]) for i in range(n - 1)]
 print("cycles per tile (softmax0 S-ready to S-ready):", sorted(per)[len(per) // 2])
 sm = [t[4 * i + 2] - t[4 * i] for i in range(n)]
 print("softmax0 busy per tile (S ready -> P released):", sorted(sm)[len(sm) // 2])
+# units of CTA 0: start (S_0 ready) / end (last P released), cycles relative to unit 0's start
+us = [(t[2048 + 2 * u], t[2048 + 2 * u + 1]) for u in range(32) if t[2048 + 2 * u]]
+print("CTA 0 units: duration, gap to the next unit's first S (cycles)")
+for u, (a, b) in enumerate(us):
+    gap = us[u + 1][0] - b if u + 1 < len(us) else 0
+    print(f"  unit {u:2d}: start {a - us[0][0]:9d} dur {b - a:7d} gap {gap:6d}")
 
 # ---- the 2-SM (CTA pair) kernel: first cluster ----
 h.rf_probe_attn2_trace.restype = ctypes.c_int
