@@ -18,6 +18,7 @@ struct Mode {
   int ts;      // A from TMEM
   int n;       // N per MMA
   int halves;  // MMAs per K sub-step (N halves)
+  int m = 256; // pair M (128: 64 rows per CTA, the MLA kernel's form)
 };
 
 __device__ __forceinline__ void mma_f8_ts_2sm(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
@@ -36,7 +37,7 @@ struct Smem {
 };
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
-    rate_kernel(int kind, int ts, int n, int halves, int reps, long long* out) {
+    rate_kernel(int kind, int ts, int n, int halves, int reps, long long* out, int m = 256) {
   extern __shared__ uint8_t raw[];
   Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   const bool leader = cluster_ctarank() == 0;
@@ -56,7 +57,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
   const uint32_t tmem = s.tmem_base;
   if (leader && threadIdx.x < 32) {
     const bool el = elect_one();
-    const uint32_t id = kind == 0 ? idesc_f8(256, n) : idesc_f16(256, n, kFmtBF16, false, false);
+    const uint32_t id = kind == 0 ? idesc_f8(m, n) : idesc_f16(m, n, kFmtBF16, false, false);
     const int ksub = 4;  // 128 B of K per row: 4 x K=32 (fp8) or 4 x K=16 (bf16)
     const uint32_t acol = 448;           // TS: A operand columns (32 per K tile)
     long long t0 = clock64();
@@ -154,6 +155,8 @@ int main() {
       {"bf16 SS N=256 x2", 1, 0, 256, 2},      {"bf16 TS N=224 x2", 1, 1, 224, 2},
       {"bf16 SS N=128 x1 (M=256)", 1, 0, 128, 1}, {"bf16 TS N=128 x1 (M=256)", 1, 1, 128, 1},
       {"bf16 SS N=256 x1 (M=256)", 1, 0, 256, 1}, {"bf16 SS N=128 x2 (M=256)", 1, 0, 128, 2},
+      {"bf16 SS N=128 x1 (M=128, MLA S)", 1, 0, 128, 1, 128}, {"bf16 SS N=256 x1 (M=128, MLA PV)", 1, 0, 256, 1, 128},
+      {"bf16 TS N=256 x1 (M=128)", 1, 1, 256, 1, 128},
   };
   const int pairs = 74, reps = 512;
   long long* out;
@@ -161,7 +164,7 @@ int main() {
   const size_t smem = sizeof(Smem) + 1024;
   cudaFuncSetAttribute(rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   for (const Mode& m : modes) {
-    for (int it = 0; it < 2; ++it) rate_kernel<<<2 * pairs, 128, smem>>>(m.kind, m.ts, m.n, m.halves, reps, out);
+    for (int it = 0; it < 2; ++it) rate_kernel<<<2 * pairs, 128, smem>>>(m.kind, m.ts, m.n, m.halves, reps, out, m.m);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
       printf("%s: %s\n", m.name, cudaGetErrorString(e));
@@ -175,7 +178,7 @@ int main() {
       sum += v;
     }
     // floor per CTA: M = 128 rows per SM, 8192 (f8) / 4096 (bf16) MAC per clock per SM
-    const double macs = 128.0 * m.n * (m.kind == 0 ? 128.0 : 64.0) * m.halves;  // one 128-byte K tile
+    const double macs = (m.m / 2.0) * m.n * (m.kind == 0 ? 128.0 : 64.0) * m.halves;  // one 128-byte K tile, per CTA
     const double floor_cyc = macs / (m.kind == 0 ? 8192.0 : 4096.0);
     const double per = static_cast<double>(sum) / 74 / reps;
     printf("%-26s cycles per K tile: %7.1f (floor %6.1f) -> %.3f of peak (max-pair %.1f)\n", m.name, per,
