@@ -180,6 +180,12 @@ const char* kernel_name(rf::Kernel k) {
   return "?";
 }
 
+// Row coordinates of the flattened [B*H*S, D] attention views fit the TMA
+// kernels' 32-bit coordinates.
+bool tma_rows_fit(const rf_desc& d) {
+  return d.batch * d.heads * std::max<int64_t>(d.rows, d.len) < (int64_t{1} << 31);
+}
+
 // Decode split count: a multiple of `segments` dividing Skv with slices of at
 // least 512 keys, aiming at >= 4 CTAs per SM worth of (row, slice) units.
 int64_t pick_decode_splits(int64_t rows, int64_t skv, int64_t segments) {
@@ -535,7 +541,9 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
         return bail(RF_ERR_UNSUPPORTED, "attention: head_dim must be 16/32/64/128");
       p->rows_total = d.batch * d.heads * d.rows;
       p->nsplit = d.segments;
-      if (d.dtype == RF_F32 && d.segments <= 8 && d.rows >= 128 &&
+      // (tma_rows_fit: the TMA kernels address rows of the flattened
+      // [B*H*S, D] views with 32-bit coordinates)
+      if (d.dtype == RF_F32 && d.segments <= 8 && d.rows >= 128 && tma_rows_fit(d) &&
           rf::attention_tf32_supports(d.rows, d.len, d.free_len, d.segments) && !std::getenv("RF_ATTN_F32_SIMT")) {
         // tcgen05 (3xTF32): cut the reference slices into up to 8 sub-slices of
         // >= 128 keys (one cluster per 128-row tile) while the grid is below
@@ -560,7 +568,7 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
       } else if (d.rows == 1) {
         p->kernel = rf::Kernel::AttentionDecode;
         p->nsplit = pick_decode_splits(d.batch * d.heads, d.len, d.segments);
-      } else if (rf::attention_sm100_supports(d.rows, d.len, d.free_len, d.segments)) {
+      } else if (tma_rows_fit(d) && rf::attention_sm100_supports(d.rows, d.len, d.free_len, d.segments)) {
         p->kernel = rf::Kernel::AttentionSm100;
       } else {
         p->kernel = rf::Kernel::AttentionF32;  // SIMT CUDA path for odd shapes
