@@ -173,7 +173,10 @@ class ClockSampler:
         med = statistics.median(sm) if sm else None
         loaded = [x for x in sm if med is None or x >= 0.8 * med]
         return {"sm_mhz": statistics.median(loaded) if loaded else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows),
+                "note": ("nvidia-smi clock counters refresh every ~100 ms, longer than short timed windows; "
+                         "under sw_power_cap the device-side clock of the tensor-bound kernels is lower "
+                         "(cfg2: profiles/r2g_attn_effective_clock.txt, tools/attn_clock.py)")}
 
 
 def cpu_reference(cfg, budget_s=12.0, threads=None):
