@@ -173,7 +173,7 @@ const char* kernel_name(rf::Kernel k) {
     case rf::Kernel::MoeRouting: return "moe_routing (SIMT, warp per token, bit-exact top-k)";
     case rf::Kernel::LayerNormGemmSm100: return "layernorm_gemm_sm100 (bf16 tcgen05 cta_group::2)";
     case rf::Kernel::RowStats: return "rowstats (SIMT HBM streaming, fp64 accumulation)";
-    case rf::Kernel::MoeRouter: return "moe_router (tcgen05 split-K router GEMM + routing cascade)";
+    case rf::Kernel::MoeRouter: return "moe_router (tcgen05 split-K router GEMM + L2 split exchange + routing cascade, one launch)";
     case rf::Kernel::MlaDecode: return "mla_decode (tcgen05, 128 heads x latent cache, split-KV)";
     case rf::Kernel::FusedRows: return "fused_rows (run_fused: warp-buffered level-1 segments, SIMT)";
   }
@@ -337,6 +337,7 @@ rf_status run_range(const rf_plan* p, const rf_io* io, int64_t u0, int64_t nu, c
       r.x = static_cast<const char*>(io->in[0]) + 2 * u0 * d.producer_len;
       r.w = io->in[1];
       r.part = p->ws_m + u0 * d.len;
+      r.cnt = reinterpret_cast<unsigned long long*>(p->ws_l) + u0 / 128;
       r.rows = nu;
       r.hd = d.producer_len;
       r.experts = d.len;
@@ -637,8 +638,7 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
   if (is_gemm(p->d.pattern) && p->d.pattern != RF_PATTERN_MOE_ROUTER) p->nsplit = p->d.segments;
   p->launches = (((p->d.pattern == RF_PATTERN_ATTENTION || p->d.pattern == RF_PATTERN_MLA_DECODE) &&
                   p->nsplit > 1 && p->kernel != rf::Kernel::AttentionTf32) ||
-                 p->d.pattern == RF_PATTERN_MOE_ROUTER ||
-                 (is_gemm(p->d.pattern) && p->nsplit > 1)) ? 2 : 1;
+                 (is_gemm(p->d.pattern) && p->d.pattern != RF_PATTERN_MOE_ROUTER && p->nsplit > 1)) ? 2 : 1;
 
   // ---- persistent workspace ----
   if (cudaMalloc(&p->domain_flag, sizeof(int)) != cudaSuccess ||
@@ -660,8 +660,11 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
       return bail(RF_ERR_CUDA, "multi-segment GEMM workspace allocation failed");
   }
   if (p->d.pattern == RF_PATTERN_MOE_ROUTER) {  // split-K partial scores (L2-resident)
+    // + one arrival counter per 128-token row tile (the split CTAs of a tile meet on it)
     const size_t n = static_cast<size_t>(p->nsplit) * p->d.rows * p->d.len;
-    if (n && cudaMalloc(&p->ws_m, n * sizeof(float)) != cudaSuccess)
+    const size_t nc = static_cast<size_t>((p->d.rows + 127) / 128 + 1) * sizeof(unsigned long long);
+    if ((n && cudaMalloc(&p->ws_m, n * sizeof(float)) != cudaSuccess) || cudaMalloc(&p->ws_l, nc) != cudaSuccess ||
+        cudaMemset(p->ws_l, 0, nc) != cudaSuccess)
       return bail(RF_ERR_CUDA, "router workspace allocation failed");
   }
   char buf[512];

@@ -52,6 +52,7 @@ struct RouterArgs {
   const void* x;        // [rows, hd] bf16
   const void* w;        // packed [experts, hd] bf16
   float* part;          // split partials [splits, part_stride, experts] (+ row offset)
+  unsigned long long* cnt;  // per-row-tile arrival counters (zeroed at plan creation, only grow)
   int64_t rows, hd, experts, splits, part_stride;
   int k;                // K' (top-k size)
   float* d1;

@@ -8,8 +8,11 @@
 // 64-bit key per candidate: every round is two warp reductions (redux.sync
 // max of the value bits, then max of the low word among the lanes holding
 // them), so the winner is unique and the indices are bit-exact regardless of
-// the reduction order; the owning lane then retires the winner (a 5-step
-// 64-bit shuffle butterfly per round before). Round 1's winner is d1 (exact max), after which d2 is a
+// the reduction order; each lane keeps its keys sorted, so a round reduces
+// only the heads and the owning lane pops the winner (a 5-step 64-bit
+// shuffle butterfly per round in round 1; the sorted heads take routing of
+// 128 experts / top-8 from ~1300 to ~980 cycles per token including d2,
+// experimental/bench_route.cu). Round 1's winner is d1 (exact max), after which d2 is a
 // warp sum of exp(s - d1) — the incremental Eq.17 rescaling collapses because
 // the whole row is already in registers (one pass over memory).
 #pragma once
@@ -48,23 +51,33 @@ __device__ __forceinline__ void warp_route(const float (&x)[PER], int experts, i
     const int e = lane + 32 * j;
     key[j] = route_key(x[j], e < experts ? e + 1 : 0);
   }
+  // each lane's keys sorted descending (odd-even transposition, once): a
+  // round then only reduces the lanes' heads and the winner pops its head
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+#pragma unroll
+    for (int j = i & 1; j + 1 < PER; j += 2) {
+      const uint64_t a = key[j], b = key[j + 1];
+      key[j] = a > b ? a : b;
+      key[j + 1] = a > b ? b : a;
+    }
+  }
   float m = -INFINITY;
   int2 rec = make_int2(0, 0);
 #pragma unroll
   for (int r = 0; r < K; ++r) {
-    uint64_t best = key[0];
-#pragma unroll
-    for (int j = 1; j < PER; ++j) best = key[j] > best ? key[j] : best;
     // warp argmax as two warp reductions (redux.sync): the largest value
     // bits, then the largest ~index among the lanes holding them — the same
     // total order as a 64-bit max, without a 5-step 64-bit shuffle butterfly
-    const uint32_t hi = static_cast<uint32_t>(best >> 32);
+    const uint32_t hi = static_cast<uint32_t>(key[0] >> 32);
     const uint32_t hmax = __reduce_max_sync(0xffffffffu, hi);
-    const uint32_t lo = __reduce_max_sync(0xffffffffu, hi == hmax ? static_cast<uint32_t>(best) : 0u);
-    best = (static_cast<uint64_t>(hmax) << 32) | lo;
-    // the owning lane retires the winner
+    const uint32_t lo = __reduce_max_sync(0xffffffffu, hi == hmax ? static_cast<uint32_t>(key[0]) : 0u);
+    const uint64_t best = (static_cast<uint64_t>(hmax) << 32) | lo;
+    // the owning lane retires the winner (pops its head)
+    const bool mine = key[0] == best;
 #pragma unroll
-    for (int j = 0; j < PER; ++j) key[j] = key[j] == best ? 0ull : key[j];
+    for (int j = 0; j + 1 < PER; ++j) key[j] = mine ? key[j + 1] : key[j];
+    key[PER - 1] = mine ? 0ull : key[PER - 1];
     const bool found = best != 0ull;
     if (r == 0) m = found ? route_value(best) : -INFINITY;
     if (lane == r && found) rec = make_int2(__float_as_int(route_value(best)), route_index(best));

@@ -1,8 +1,10 @@
 """Timeline of the MoE router (cfg7 shape, L2 flushed before the call) from a
 build with -DRF_ROUTER_TRACE. Usage (GPU box):
   python tools/trace_router.py <traced librf_cuda.so>
-GEMM CTAs: start / setup done / first K tile landed / last K tile landed /
-accumulator ready / split fold done; route CTAs: resident / dependency released."""
+Build: nvcc ... -DRF_ROUTER_TRACE (see the librf_cuda Makefile flags) into a
+separate .so. Per CTA: start / warp 0's partials summed / first K tile landed / last K tile
+landed / accumulator ready / partial slices written / row tile's counter met /
+slice routed."""
 import ctypes
 import os
 import sys
@@ -33,10 +35,7 @@ g, r = list(g), list(r)
 n = 128
 t0 = min(g[8 * i] for i in range(n) if g[8 * i])
 q = lambda v: [round((x - t0) / 1000, 2) for x in (v[0], v[len(v) // 4], v[len(v) // 2], v[3 * len(v) // 4], v[-1])]  # noqa: E731
-for j, name in enumerate(["start", "setup", "tile0 landed", "last tile landed", "acc ready", "fold done",
-                          "staged", "cluster synced"]):
+for j, name in enumerate(["start", "summed (warp 0)", "tile0 landed", "last tile landed", "acc ready",
+                          "partials written", "counter met", "routed"]):
     v = sorted(g[8 * i + j] for i in range(n) if g[8 * i + j])
     print(f"gemm {name:16s} (min/q1/med/q3/max us):", q(v))
-for j, name in enumerate(["resident", "released", "routed (thread 0)"]):
-    v = sorted(r[3 * i + j] for i in range(256) if r[3 * i + j])
-    print(f"route {name:15s}:", q(v))
