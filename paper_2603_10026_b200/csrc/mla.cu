@@ -38,6 +38,8 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 
 #include "rf_internal.h"
 #include "sm100.cuh"
@@ -69,10 +71,10 @@ extern "C" int rf_mla_fold_trace_read(unsigned long long* out) {
 }
 #define FT_STAMP(i)                                                                   \
   do {                                                                                \
-    if (threadIdx.x == 0 && blockIdx.x < 1024) {                                      \
+    if (threadIdx.x == 0 && blockIdx.y * 2 + blockIdx.x < 1024) {                     \
       unsigned long long v_;                                                          \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v_));                         \
-      g_fold_trace[blockIdx.x][(i)] = v_;                                             \
+      g_fold_trace[blockIdx.y * 2 + blockIdx.x][(i)] = v_;                            \
     }                                                                                 \
   } while (0)
 #else
@@ -116,15 +118,17 @@ struct Smem {
   uint64_t q_full, kfull[NKR], kempty[NKR], vfull[NVR], vempty[NVR];
   uint64_t q_empty, s_full[2], p_full[2], pv_done[2], o_full, o_empty;
   uint32_t tmem_base;
+  int nfold;                          // batch segments of this CTA folded at the end (<= 2)
+  int fold_b[2], fold_slot[2], fold_nseg[2];
 };
+
+constexpr int kMaxClusters = 74;  // CTA pairs resident on a 148-SM B200
 
 struct Params {
   int64_t skv, rows_total;
   int tpb;        // 128-key tiles per batch
-  int64_t total;  // cost units of the whole grid (bs x (tpb + kSegCost))
   int clusters;   // CTA pairs (= gridDim.y)
   int nslots;     // partial slots per batch (1: direct output)
-  bool fast32;    // (total + 1) * clusters < 2^32: 32-bit segment math
   float scale;
   __nv_bfloat16* o;
   float* m;
@@ -132,151 +136,156 @@ struct Params {
   float* part_m;
   float* part_l;
   float* part_o;
+  unsigned long long* cnt;  // [bs, 2] arrivals per batch half (multiples of kCntStride between launches)
+  // Range of CTA pair k: flattened tiles [cut[k], cut[k + 1]) of the (batch,
+  // tile) sequence, every range non-empty (host: balanced_cuts).
+  int64_t cut[kMaxClusters + 1];
 };
 
 // Range scheduling: the flattened (batch, tile) sequence is cut into
 // `clusters` contiguous ranges, one per CTA pair; a range covers one or more
 // batch segments, each of which writes a partial (m, l, O/l) state to slot
-// (cluster - first cluster of that batch). Ranges are balanced in a cost
-// space where every batch starts with kSegCost virtual tiles: a cluster that
-// crosses into a new batch pays a Q reload (72 KB, no second Q buffer fits)
-// and one more epilogue, worth about three tiles' time.
-constexpr int64_t kSegCost = 3;  // A/B on L3: 0 -> 48.1, 1 -> 48.2, 2 -> 46.7, 3 -> 45.8, 4 -> 46.4 us
-// The index math runs in 32 bits when (units + 1) * clusters fits (Params::
-// fast32): a 64-bit division is a long software sequence and every role
-// re-derives its segments (measured ~0.1 us per launch on L3).
-template <typename T>
-__host__ __device__ __forceinline__ T range_start(T k, T clusters, T units) {
-  return k * units / clusters;
-}
-template <typename T>
-__host__ __device__ __forceinline__ T cluster_of(T u, T clusters, T units) {
-  return ((u + 1) * clusters - 1) / units;
-}
-// First / last cluster holding tiles of batch b (w = tpb + kSegCost).
-template <typename T>
-__host__ __device__ __forceinline__ T first_cluster(T b, T w, T clusters, T units) {
-  return cluster_of<T>(b * w + kSegCost, clusters, units);
-}
-template <typename T>
-__host__ __device__ __forceinline__ T last_cluster(T b, T w, T clusters, T units) {
-  return cluster_of<T>((b + 1) * w - 1, clusters, units);
+// (cluster - first cluster of that batch). The cuts are chosen on the host
+// (balanced_cuts) to minimise the largest range cost, where a range costs its
+// tiles plus `seg` tiles for every batch it switches to after its first: a
+// switch inside a range pays a Q reload (72 KB; no second Q buffer fits) and
+// one more epilogue. (Round 1 charged every batch START a fixed number of
+// virtual tiles in a uniform cost space, which also discounted ranges that
+// merely began at a batch start: their CTAs ended up to ~7 us early on L3.)
+
+// Pair holding flattened tile x: the last k with cut[k] <= x.
+__host__ __device__ __forceinline__ int cluster_of_tile(const int64_t* cut, int clusters, int64_t x) {
+  int lo = 0, hi = clusters - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (cut[mid] <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
 }
 
 struct Segment {
   int b, t0, t1, slot, nseg;  // nseg: segments (ranges) the batch is cut into
 };
-template <typename T>
-__device__ __forceinline__ bool segment_t(const Params& p, int k, int i, Segment& sg) {
-  const T w = static_cast<T>(p.tpb + kSegCost), cl = static_cast<T>(p.clusters), un = static_cast<T>(p.total);
-  const T x1 = range_start<T>(static_cast<T>(k + 1), cl, un);
-  T x = range_start<T>(static_cast<T>(k), cl, un);
-  for (int j = 0; x < x1;) {
-    const T b = x / w;
-    const T lo = x > b * w + kSegCost ? x : b * w + kSegCost;
-    const T hi = x1 < (b + 1) * w ? x1 : (b + 1) * w;
-    x = (b + 1) * w;
-    if (hi <= lo) continue;  // only the batch's virtual head
-    if (j++ == i) {
+// Segment `i` of pair k's range; false when the range is exhausted.
+__device__ __forceinline__ bool segment(const Params& p, int k, int i, Segment& sg) {
+  const int64_t x1 = p.cut[k + 1];
+  int64_t x = p.cut[k];
+  for (int j = 0; x < x1; ++j) {
+    const int64_t b = x / p.tpb;
+    const int64_t hi = x1 < (b + 1) * p.tpb ? x1 : (b + 1) * p.tpb;
+    if (j == i) {
       sg.b = static_cast<int>(b);
-      sg.t0 = static_cast<int>(lo - b * w - kSegCost);
-      sg.t1 = static_cast<int>(hi - b * w - kSegCost);
-      const T k0 = first_cluster<T>(b, w, cl, un);
-      sg.slot = static_cast<int>(static_cast<T>(k) - k0);
-      sg.nseg = static_cast<int>(last_cluster<T>(b, w, cl, un) - k0 + 1);
+      sg.t0 = static_cast<int>(x - b * p.tpb);
+      sg.t1 = static_cast<int>(hi - b * p.tpb);
+      const int k0 = cluster_of_tile(p.cut, p.clusters, b * p.tpb);
+      sg.slot = k - k0;
+      sg.nseg = cluster_of_tile(p.cut, p.clusters, (b + 1) * p.tpb - 1) - k0 + 1;
       return true;
     }
+    x = hi;
   }
   return false;
 }
-// Segment `i` of cluster k's range; false when the range is exhausted.
-__device__ __forceinline__ bool segment(const Params& p, int k, int i, Segment& sg) {
-  return p.fast32 ? segment_t<uint32_t>(p, k, i, sg) : segment_t<int64_t>(p, k, i, sg);
+
+// Fold of a batch's segment partials (the Multi-Segment merge,
+// incr_push_child / acceptance.cpp:162-178 closed form, as fold.cuh, in slot
+// order), inside the decode kernel: every CTA whose range cut a batch arrives
+// on the batch half's counter once its partial is written; after its last
+// segment it waits for the other segments of that batch and folds its share
+// of the half's 64 heads (share = its slot of ns). All CTAs are co-resident
+// (cooperative launch, one CTA per SM), so the wait cannot starve a producer.
+// Round 1 ran this as a second kernel (programmatic dependent launch): its
+// launch gap and serial drain cost ~5 us of the 45 us L3 step.
+// Warp = one head row; lane = 4 float4 columns 512 B apart; two slots'
+// (m, l, O) loads per round trip.
+constexpr unsigned long long kCntStride = 128;  // > any slot count (<= kMaxClusters)
+
+__device__ __forceinline__ unsigned long long atom_add_acq_rel_u64(unsigned long long* p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
-// Fold of each batch's segment partials (the Multi-Segment merge,
-// incr_push_child / acceptance.cpp:162-178 closed form, as fold.cuh, in slot
-// order) over exactly the segments the batch was cut into. A programmatic
-// dependent of mla_decode_kernel (launch overlaps the decode grid's drain;
-// griddepcontrol.wait orders the reads). Triggering it at the decode
-// kernel's start, so fold CTAs sit resident next to the decode CTAs, measured
-// ~1% slower.
-// CTA = 8 heads of one batch; thread = (head, 4 float4 columns 512 B apart:
-// a warp reads whole rows); two slots' (m, l, O) loads per round trip.
-constexpr int FR = 8;  // heads per fold CTA
-__global__ void __launch_bounds__(256, 4) mla_fold_kernel(const Params p) {
-  FT_STAMP(0);
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  FT_STAMP(1);
-  const int b = blockIdx.x / (HN / FR), blk = blockIdx.x % (HN / FR);
-  const int64_t w = p.tpb + kSegCost;
-  const int ns = static_cast<int>(last_cluster<int64_t>(b, w, p.clusters, p.total) -
-                                  first_cluster<int64_t>(b, w, p.clusters, p.total) + 1);
-  if (ns == 1) return;  // written directly by its only segment
-  const int r = threadIdx.x >> 5, c0 = threadIdx.x & 31;
-  const int64_t grow = static_cast<int64_t>(b) * HN + blk * FR + r;
-  // one round trip per 2 slots: (m, l) and the O rows are loaded together
-  // (every slot of the batch is written, so its O row is valid); the slot
-  // maxima are folded by re-basing, as fold.cuh does across its rounds
-  float m = -INFINITY, L = 0.f;
-  float4 acc[4];
+// NR head rows per warp at once (all their loads in flight together).
+template <int NR>
+__device__ __forceinline__ void fold_rows(const Params& p, const int64_t (&grow)[NR], int ns, int c0) {
+  float m[NR], L[NR];
+  float4 acc[NR][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int q = 0; q < NR; ++q) {
+    m[q] = -INFINITY;
+    L[q] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[q][i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   for (int e0 = 0; e0 < ns; e0 += 2) {
-    float ms[2], ls[2];
-    float4 o[2][4];
+    float ms[NR][2], ls[NR][2];
+    float4 o[NR][2][4];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int e = e0 + j < ns ? e0 + j : ns - 1;  // (duplicates are dropped below)
-      ms[j] = __ldcg(p.part_m + e * p.rows_total + grow);
-      ls[j] = __ldcg(p.part_l + e * p.rows_total + grow);
-      const float4* src = reinterpret_cast<const float4*>(p.part_o + (e * p.rows_total + grow) * DV) + c0;
+    for (int q = 0; q < NR; ++q)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) o[j][i] = __ldcg(src + 32 * i);
-    }
-    float mr = m;
+      for (int j = 0; j < 2; ++j) {
+        const int e = e0 + j < ns ? e0 + j : ns - 1;  // (duplicates are dropped below)
+        ms[q][j] = __ldcg(p.part_m + e * p.rows_total + grow[q]);
+        ls[q][j] = __ldcg(p.part_l + e * p.rows_total + grow[q]);
+        const float4* src = reinterpret_cast<const float4*>(p.part_o + (e * p.rows_total + grow[q]) * DV) + c0;
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
-      if (e0 + j < ns) mr = fmaxf(mr, ms[j]);
-    if (mr != m && L != 0.f) {  // re-base what is accumulated
-      const float f = __expf(m - mr);
-      L *= f;
+        for (int i = 0; i < 4; ++i) o[q][j][i] = __ldcg(src + 32 * i);
+      }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        acc[i].x *= f;
-        acc[i].y *= f;
-        acc[i].z *= f;
-        acc[i].w *= f;
+    for (int q = 0; q < NR; ++q) {
+      float mr = m[q];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (e0 + j < ns) mr = fmaxf(mr, ms[q][j]);
+      if (mr != m[q] && L[q] != 0.f) {  // re-base what is accumulated
+        const float f = __expf(m[q] - mr);
+        L[q] *= f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc[q][i].x *= f;
+          acc[q][i].y *= f;
+          acc[q][i].z *= f;
+          acc[q][i].w *= f;
+        }
+      }
+      m[q] = mr;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const float w = e0 + j < ns && ls[q][j] != 0.f ? ls[q][j] * __expf(ms[q][j] - m[q]) : 0.f;
+        if (w == 0.f) continue;
+        L[q] += w;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc[q][i].x = fmaf(o[q][j][i].x, w, acc[q][i].x);
+          acc[q][i].y = fmaf(o[q][j][i].y, w, acc[q][i].y);
+          acc[q][i].z = fmaf(o[q][j][i].z, w, acc[q][i].z);
+          acc[q][i].w = fmaf(o[q][j][i].w, w, acc[q][i].w);
+        }
       }
     }
-    m = mr;
+  }
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const float w = e0 + j < ns && ls[j] != 0.f ? ls[j] * __expf(ms[j] - m) : 0.f;
-      if (w == 0.f) continue;
-      L += w;
+  for (int q = 0; q < NR; ++q) {
+    const float inv = 1.f / L[q];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        acc[i].x = fmaf(o[j][i].x, w, acc[i].x);
-        acc[i].y = fmaf(o[j][i].y, w, acc[i].y);
-        acc[i].z = fmaf(o[j][i].z, w, acc[i].z);
-        acc[i].w = fmaf(o[j][i].w, w, acc[i].w);
-      }
+    for (int i = 0; i < 4; ++i) {
+      uint2 v;
+      v.x = pack_bf16x2(acc[q][i].x * inv, acc[q][i].y * inv);
+      v.y = pack_bf16x2(acc[q][i].z * inv, acc[q][i].w * inv);
+      *reinterpret_cast<uint2*>(p.o + grow[q] * DV + 4 * (c0 + 32 * i)) = v;
+    }
+    if (c0 == 0) {
+      p.m[grow[q]] = m[q];
+      p.l[grow[q]] = L[q];
     }
   }
-  const float inv = 1.f / L;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    uint2 v;
-    v.x = pack_bf16x2(acc[i].x * inv, acc[i].y * inv);
-    v.y = pack_bf16x2(acc[i].z * inv, acc[i].w * inv);
-    *reinterpret_cast<uint2*>(p.o + grow * DV + 4 * (c0 + 32 * i)) = v;
-  }
-  if (c0 == 0) {
-    p.m[grow] = m;
-    p.l[grow] = L;
-  }
-  FT_STAMP(2);
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
@@ -314,7 +323,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     mbar_init(&s.o_full, 1);
     mbar_init(&s.o_empty, 8);  // both CTAs' epilogues have drained their O
     fence_barrier_init();
+    s.nfold = 0;
   }
+  unsigned long long fold_old[2] = {0, 0};  // thread 0: the counters before its arrivals
   if (warp == 5) tmem_alloc_2sm<512>(&s.tmem_base);
   tc_fence_before();
   cluster_sync();
@@ -602,6 +613,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
           __syncwarp();
         }
       }
+      if (!direct) {  // partial written: arrive on this batch half's counter (release; acquire for the fold)
+        named_bar_sync(1, 128);
+        if (lane == 0) {
+          const int f = s.nfold++;
+          if (f >= 2) __trap();  // only a range's first and last segments can be cut
+          s.fold_b[f] = sg.b;
+          s.fold_slot[f] = sg.slot;
+          s.fold_nseg[f] = sg.nseg;
+          fold_old[f] = atom_add_acq_rel_u64(p.cnt + 2 * sg.b + h, 1ull);
+        }
+      }
     }
   }
   if (threadIdx.x == 0) MT_STAMP(63, 1);
@@ -615,6 +637,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   tc_fence_before();
   cluster_sync();  // no remote traffic into a CTA that has exited
   if (warp == 5) tmem_dealloc_2sm<512>(tmem);
+  // ---- fold of the batches this CTA's range cut (heads [64 h, +64) of each) ----
+  const int nfold = s.nfold;  // written by thread 0 before the cluster barrier
+  for (int f = 0; f < nfold; ++f) {
+    const int b = s.fold_b[f], slot = s.fold_slot[f], ns = s.fold_nseg[f];
+    if (threadIdx.x == 0) {
+      FT_STAMP(0);
+      unsigned long long* c = p.cnt + 2 * b + h;
+      const unsigned long long old = fold_old[f], target = old - old % kCntStride + ns;
+      if (old + 1 == target) atomicAdd(c, kCntStride - ns);  // last arrival: pad to the next launch's base
+      else
+        while (ld_acquire_u64(c) < target) {
+        }
+      FT_STAMP(1);
+    }
+    __syncthreads();
+    const int r0 = slot * HC / ns, r1 = (slot + 1) * HC / ns;
+    const int64_t g0 = static_cast<int64_t>(b) * HN + h * HC;
+    int r = r0 + warp;
+    for (; r + NT / 32 < r1; r += 2 * (NT / 32)) {  // two rows per warp in flight
+      const int64_t g[2] = {g0 + r, g0 + r + NT / 32};
+      fold_rows<2>(p, g, ns, threadIdx.x & 31);
+    }
+    if (r < r1) {
+      const int64_t g[1] = {g0 + r};
+      fold_rows<1>(p, g, ns, threadIdx.x & 31);
+    }
+    if (threadIdx.x == 0) FT_STAMP(2);
+  }
 }
 
 }  // namespace
@@ -624,22 +674,72 @@ bool mla_supports(int64_t heads, int64_t skv, int64_t dv, int64_t dqk, int64_t s
 }
 
 namespace {
-constexpr int64_t kMaxClusters = 74;  // CTA pairs resident on a 148-SM B200
+// Virtual tiles charged for a batch switch inside a range (RF_MLA_SEG overrides, for A/B).
+int64_t switch_cost() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("RF_MLA_SEG");
+    return e != nullptr ? static_cast<int64_t>(std::atoi(e)) : int64_t{4};
+  }();
+  return v;
+}
 
-int64_t slots_needed(int64_t bs, int64_t tpb, int64_t clusters) {
-  const int64_t w = tpb + kSegCost, units = bs * w;
-  int64_t n = 1;
-  for (int64_t b = 0; b < bs; ++b)
-    n = std::max(n, last_cluster<int64_t>(b, w, clusters, units) - first_cluster<int64_t>(b, w, clusters, units) + 1);
+// Greedy ranges of cost <= cap (a range's cost: its tiles + seg per batch it
+// switches to after its first); returns the number of ranges, fills cut[]
+// when given (at most `limit` ranges are written).
+int64_t greedy_cuts(int64_t bs, int64_t tpb, int64_t seg, int64_t cap, int64_t limit, int64_t* cut) {
+  const int64_t total = bs * tpb;
+  int64_t x = 0, n = 0;
+  while (x < total) {
+    if (cut != nullptr && n < limit) cut[n] = x;
+    ++n;
+    int64_t cost = 0;
+    bool first = true;
+    while (x < total) {
+      const int64_t end_b = (x / tpb + 1) * tpb;
+      const int64_t extra = first ? 0 : seg;
+      const int64_t take = std::min(end_b - x, cap - cost - extra);
+      if (take <= 0) break;
+      cost += extra + take;
+      x += take;
+      first = false;
+      if (x < end_b) break;  // the range is full inside this batch
+    }
+  }
+  if (cut != nullptr && n <= limit) cut[n] = total;
   return n;
 }
 
-// The most CTA pairs (<= one per SM pair, <= one per tile) whose ranges cut
-// no batch into more than max_slots segments.
-int64_t pick_clusters(int64_t bs, int64_t tpb, int64_t max_slots) {
-  int64_t c = std::min(kMaxClusters, bs * tpb);
-  while (c > 1 && slots_needed(bs, tpb, c) > max_slots) --c;
-  return c;
+// Cuts of the (batch, tile) sequence into at most k non-empty ranges
+// minimising the largest range cost (binary search on the cap; the greedy
+// fill is optimal for a given cap). Returns the number of ranges.
+int64_t balanced_cuts(int64_t bs, int64_t tpb, int64_t k, int64_t* cut) {
+  const int64_t seg = switch_cost(), total = bs * tpb;
+  int64_t lo = (total + k - 1) / k, hi = total + seg * bs;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (greedy_cuts(bs, tpb, seg, mid, k, nullptr) <= k) hi = mid;
+    else lo = mid + 1;
+  }
+  return greedy_cuts(bs, tpb, seg, lo, k, cut);
+}
+
+// Largest number of ranges a batch is cut into (the plan's partial slots).
+int64_t slots_of(const int64_t* cut, int64_t clusters, int64_t bs, int64_t tpb) {
+  int64_t n = 1;
+  for (int64_t b = 0; b < bs; ++b)
+    n = std::max<int64_t>(n, cluster_of_tile(cut, static_cast<int>(clusters), (b + 1) * tpb - 1) -
+                                 cluster_of_tile(cut, static_cast<int>(clusters), b * tpb) + 1);
+  return n;
+}
+
+// The balanced cuts over the most CTA pairs (<= one per SM pair, <= one per
+// tile) that cut no batch into more than max_slots ranges (the plan's slots:
+// a host-path chunk of few batches must not need more than the whole grid).
+int64_t pick_cuts(int64_t bs, int64_t tpb, int64_t max_slots, int64_t* cut) {
+  for (int64_t k = std::min<int64_t>(kMaxClusters, bs * tpb);; --k) {
+    const int64_t n = balanced_cuts(bs, tpb, k, cut);
+    if (k == 1 || slots_of(cut, n, bs, tpb) <= max_slots) return n;
+  }
 }
 }  // namespace
 
@@ -650,7 +750,9 @@ int64_t pick_clusters(int64_t bs, int64_t tpb, int64_t max_slots) {
 int64_t mla_pick_splits(int64_t bs, int64_t skv, int64_t segments) {
   (void)segments;
   const int64_t tpb = skv / TK;
-  return slots_needed(bs, tpb, std::min(kMaxClusters, bs * tpb));
+  int64_t cut[kMaxClusters + 1];
+  const int64_t n = pick_cuts(bs, tpb, INT64_MAX, cut);
+  return slots_of(cut, n, bs, tpb);
 }
 
 cudaError_t launch_mla_decode(const MlaArgs& a, cudaStream_t st) {
@@ -664,13 +766,11 @@ cudaError_t launch_mla_decode(const MlaArgs& a, cudaStream_t st) {
       !make_tmap(&tv, a.kv, 2, kdims, strides, vbox, 2))
     return cudaErrorInvalidValue;
   const int64_t tpb = a.skv / TK;
-  const int64_t clusters = pick_clusters(a.bs, tpb, a.nslices);
   Params p{};
+  const int64_t clusters = pick_cuts(a.bs, tpb, a.nslices, p.cut);
   p.skv = a.skv;
   p.rows_total = a.rows_total;
   p.tpb = static_cast<int>(tpb);
-  p.total = a.bs * (tpb + kSegCost);  // cost units
-  p.fast32 = (p.total + 1) * clusters < (int64_t{1} << 32);
   p.clusters = static_cast<int>(clusters);
   p.nslots = static_cast<int>(a.nslices);
   p.scale = a.scale;
@@ -680,25 +780,23 @@ cudaError_t launch_mla_decode(const MlaArgs& a, cudaStream_t st) {
   p.part_m = a.part_m;
   p.part_l = a.part_l;
   p.part_o = a.part_o;
+  p.cnt = a.cnt;
   const size_t smem = sizeof(Smem);
   static_assert(sizeof(Smem) <= 227 * 1024, "fits the opt-in shared memory of one CTA");
   cudaError_t e = cudaFuncSetAttribute(mla_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  dim3 grid(2, static_cast<unsigned>(clusters), 1);
-  mla_decode_kernel<<<grid, NT, smem, st>>>(tq, tk, tv, p);
-  e = cudaGetLastError();
-  if (e != cudaSuccess || a.nslices == 1) return e;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(a.bs * (HN / FR)));
-  cfg.blockDim = dim3(256);
+  cfg.gridDim = dim3(2, static_cast<unsigned>(clusters), 1);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].id = cudaLaunchAttributeCooperative;  // the in-kernel fold waits on other pairs
+  attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, mla_fold_kernel, p);
+  cfg.numAttrs = a.nslices > 1 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, mla_decode_kernel, tq, tk, tv, p);
 }
 
 }  // namespace rf

@@ -36,6 +36,7 @@ struct rf_plan {
   float* ws_m = nullptr;
   float* ws_l = nullptr;
   float* ws_o = nullptr;
+  unsigned long long* ws_cnt = nullptr;  // arrival counters (MLA decode's in-kernel fold)
   int* domain_flag = nullptr;
   // Host-path staging (rf_run_host), allocated on first use.
   bool staged = false;
@@ -174,7 +175,7 @@ const char* kernel_name(rf::Kernel k) {
     case rf::Kernel::LayerNormGemmSm100: return "layernorm_gemm_sm100 (bf16 tcgen05 cta_group::2)";
     case rf::Kernel::RowStats: return "rowstats (SIMT HBM streaming, fp64 accumulation)";
     case rf::Kernel::MoeRouter: return "moe_router (tcgen05 split-K router GEMM + L2 split exchange + routing cascade, one launch)";
-    case rf::Kernel::MlaDecode: return "mla_decode (tcgen05, 128 heads x latent cache, split-KV)";
+    case rf::Kernel::MlaDecode: return "mla_decode (tcgen05, 128 heads x latent cache, split-KV folded in-kernel)";
     case rf::Kernel::FusedRows: return "fused_rows (run_fused: warp-buffered level-1 segments, SIMT)";
   }
   return "?";
@@ -322,10 +323,11 @@ rf_status run_range(const rf_plan* p, const rf_io* io, int64_t u0, int64_t nu, c
       a.nslices = p->nsplit;
       a.rows_total = p->rows_total;
       a.scale = static_cast<float>(d.softmax_scale);
-      if (p->nsplit > 1) {  // segment partials, folded by mla_fold_kernel (PDL)
+      if (p->nsplit > 1) {  // segment partials, folded inside the kernel (arrival counters per batch half)
         a.part_m = p->ws_m + u0 * hn;
         a.part_l = p->ws_l + u0 * hn;
         a.part_o = p->ws_o + u0 * hn * d.free_len;
+        a.cnt = p->ws_cnt + 2 * u0;
       }
       cudaError_t e = rf::launch_mla_decode(a, st);
       if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("mla launch: ") + cudaGetErrorString(e));
@@ -636,8 +638,8 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
       return bail(RF_ERR_UNSUPPORTED, "unknown pattern");
   }
   if (is_gemm(p->d.pattern) && p->d.pattern != RF_PATTERN_MOE_ROUTER) p->nsplit = p->d.segments;
-  p->launches = (((p->d.pattern == RF_PATTERN_ATTENTION || p->d.pattern == RF_PATTERN_MLA_DECODE) &&
-                  p->nsplit > 1 && p->kernel != rf::Kernel::AttentionTf32) ||
+  p->launches = ((p->d.pattern == RF_PATTERN_ATTENTION && p->nsplit > 1 &&
+                  p->kernel != rf::Kernel::AttentionTf32) ||
                  (is_gemm(p->d.pattern) && p->d.pattern != RF_PATTERN_MOE_ROUTER && p->nsplit > 1)) ? 2 : 1;
 
   // ---- persistent workspace ----
@@ -650,6 +652,11 @@ rf_status rf_plan_create(const rf_desc* desc, rf_plan** out) {
         cudaMalloc(&p->ws_l, n * sizeof(float)) != cudaSuccess ||
         cudaMalloc(&p->ws_o, n * p->d.free_len * sizeof(float)) != cudaSuccess)
       return bail(RF_ERR_CUDA, "segment workspace allocation failed");
+    if (p->d.pattern == RF_PATTERN_MLA_DECODE) {  // two counters per batch (one per CTA of the pair)
+      const size_t nc = static_cast<size_t>(2 * p->d.batch) * sizeof(unsigned long long);
+      if (cudaMalloc(&p->ws_cnt, nc) != cudaSuccess || cudaMemset(p->ws_cnt, 0, nc) != cudaSuccess)
+        return bail(RF_ERR_CUDA, "segment workspace allocation failed");
+    }
   }
   if (is_gemm(p->d.pattern) && p->d.pattern != RF_PATTERN_MOE_ROUTER && p->nsplit > 1) {
     // Multi-Segment GEMM: [S, M, N] f32 slice accumulators + [S, M] statistics
@@ -685,6 +692,7 @@ void rf_plan_destroy(rf_plan* p) {
   cudaFree(p->ws_m);
   cudaFree(p->ws_l);
   cudaFree(p->ws_o);
+  cudaFree(p->ws_cnt);
   cudaFree(p->domain_flag);
   for (void* b : p->dev_in) cudaFree(b);
   for (void* b : p->dev_out) cudaFree(b);

@@ -72,6 +72,7 @@ struct MlaArgs {
   float* part_m;    // [nslices, rows_total] (nslices > 1)
   float* part_l;
   float* part_o;    // [nslices, rows_total, 512]
+  unsigned long long* cnt;  // [bs, 2] arrival counters (zeroed at plan creation; multiples of 128 between launches)
   int64_t bs, skv, nslices, rows_total;
   float scale;
 };

@@ -123,7 +123,8 @@ def routing():
 
 
 def router():
-    T, hd, E = 256, 512, 64
+    """2 row tiles x 2 K splits: the split CTAs exchange partials through L2 (arrival counter)."""
+    T, hd, E = 256, 1024, 64
     p = moe_router_plan(T, hd, E, 4)
     w = _w(hd, E) / hd ** 0.5
     wp = p.pack_weight(w)
@@ -133,6 +134,7 @@ def router():
 
 
 def mla():
+    """One batch over 4 CTA pairs: the in-kernel fold of the cut batch (arrival counters)."""
     q = ((torch.rand(1, 128, 576, device="cuda") * 2 - 1)).bfloat16()
     kv = (torch.rand(1, 512, 576, device="cuda") * 2 - 1).bfloat16()
     m, l, o = mla_decode(q, kv, segments=2, softmax_scale=576 ** -0.5)

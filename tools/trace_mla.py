@@ -1,6 +1,6 @@
 """Timeline of the first and last CTA pair of mla_decode (cfg8 shape) from a
 build with -DRF_MLA_TRACE. Usage (GPU box):
-  python tools/trace_mla.py <traced librf_cuda.so>
+  python tools/trace_mla.py <traced librf_cuda.so> [noflush]
 Columns per tile, microseconds from the kernel's first stamp:
   K0 / K8: first / last K stage load issued, V0: first V stage issued,
   S: S MMAs issued (all K stages landed), Pin: P ready (MMA warp), PV: P V issued,
@@ -22,8 +22,10 @@ B, SKV = 32, 4096
 q = (torch.rand(B, 128, 576, device="cuda") * 2 - 1).bfloat16()
 kv = (torch.rand(B, SKV, 576, device="cuda") * 2 - 1).bfloat16()
 flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+NOFLUSH = "noflush" in sys.argv[2:]  # the bench does not flush for cfg8 (160 MB of inputs > L2)
 for _ in range(3):
-    flush.fill_(1)
+    if not NOFLUSH:
+        flush.fill_(1)
     mla_decode(q, kv, segments=4, softmax_scale=576 ** -0.5)
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * (2 * 2 * 64 * 8))()
@@ -50,14 +52,14 @@ for c in range(2):
 fb = (ctypes.c_ulonglong * (1024 * 3))()
 if hasattr(lib, "rf_mla_fold_trace_read") and lib.rf_mla_fold_trace_read(fb) == 0:
     f = list(fb)
-    n = B * 16
+    n = 148  # in-kernel fold: one entry per decode CTA (y * 2 + x) that folded a cut batch
     st = sorted(us(f[3 * i]) for i in range(n) if f[3 * i])
     go = sorted(us(f[3 * i + 1]) for i in range(n) if f[3 * i + 1])
     en = sorted(us(f[3 * i + 2]) for i in range(n) if f[3 * i + 2])
     q = lambda v: [v[0], v[len(v) // 4], v[len(v) // 2], v[3 * len(v) // 4], v[-1]] if v else None  # noqa: E731
-    print("fold CTAs: resident at (min/q1/med/q3/max)", q(st))
-    print("           batch ready", q(go))
-    print("           done       ", q(en))
+    print("fold (in-kernel): started (min/q1/med/q3/max)", q(st))
+    print("                  counter met", q(go))
+    print("                  done       ", q(en))
 
 eb = (ctypes.c_ulonglong * 256)()
 if hasattr(lib, "rf_mla_end_trace_read") and lib.rf_mla_end_trace_read(eb) == 0:
