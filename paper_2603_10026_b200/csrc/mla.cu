@@ -167,7 +167,14 @@ __host__ __device__ __forceinline__ int cluster_of_tile(const int64_t* cut, int 
 struct Segment {
   int b, t0, t1, slot, nseg;  // nseg: segments (ranges) the batch is cut into
 };
-// Segment `i` of pair k's range; false when the range is exhausted.
+__device__ __forceinline__ void segment_slots(const Params& p, int k, Segment& sg) {
+  const int64_t b = sg.b;
+  const int k0 = cluster_of_tile(p.cut, p.clusters, b * p.tpb);
+  sg.slot = k - k0;
+  sg.nseg = cluster_of_tile(p.cut, p.clusters, (b + 1) * p.tpb - 1) - k0 + 1;
+}
+// Segment `i` of pair k's range (batch and tiles; slot / nseg by
+// segment_slots, which only the epilogue needs); false when exhausted.
 __device__ __forceinline__ bool segment(const Params& p, int k, int i, Segment& sg) {
   const int64_t x1 = p.cut[k + 1];
   int64_t x = p.cut[k];
@@ -178,9 +185,6 @@ __device__ __forceinline__ bool segment(const Params& p, int k, int i, Segment& 
       sg.b = static_cast<int>(b);
       sg.t0 = static_cast<int>(x - b * p.tpb);
       sg.t1 = static_cast<int>(hi - b * p.tpb);
-      const int k0 = cluster_of_tile(p.cut, p.clusters, b * p.tpb);
-      sg.slot = k - k0;
-      sg.nseg = cluster_of_tile(p.cut, p.clusters, (b + 1) * p.tpb - 1) - k0 + 1;
       return true;
     }
     x = hi;
@@ -302,31 +306,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   const int k = blockIdx.y;  // this pair's range of (batch, tile)
   if (threadIdx.x == 0) MT_STAMP(63, 0);
 
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
     // full barriers: the leader's copy is armed with both CTAs' bytes and
-    // completed by both CTAs' 2-SM TMA loads (the peer's copies are unused)
-    mbar_init(&s.q_full, 1);
-    mbar_init(&s.q_empty, 1);
-    for (int i = 0; i < NKR; ++i) {
+    // completed by both CTAs' 2-SM TMA loads (the peer's copies are unused).
+    // One lane per ring slot: ~40 serial inits took ~0.7 us of the start.
+    const int i = threadIdx.x;
+    if (i < NKR) {
       mbar_init(&s.kfull[i], 1);
       mbar_init(&s.kempty[i], 1);
     }
-    for (int i = 0; i < NVR; ++i) {
+    if (i < NVR) {
       mbar_init(&s.vfull[i], 1);
       mbar_init(&s.vempty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    if (i < 2) {
       mbar_init(&s.s_full[i], 1);
       mbar_init(&s.p_full[i], 8);  // 4 softmax warps of each CTA (the leader's copy is used)
       mbar_init(&s.pv_done[i], 1);
     }
-    mbar_init(&s.o_full, 1);
-    mbar_init(&s.o_empty, 8);  // both CTAs' epilogues have drained their O
+    if (i == 31) {
+      mbar_init(&s.q_full, 1);
+      mbar_init(&s.q_empty, 1);
+      mbar_init(&s.o_full, 1);
+      mbar_init(&s.o_empty, 8);  // both CTAs' epilogues have drained their O
+      s.nfold = 0;
+    }
     fence_barrier_init();
-    s.nfold = 0;
+    if (i == 0) MT_STAMP(63, 6);
   }
   unsigned long long fold_old[2] = {0, 0};  // thread 0: the counters before its arrivals
   if (warp == 5) tmem_alloc_2sm<512>(&s.tmem_base);
+  if (threadIdx.x == 160) MT_STAMP(63, 7);
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
@@ -340,8 +350,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     // ------------------------------------------------------ TMA: Q, K ----
     // 2-SM loads: bytes land in this CTA, completion on the leader's barrier
     if (elect_one()) {
+      MT_STAMP(63, 4);
       prefetch_tmap(&tq);
       prefetch_tmap(&tk);
+      MT_STAMP(63, 5);
       int g = 0, nq = 0, gt = 0, qb = -1;
       for (int si = 0; segment(p, k, si, sg); ++si) {
         if (sg.b != qb) {  // a new batch: its Q once the previous batch's S MMAs are done
@@ -551,6 +563,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       named_bar_sync(1, 128);  // xm is free for the next segment
       const float l_true = l_ref * ex2_mufu((m_ref - m_true) * kLog2e);
       const int64_t grow = static_cast<int64_t>(sg.b) * HN + h * HC + row;
+      segment_slots(p, k, sg);
       const bool direct = sg.nseg == 1;  // the whole batch is this segment: final outputs
       if (half == 0) {
         if (direct) {

@@ -42,7 +42,9 @@ us = lambda v: round((v - t0) / 1000, 2) if v else None  # noqa: E731
 for c in range(2):
     print(f"cluster {'first' if c == 0 else 'last'}: start {us(at(c, 0, 63, 0))} / {us(at(c, 1, 63, 0))}"
           f"  end {us(at(c, 0, 63, 1))} / {us(at(c, 1, 63, 1))}  setup done {us(at(c, 0, 63, 2))}"
-          f"  first Q issue {us(at(c, 0, 63, 3))}")
+          f"  (barriers {us(at(c, 0, 63, 6))}, TMEM allocated {us(at(c, 0, 63, 7))})"
+          f"  first Q issue {us(at(c, 0, 63, 3))}  (TMA warp: elected {us(at(c, 0, 63, 4))},"
+          f" tensor maps prefetched {us(at(c, 0, 63, 5))})")
     print(" tile |   K0    K8    V0 |    S    Pin    PV | Srdy0  Prel0 | Srdy1  Prel1")
     for i in range(16):
         print(f" {i:4d} | {us(at(c, 0, i, 0))} {us(at(c, 0, i, 7))} {us(at(c, 0, i, 1))} | "
