@@ -108,12 +108,12 @@ __global__ void __launch_bounds__(NT, 1)
   const int kt = k_tiles_per_split;
   if (threadIdx.x == 0) RT_STAMP(0);
 
-  if (warp == 0) {  // one lane per ring slot (serial inits cost ~30 cycles each)
-    if (lane < STAGES) {
-      mbar_init(&s.full[lane], 1);
-      mbar_init(&s.empty[lane], 1);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&s.full[i], 1);
+      mbar_init(&s.empty[i], 1);
     }
-    if (lane == 31) mbar_init(&s.acc_full, 1);
+    mbar_init(&s.acc_full, 1);
     fence_barrier_init();
   }
   if (warp == 5) tmem_alloc<kCols>(&s.tmem_base);
