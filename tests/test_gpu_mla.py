@@ -74,3 +74,38 @@ def test_mla_decode_host_path_and_errors():
     with pytest.raises(UnsupportedPattern):
         Plan(Desc(N.RF_PATTERN_MLA_DECODE, "bf16", rows=1, len=1000, free_len=512, batch=1, heads=128,
                   producer_len=576))
+
+
+def test_mla_decode_counters_across_launches():
+    """The in-kernel fold's arrival counters (plan workspace, never reset): many launches of one plan,
+    device runs interleaved with host-path runs (chunked: other batch offsets and cut patterns), give
+    bit-identical outputs every time (the fold order is fixed; a stale or early counter would not)."""
+    import torch
+    from paper_2603_10026_b200 import Desc, Plan
+    from paper_2603_10026_b200 import _native as N
+
+    B, skv = 5, 1024  # 40 tiles over 40 CTA pairs: every batch is cut into 8 segments
+    g = torch.Generator().manual_seed(11)
+    q = (torch.rand(B, 128, 576, generator=g) * 2 - 1).bfloat16()
+    kv = (torch.rand(B, skv, 576, generator=g) * 2 - 1).bfloat16()
+    desc = Desc(N.RF_PATTERN_MLA_DECODE, "bf16", rows=1, len=skv, free_len=512, batch=B, heads=128,
+                softmax_scale=576 ** -0.5, producer_len=576)
+    p = Plan(desc)
+    assert p.launches_per_run == 1
+    qd, kvd = q.cuda(), kv.cuda()
+    outs = [torch.empty(B, 128, device="cuda"), torch.empty(B, 128, device="cuda"),
+            torch.empty(B, 128, 512, dtype=torch.bfloat16, device="cuda")]
+    p.run([qd, kvd], outs)
+    ref = [t.clone() for t in outs]
+    hm, hl = torch.empty(B, 128).pin_memory(), torch.empty(B, 128).pin_memory()
+    ho = torch.empty(B, 128, 512, dtype=torch.bfloat16).pin_memory()
+    for i in range(40):
+        for t in outs:
+            t.zero_()
+        p.run([qd, kvd], outs)
+        for t, r in zip(outs, ref):
+            assert torch.equal(t, r), i
+        if i % 8 == 0:
+            p.run_host([q.pin_memory(), kv.pin_memory()], [hm, hl, ho])
+            torch.cuda.synchronize()
+            assert O.scaled_max_err(ho.double().numpy().ravel(), ref[2].double().cpu().numpy().ravel())[0] <= 2e-2

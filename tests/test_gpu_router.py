@@ -100,3 +100,32 @@ def test_router_unsupported_shapes():
         moe_router_plan(128, 128, 48, 2)  # experts
     with pytest.raises(UnsupportedPattern):
         moe_router_plan(128, 128, 64, 9)  # K' > 8
+
+
+def test_router_counters_across_launches():
+    """The split exchange's arrival counters (plan workspace, never reset): repeated device runs of one
+    plan interleaved with host-path runs (16 chunks: other row-tile counters, one row tile per launch)
+    give bit-identical scores and routes every time."""
+    import torch
+    from paper_2603_10026_b200 import moe_router, moe_router_plan
+
+    tokens, hd, experts, k = 2048, 4096, 128, 8  # R8: 16 row tiles x 8 splits
+    g = torch.Generator().manual_seed(5)
+    x = (torch.rand(tokens, hd, generator=g) * 2 - 1).bfloat16()
+    w = (torch.rand(hd, experts, generator=g) * 2 - 1) / hd ** 0.5
+    p = moe_router_plan(tokens, hd, experts, k)
+    assert p.launches_per_run == 1
+    wp = p.pack_weight(w.cuda())
+    xd = x.cuda()
+    ref = moe_router(xd, wp, k, with_scores=True)
+    h1 = torch.empty(tokens).pin_memory()
+    h2 = torch.empty(tokens).pin_memory()
+    hr = torch.empty(tokens, k, 2, dtype=torch.int32).pin_memory()
+    for i in range(40):
+        got = moe_router(xd, wp, k, with_scores=True)
+        for a, b in zip(got, ref):
+            assert torch.equal(a, b), i
+        if i % 8 == 0:
+            p.run_host([x.pin_memory(), wp], [h1, h2, hr, None])
+            torch.cuda.synchronize()
+            assert torch.equal(h1, ref[0].cpu()) and torch.equal(hr[..., 1], ref[3].cpu())
