@@ -14,7 +14,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KERNELS = {0: "attn_tf32_kernel", 1: "attn_sm100_kernel", 2: "attn_decode_kernel",
-           3: "quant_gemm", 4: "rms_gemm", 5: "rms_gemm", 6: "router_gemm", 7: "mla_decode"}
+           3: "quant_gemm", 4: "rms_gemm", 5: "rms_gemm", 6: "router_kernel", 7: "mla_decode"}
 METRICS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
