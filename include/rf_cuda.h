@@ -25,7 +25,9 @@
  *    Plans are immutable after creation (one plan per device). A plan owns its
  *    split workspace and host-path staging, so rf_run / rf_run_host calls on
  *    ONE plan must be ordered (same stream or events); use one plan per
- *    stream for concurrent execution.
+ *    stream for concurrent execution. (The MoE router's and MLA decode's
+ *    kernels also keep arrival counters in the plan workspace; they rely on
+ *    this ordering to tell one launch's arrivals from the next one's.)
  *  - No exceptions cross the boundary. Errors are rf_status codes that the
  *    host layer maps back onto the reference's exception types:
  *      RF_ERR_SHAPE        -> redfuse::ShapeMismatch          (simulator.hpp:17-19)
