@@ -61,7 +61,11 @@ def test_router_paper_shapes(name):
     assert np.all(gap[bad] < 1e-4), gap[bad]
 
 
-@pytest.mark.parametrize("tokens,hd,experts,k", [(1000, 512, 32, 2), (300, 256, 256, 8), (128, 64, 64, 1)])
+@pytest.mark.parametrize("tokens,hd,experts,k", [
+    (1000, 512, 32, 2), (300, 256, 256, 8), (128, 64, 64, 1),
+    # split-K with the L2 exchange on a ragged last row tile (1000 = 7 x 128 + 104; 4 splits), 256 experts
+    # over 8 splits with a 2-token last tile (some split CTAs own no live token), 32 experts
+    (1000, 2048, 64, 4), (130, 4096, 256, 8), (200, 1024, 32, 3)])
 def test_router_ragged_and_expert_counts(tokens, hd, experts, k):
     ref, d1, d2, tv, ti, sc = _run(tokens, hd, experts, k, seed=tokens + hd)
     assert O.scaled_max_err(sc.ravel(), ref.ravel())[0] <= 1e-5
